@@ -1,0 +1,273 @@
+"""bench.py — R-NW Gray-code throughput of the hot path on BASELINE.json configs[1].
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (configs[1]): 256 seeded n=24 matrices, each the sum of 3 disjoint random
+permutation matrices (half 0/1, half with nonzeros uniform in [1,7]); direct batched
+R-NW, no expansion.  One step = the whole hot path on that batch: KKLLL estimates
+(N = n^2 trials) -> improved-Step-3 order (LPT on the estimates) -> persistent R-NW
+kernel over all 256 x 2^23 Gray-code terms in exact multi-prime arithmetic ->
+residues -> host CRT of the 256 exact permanents.
+Metric: Gray-code terms per second (whole job, all ranks).  Under torchrun each rank
+evaluates its own seeded batch of 256 (weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "R-NW Gray-code terms/s (configs[1]: 256 x n=24 3-regular, exact per(A))"
+UNIT = "terms/s"
+N_MATS, ORDER, SEED = 256, 24, 2024
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def int_ops_per_term(n_pad: int, G: int, k: int) -> float:
+    """Algorithmic 32-bit integer lane-ops of one Gray-code term in the kernel's
+    formulation: NP row-sum adds, NP - NP/G exact group multiplies,
+    (NP/G - 1) signed Montgomery products per prime (IMAD.WIDE, IMAD, IMAD.HI, IADD:
+    the two wide/high multiplies occupy the multiply pipe twice as long, counted 2 each
+    => 6 ops), and 2 ops per prime to accumulate."""
+    ng = n_pad // G
+    return n_pad + (n_pad - ng) + (ng - 1) * k * 6 + 2 * k
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1112_6072_b200 as P
+    from workloads import random_3perm_batch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    # each rank: its own seeded batch (rank 0 is exactly configs[1])
+    h_np = random_3perm_batch(N_MATS, ORDER, seed=SEED + rank)
+    h_mats = torch.tensor(h_np, dtype=torch.int32).pin_memory()
+    d_mats = h_mats.to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream()
+    jobs = torch.arange(N_MATS, dtype=torch.int32, device=dev)
+
+    def step(mats):
+        est = P.sperm_estimate(mats, trials=0, seed=1, ids=jobs)
+        _, order, _ = P.sperm_schedule(est.cpu().numpy(), 1, "estimate")
+        d_order = torch.from_numpy(order).to(dev, non_blocking=True)
+        res, k = P.sperm_permanent(mats, order=d_order, min_primes=1)
+        return res, k
+
+    def finish(res, k):
+        r, kk = res.cpu(), k.cpu()  # D2H of the step's result
+        return P.residues_to_ints(r, kk)
+
+    for _ in range(max(args.warmup, 3)):
+        vals = finish(*step(d_mats))
+    # device-timed region: K steps, L2 flushed before each (outside the events)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    P.sperm_timing_enable(True)
+    P.sperm_timing_reset()
+    for i in range(args.steps):
+        flush.fill_(i)
+        ev[i][0].record(stream)
+        res, k = step(d_mats)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    rnw_ms, rnw_launches = P.sperm_timing_get("rnw")
+    kk_ms, kk_launches = P.sperm_timing_get("kklll")
+    P.sperm_timing_enable(False)
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    vals = finish(res, k)
+    # end to end through the public API: pinned H2D of the inputs, the step, D2H of results
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(i)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m = h_mats.to(dev, non_blocking=True)
+        vals = finish(*step(m))
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_total, rnw_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_total, rnw_ms = [float(x) for x in t.cpu()]
+    terms_step = P.sperm_rnw_terms(ORDER, N_MATS) * world
+    value = terms_step * args.steps / (total_ms * 1e-3)
+    e2e_value = terms_step * args.steps / (e2e_total * 1e-3)
+    # roofline of the dominant kernel (rnw_main) on this rank
+    pk, pk_kind = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_ops = nsm * 128 * sm_mhz * 1e6  # 64 fma-pipe + 64 alu-pipe lane-ops / clk / SM
+    half = N_MATS // 2
+    ops_step = (half * int_ops_per_term(24, 8, 2) + half * int_ops_per_term(24, 4, 4)) * 2 ** (ORDER - 1)
+    rnw_avg_s = (rnw_ms / max(rnw_launches, 1)) * 1e-3
+    achieved = ops_step / rnw_avg_s
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32 (exact mod 2^31 primes)", "data": "synthetic",
+        "config": {"workload": "configs[1]: 256 x n=24 sum of 3 disjoint permutation matrices, half 0/1, "
+                               "half weights U[1,7], seed 2024(+rank); KKLLL N=n^2 -> LPT order -> R-NW",
+                   "matrices_per_gpu": N_MATS, "n": ORDER, "terms_per_step_per_gpu": terms_step / world,
+                   "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world} weak"},
+        "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
+                     "frac": achieved / peak_ops, "traffic": None, "kernel": "rnw_main_kernel<24>",
+                     "kernel_ms": rnw_avg_s * 1e3, "kernel_share_of_step": (rnw_ms / args.steps) / (total_ms / args.steps),
+                     "peak_note": f"148 SM x 128 int lane-ops/clk x {sm_mhz:.0f} MHz ({pk_kind} sm_max)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_mats.numel() * 4),
+                "d2h_bytes_per_step": int(N_MATS * (P.KMAX + 1) * 4 + N_MATS * 8)},
+        "gpu_launches": args.steps * 5,
+        "clocks": clocks,
+        "kklll_ms_per_step": kk_ms / max(args.steps, 1),
+        "check": {"per_first": str(vals[0]), "per_last": str(vals[-1])},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(h_np)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(mats, seconds: float = 12.0):
+    """The oracle (oracle/ryser_nw.c, exact multi-limb R-NW, 1 thread) on a bounded
+    sample of the same workload: whole matrices alternately from the 0/1 and the
+    weighted half until ~`seconds` of CPU time."""
+    from oracle.cryser import per_ryser_nw_c
+    t0 = time.perf_counter()
+    done = []
+    i = 0
+    while time.perf_counter() - t0 < seconds and i < len(mats):
+        idx = (i // 2) if i % 2 == 0 else len(mats) // 2 + i // 2
+        per_ryser_nw_c(mats[idx])
+        done.append(idx)
+        i += 1
+    dt = time.perf_counter() - t0
+    terms = len(done) * 2 ** (mats.shape[1] - 1)
+    return {"value": terms / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{len(done)} of the 256 configs[1] matrices (alternating 0/1 / weighted), "
+                      f"oracle/ryser_nw.c exact multi-limb R-NW, {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm = the CPU oracle, as it stands, on this arm's config and metric."""
+    if rank != 0:
+        return
+    sys.path.insert(0, ROOT)
+    from workloads import random_3perm_batch
+    from oracle.cryser import build_oracle_c, per_ryser_nw_c
+    build_oracle_c()
+    mats = random_3perm_batch(N_MATS, ORDER, seed=SEED)
+    per_step = 2  # bounded sample per step: one 0/1 and one weighted matrix (~2 s)
+    times = []
+    for s in range(max(args.warmup, 3) + args.steps):
+        t0 = time.perf_counter()
+        for i in range(per_step):
+            idx = (s % (N_MATS // 2)) + (N_MATS // 2) * (i % 2)
+            per_ryser_nw_c(mats[idx])
+        if s >= max(args.warmup, 3):
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    terms = per_step * 2 ** (ORDER - 1) * args.steps
+    v = terms / tot
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "exact multi-limb int (CPU)", "data": "synthetic",
+        "config": {"workload": "configs[1] (same batch, seed 2024); each step a bounded sample of 2 matrices"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{per_step} matrices per step (one 0/1, one weighted), oracle/ryser_nw.c"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/* sperm.h — C ABI of libsperm.so, the B200 (sm_100a) hot path of the
+ * parallel hybrid algorithm for exact sparse permanents.
+ *
+ * Paper: Wang, Liang, Bai, Huo, "A load balancing strategy for parallel
+ * computation of sparse permanents" (arXiv 1112.6072), cited as PAPER.md:<line>.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Matrices are square, DENSE, int32, row-major, stored back to back:
+ *    mats[m*n*n + i*n + j] = a_ij of matrix m.  All matrices of one call have
+ *    the same order n (the BFS levels of Algorithm PH, have
+ *    a single order per level).
+ *  - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA
+ *    tensors); h_* are HOST pointers.  The library never frees caller memory;
+ *    internal temporaries are stream-ordered (cudaMallocAsync) and released
+ *    before the call returns or in stream order.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls are asynchronous with respect to the host unless stated otherwise.
+ *  - Return value: SPERM_OK (0) or a negative SPERM_ERR_* code; the message
+ *    of the last error on the calling thread is sperm_last_error().
+ *  - Exact results are produced as residues modulo the primes of
+ *    sperm_prime(): p_0 > p_1 > ... all in (2^30, 2^31).  A value x with
+ *    |x| < (p_0 ... p_{k-1}) / 2 is recovered by sperm_crt().
+ */
+#ifndef SPERM_H_
+#define SPERM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPERM_KMAX 8     /* maximal number of CRT primes per value        */
+#define SPERM_NMAX 48    /* maximal order of an R-NW leaf (2^47 terms)    */
+#define SPERM_EXPAND_NMAX 128 /* maximal order of an expanded node        */
+
+enum {
+  SPERM_OK = 0,
+  SPERM_ERR_ARG = -1,       /* invalid argument (size, NULL pointer, n > max)   */
+  SPERM_ERR_CUDA = -2,      /* a CUDA runtime call or a kernel launch failed    */
+  SPERM_ERR_RANGE = -3,     /* entries too large for exact int32 evaluation     */
+  SPERM_ERR_CAPACITY = -4,  /* output buffer too small; see the *_needed output */
+  SPERM_ERR_PRIMES = -5     /* bound needs more than SPERM_KMAX primes          */
+};
+
+/* ---------------------------------------------------------------- utility */
+int sperm_version(void);
+const char* sperm_last_error(void);
+
+/* The i-th CRT prime (0 <= i < SPERM_KMAX), or 0 if i is out of range. */
+uint32_t sperm_prime(int i);
+
+/* Chinese remaindering (host, synchronous).  residues[q] is x mod p_q for
+ * q < k.  Writes the unique x with -M/2 < x <= M/2, M = p_0 ... p_{k-1}, as a
+ * sign (-1, 0, +1) and a magnitude of `limbs` little-endian uint32 words
+ * (limbs >= k+1 suffices).  Garner's algorithm. */
+int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int* h_sign);
+
+/* ---------------------------------------------------------------- R-NW */
+/* sperm_permanent — batched exact permanents of the leaves of Algorithm
+ * H_per ("return by R-NW(A)"), by Ryser's formula with the
+ * Nijenhuis-Wilf refinement in binary-reflected Gray-code order (R-NW,
+ * PAPER.md:61-65), evaluated in exact arithmetic modulo k primes:
+ *
+ *   per(A) = (-1)^(n-1) 2^(1-n) sum_{t=0}^{2^(n-1)-1} (-1)^t prod_i w_i(g(t)),
+ *   w_i(S) = 2 a_{i,n-1} - sum_j a_ij + 2 sum_{j in S} a_ij,   g(t) = t ^ (t>>1).
+ *
+ *  d_mats     [count][n][n] int32 leaves (device), 0 <= n <= SPERM_NMAX.
+ *  d_coef     [count] int64 leaf coefficients (device) or NULL (all 1): the
+ *             leaf contributes coef * per(leaf) (the scalars Eq. (2),
+ *             PAPER.md:105-112, leaves on its children).
+ *  d_order    [count] int32 evaluation order (device) or NULL (natural order):
+ *             the persistent kernel's work queue hands out the leaves in this
+ *             order (improved Step 3: non-increasing
+ *             estimate).  Must be a permutation of 0..count-1.
+ *  d_job      [count] int32 job id of each leaf (device) or NULL (every leaf
+ *             belongs to job 0, so d_job_acc[0] accumulates the total).
+ *  num_jobs   size of d_job_acc's first dimension (>= 1 when d_job_acc is set).
+ *  min_primes every leaf uses at least this many primes (so that sums over
+ *             leaves can be reconstructed); each leaf also uses as many as
+ *             its own bound  |coef| * min(prod_i sum_j |a_ij|, prod_j sum_i |a_ij|)
+ *             requires.  1 <= min_primes <= SPERM_KMAX.
+ *  d_leaf_res [count][SPERM_KMAX] uint32 out (device) or NULL:
+ *             coef * per(leaf) mod p_q for q < d_leaf_k[m], 0 beyond.
+ *  d_leaf_k   [count] int32 out (device) or NULL: primes used per leaf.
+ *  d_job_acc  [num_jobs + 1][SPERM_KMAX] uint64 in/out (device) or NULL: the
+ *             leaf residues (each < 2^31) are ADDED to the accumulator of their
+ *             job and to the last row (the total, Algorithm PH Step 4,
+ *             PAPER.md:179), so sums over many calls, GPUs (an NCCL sum) and
+ *             leaves stay exact below 2^64; reduce mod p_q before sperm_crt.
+ *             With d_job NULL only row 0 is used (it is the total).
+ *  stream     cudaStream_t.
+ * Errors: SPERM_ERR_ARG (n > SPERM_NMAX, count < 0), SPERM_ERR_RANGE (some
+ * row or column abs sum >= 2^30), SPERM_ERR_PRIMES.  RANGE/PRIMES are
+ * detected on the device and reported synchronously (the call synchronizes
+ * `stream` once after the bound pass). */
+int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* d_coef,
+                    const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
+                    int min_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
+                    uint64_t* d_job_acc, void* stream);
+
+/* Number of Gray-code terms sperm_permanent evaluates for `count` leaves of
+ * order n: count * 2^(n-1) (as double; exact for n <= 53). */
+double sperm_rnw_terms(int n, int64_t count);
+
+/* Reduce accumulators mod the primes: out[r][q] = acc[r][q] mod p_q (device). */
+int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d_out, void* stream);
+
+/* ---------------------------------------------------------------- expansion */
+/* sperm_expand — one breadth-first level of Algorithm PH Step 2
+ * (PAPER.md:161-174): every node (coef, A) of order n is split by Eq. (2)
+ * on the line with the minimal number of nonzeros s
+ * (Algorithm H_per Step 1), into its children of order n-1:
+ *   s = 1: the single child  a * minor(pivot row, p0);
+ *   s = 2: A1 = merge of p0,p1: column p0 := a*col(p1) + b*col(p0), column p1
+ *          and the pivot row deleted (A2 has a zero column);
+ *   s = 3: A1 as above, plus c * minor(pivot row, p2);
+ *   s = 4: A1 and A2 = the same merge of p2,p3 with scalars c,d;
+ * with p0 < p1 < p2 < p3 the pivot line's nonzero positions and a,b,c,d their
+ * values.  Pivot tie-break: rows before columns, lowest index; a column pivot
+ * acts on the transpose (reading R2).  Children with a zero row or
+ * column are dropped (per = 0).  Nodes with s >= 5 are not split; they are
+ * copied unchanged (order n) to the `early` outputs.  Nodes with s = 0 vanish.
+ * Children are written in natural order (parents in order, A1 before A2) —
+ * stable, so the job list equals the oracle's.
+ *
+ *  d_in_mats/coef/job  [count] nodes of order n (device).  d_in_job may be
+ *                      NULL: the node index is used as its job id.
+ *  d_out_mats/coef/job [cap_out] children of order n-1 (device).
+ *  d_early_*           [cap_early] unsplit nodes of order n (device; may be
+ *                      NULL when cap_early == 0).
+ *  h_out_count, h_early_count  host outputs: numbers written (or needed).
+ * Synchronous w.r.t. the host (the counts are read back).  Returns
+ * SPERM_ERR_CAPACITY if a capacity is too small (counts still report the
+ * needed sizes), SPERM_ERR_RANGE if a merged entry or coefficient overflows. */
+int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job,
+                 int n, int64_t count,
+                 int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job, int64_t cap_out,
+                 int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
+                 int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
+
+/* ---------------------------------------------------------------- estimator */
+/* sperm_estimate — Algorithm KKLLL on the 0/1 pattern of
+ * each matrix: B_ij = 0 where a_ij = 0, else an
+ * independent uniform cube root of unity; X = det(B) conj(det(B)); the
+ * estimate is the mean of `trials` X's (0 -> n^2).  Theorem 1
+ * (PAPER.md:218-220): E[X] = per(pattern).  Randomness is the counter-based
+ * generator of DESIGN.md reading K1 keyed by (seed, d_ids[m] or m, trial, i, j);
+ * det by complex LU with partial pivoting in IEEE fp64 without contraction
+ * (reading K2), so estimates are reproducible bit for bit.
+ *  d_mats    [count][n][n] int32 (device); d_ids [count] int32 or NULL.
+ *  d_est     [count] double out (device).
+ *  d_trials_out [count][trials] double out (device) or NULL: every X.  */
+int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d_ids,
+                   int trials, uint64_t seed, double* d_est, double* d_trials_out,
+                   void* stream);
+
+/* ---------------------------------------------------------------- schedule */
+/* sperm_schedule — the improved Step 3 and LPT
+ * on the host: jobs are ordered by non-increasing weight
+ * (ties: lower job id), then each goes to the currently least-loaded of
+ * `machines` machines (ties: lowest machine id).
+ *  policy 0 = estimate order (weights as given, LPT),
+ *         1 = natural order (list scheduling in index order),
+ *         2 = random order (seeded Fisher-Yates with `seed`),
+ *  h_weights [count] double (host); h_machine [count] int32 out;
+ *  h_order [count] int32 out: the order jobs were dealt in;
+ *  h_loads [machines] double out (planned loads, may be NULL). */
+int sperm_schedule(const double* h_weights, int64_t count, int machines, int policy,
+                   uint64_t seed, int32_t* h_machine, int32_t* h_order, double* h_loads);
+
+/* ---------------------------------------------------------------- timing */
+/* Device-side kernel timing: when enabled, the library records CUDA events
+ * around each launch of its kernels (on the launching stream).
+ * sperm_timing_get synchronizes those events and returns the summed
+ * milliseconds and launch count of kernel `name` ("rnw", "expand",
+ * "kklll", "rnw_prep", "rnw_finalize") since the last reset. */
+void sperm_timing_enable(int on);
+void sperm_timing_reset(void);
+int sperm_timing_get(const char* name, double* h_ms, int64_t* h_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPERM_H_ */

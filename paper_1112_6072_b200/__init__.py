@@ -1,0 +1,13 @@
+"""paper_1112_6072_b200 — B200-native exact sparse permanents (arXiv 1112.6072 hot path).
+
+libsperm.so (csrc/, C ABI in include/sperm.h) holds the sm_100a kernels:
+  sperm_expand    Eq. (2) BFS expansion (Algorithm PH Step 2 / H_per)
+  sperm_estimate  KKLLL approximate permanents (job weights)
+  sperm_schedule  improved Step 3: non-increasing-estimate LPT
+  sperm_permanent batched R-NW Gray-code leaf permanents, exact mod primes
+`sperm` is the thin ctypes binding; `pipeline` sequences the calls (Algorithm PH).
+"""
+from .sperm import (  # noqa: F401
+    KMAX, NMAX, SpermError, lib, primes, residues_to_ints, sperm_crt, sperm_estimate, sperm_expand,
+    sperm_permanent, sperm_prime, sperm_reduce_mod, sperm_rnw_terms, sperm_schedule, sperm_timing_enable,
+    sperm_timing_get, sperm_timing_reset, sperm_version)

@@ -1,0 +1,350 @@
+// expand.cu — one breadth-first level of Algorithm PH Step 2:
+// every node is split by Eq. (2) on its pivot line (Algorithm
+// H_per Step 1) into at most two children of order n-1.
+//
+// One warp per node; lane l holds columns l, l+32, ... of the row being processed, so
+// every global access of a row is coalesced.  Pass 1 (count) builds each child in
+// registers without storing it, to learn whether it survives (no zero line, reading
+// R4); an exclusive scan of the per-node child counts gives every child its output
+// slot in natural order (parents in order, A1 before A2 — stable, reading R6); pass 2
+// (emit) rebuilds and stores.  Both passes run the same device function.
+//
+// A child is described by the lines it deletes and the merge it performs:
+//   row pivot r, merge of p_a,p_b:  delete row r, column p_b; column p_a := al*col(p_b) + be*col(p_a)
+//   row pivot r, cofactor at p:     delete row r, column p;   coef *= a_rp
+//   column pivot c (= row pivot of A^T, reading R2): the same with rows and columns exchanged.
+#include <algorithm>
+
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace sperm {
+namespace {
+
+constexpr int kExpThreads = 256;
+constexpr int kMaxChunks = SPERM_EXPAND_NMAX / 32;  // columns per lane
+
+struct Child {
+  int del_row, del_col;
+  int merge;  // 0 none, 1 column merge (keep col := al*col(del_col) + be*col(keep)), 2 row merge
+  int keep;
+  int32_t al, be;
+  int64_t coef;
+  bool valid;  // false if an entry or the coefficient overflowed
+};
+
+struct Plan {
+  int nkids;  // 0..2 candidate children (before the zero-line test)
+  int early;  // 1: s >= 5, node kept unsplit
+  Child kid[2];
+};
+
+__device__ __forceinline__ int32_t ld(const int32_t* a, int n, int i, int j) { return a[i * n + j]; }
+
+// Pivot selection and the Eq. (2) children of one node (warp-uniform result).
+__device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, int lane) {
+  int colcnt[kMaxChunks];
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) colcnt[c] = 0;
+  const int nch = (n + 31) >> 5;
+  int best_row_key = 0x7fffffff;  // (count << 8) | index, min = fewest nonzeros, lowest index
+  for (int i = 0; i < n; ++i) {
+    int rc = 0;
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c) {
+      if (c < nch) {
+        const int j = c * 32 + lane;
+        const bool nz = j < n && ld(a, n, i, j) != 0;
+        colcnt[c] += nz;
+        rc += __popc(__ballot_sync(0xffffffffu, nz));
+      }
+    }
+    best_row_key = min(best_row_key, (rc << 8) | i);
+  }
+  int best_col_key = 0x7fffffff;
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) {
+    const int j = c * 32 + lane;
+    if (c < nch && j < n) best_col_key = min(best_col_key, (colcnt[c] << 8) | j);
+  }
+  for (int o = 16; o; o >>= 1) best_col_key = min(best_col_key, __shfl_xor_sync(0xffffffffu, best_col_key, o));
+  Plan pl;
+  pl.nkids = 0;
+  pl.early = 0;
+  const int srow = best_row_key >> 8, scol = best_col_key >> 8;
+  const bool colpiv = scol < srow;  // rows first; a column only if strictly fewer (R2)
+  const int s = colpiv ? scol : srow;
+  const int idx = colpiv ? (best_col_key & 0xff) : (best_row_key & 0xff);
+  if (s == 0) return pl;
+  if (s >= 5) {
+    pl.early = 1;
+    return pl;
+  }
+  // positions and values of the pivot line's nonzeros, ascending
+  int pos[4];
+  int32_t val[4];
+  int cnt = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int t = c * 32 + lane;
+    int32_t v = 0;
+    if (t < n) v = colpiv ? ld(a, n, t, idx) : ld(a, n, idx, t);
+    unsigned b = __ballot_sync(0xffffffffu, v != 0);
+    while (b) {
+      const int l = __ffs(b) - 1;
+      b &= b - 1;
+      const int32_t vv = __shfl_sync(0xffffffffu, v, l);
+      if (cnt < 4) {
+        pos[cnt] = c * 32 + l;
+        val[cnt] = vv;
+      }
+      ++cnt;
+    }
+  }
+  auto merge_child = [&](int pa, int pb, int32_t al, int32_t be) {
+    Child ch;
+    ch.merge = colpiv ? 2 : 1;
+    ch.del_row = colpiv ? pb : idx;
+    ch.del_col = colpiv ? idx : pb;
+    ch.keep = pa;
+    ch.al = al;
+    ch.be = be;
+    ch.coef = coef;
+    ch.valid = true;
+    return ch;
+  };
+  auto minor_child = [&](int p, int32_t v) {
+    Child ch;
+    ch.merge = 0;
+    ch.del_row = colpiv ? p : idx;
+    ch.del_col = colpiv ? idx : p;
+    ch.keep = -1;
+    ch.al = ch.be = 0;
+    const __int128 r = (__int128)coef * v;
+    ch.valid = r <= (__int128)INT64_MAX && r >= (__int128)INT64_MIN;
+    ch.coef = (int64_t)r;
+    return ch;
+  };
+  if (s == 1) {
+    pl.kid[0] = minor_child(pos[0], val[0]);
+    pl.nkids = 1;
+  } else {
+    pl.kid[0] = merge_child(pos[0], pos[1], val[0], val[1]);
+    pl.nkids = 1;
+    if (s == 3) {
+      pl.kid[1] = minor_child(pos[2], val[2]);
+      pl.nkids = 2;
+    } else if (s == 4) {
+      pl.kid[1] = merge_child(pos[2], pos[3], val[2], val[3]);
+      pl.nkids = 2;
+    }
+  }
+  return pl;
+}
+
+// Builds child `ch` of node `a` row by row; stores it to `out` if WRITE.  Returns
+// 1 if the child has no zero row or column (it survives), 0 otherwise; sets *ovf on
+// an int32 overflow of a merged entry.
+template <bool WRITE>
+__device__ int build_child(const int32_t* __restrict__ a, int n, const Child& ch, int32_t* __restrict__ out,
+                           int lane, bool* ovf) {
+  const int nch = (n + 31) >> 5;
+  const int m = n - 1;
+  bool colnz[kMaxChunks];
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) colnz[c] = false;
+  bool all_rows = true;
+  bool over = false;
+  for (int i = 0; i < n; ++i) {
+    if (i == ch.del_row) continue;
+    const int ii = i - (i > ch.del_row);
+    bool rownz = false;
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c) {
+      if (c < nch) {
+        const int j = c * 32 + lane;
+        int32_t v = j < n ? ld(a, n, i, j) : 0;
+        if (ch.merge == 2 && i == ch.keep) {
+          const int32_t vr = j < n ? ld(a, n, ch.del_row, j) : 0;
+          const long long mv = (long long)ch.al * vr + (long long)ch.be * v;
+          if (mv > INT32_MAX || mv < INT32_MIN) over = true;
+          v = (int32_t)mv;
+        }
+        // column merge: the kept column takes al*a[i][del_col] + be*a[i][keep]
+        if (ch.merge == 1 && j == ch.keep) {
+          const int32_t vd = ld(a, n, i, ch.del_col);
+          const long long mv = (long long)ch.al * vd + (long long)ch.be * v;
+          if (mv > INT32_MAX || mv < INT32_MIN) over = true;
+          v = (int32_t)mv;
+        }
+        const bool keepcol = j < n && j != ch.del_col;
+        if (keepcol && v != 0) {
+          rownz = true;
+          colnz[c] = true;
+        }
+        if (WRITE && keepcol) {
+          const int jj = j - (j > ch.del_col);
+          out[ii * m + jj] = v;
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, rownz)) all_rows = false;
+  }
+  // every kept column must have a nonzero
+  bool cols_ok = true;
+#pragma unroll
+  for (int c = 0; c < kMaxChunks; ++c) {
+    const int j = c * 32 + lane;
+    if (c < nch && j < n && j != ch.del_col && !colnz[c]) cols_ok = false;
+  }
+  cols_ok = __all_sync(0xffffffffu, cols_ok);
+  if (__any_sync(0xffffffffu, over)) *ovf = true;
+  return (all_rows && cols_ok) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
+    const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, int n, int64_t count,
+    int* __restrict__ kid_count, int* __restrict__ early_count, int* __restrict__ kid_mask,
+    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (node >= count) return;
+  const int32_t* a = mats + node * (int64_t)n * n;
+  const int64_t cf = coef ? coef[node] : 1;
+  Plan pl = plan_node(a, n, cf, lane);
+  int kids = 0, mask = 0;
+  bool ovf = false;
+  for (int c = 0; c < pl.nkids; ++c) {
+    if (!pl.kid[c].valid) ovf = true;
+    if (build_child<false>(a, n, pl.kid[c], nullptr, lane, &ovf)) {
+      ++kids;
+      mask |= 1 << c;
+    }
+  }
+  if (lane == 0) {
+    kid_count[node] = kids;
+    kid_mask[node] = mask;
+    early_count[node] = pl.early;
+    if (ovf) atomicOr(err, 1);
+  }
+}
+
+__global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
+    const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, const int32_t* __restrict__ job,
+    int n, int64_t count, const int* __restrict__ kid_mask, const int64_t* __restrict__ kid_off,
+    const int64_t* __restrict__ early_off,
+    int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef, int32_t* __restrict__ out_job,
+    int32_t* __restrict__ early_mats, int64_t* __restrict__ early_coef, int32_t* __restrict__ early_job) {
+  const int lane = threadIdx.x & 31;
+  const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (node >= count) return;
+  const int32_t* a = mats + node * (int64_t)n * n;
+  const int64_t cf = coef ? coef[node] : 1;
+  const int32_t jb = job ? job[node] : (int32_t)node;
+  Plan pl = plan_node(a, n, cf, lane);
+  if (pl.early) {
+    const int64_t o = early_off[node];
+    int32_t* dst = early_mats + o * (int64_t)n * n;
+    for (int e = lane; e < n * n; e += 32) dst[e] = a[e];
+    if (lane == 0) {
+      early_coef[o] = cf;
+      early_job[o] = jb;
+    }
+    return;
+  }
+  int64_t o = kid_off[node];
+  const int64_t m2 = (int64_t)(n - 1) * (n - 1);
+  bool ovf = false;
+  const int mask = kid_mask[node];
+  for (int c = 0; c < pl.nkids; ++c) {
+    if ((mask >> c) & 1) {  // survivors found by the count pass
+      build_child<true>(a, n, pl.kid[c], out_mats + o * m2, lane, &ovf);
+      if (lane == 0) {
+        out_coef[o] = pl.kid[c].coef;
+        out_job[o] = jb;
+      }
+      ++o;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace sperm
+
+using namespace sperm;
+
+extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job, int n,
+                            int64_t count, int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job,
+                            int64_t cap_out, int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
+                            int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!h_out_count || !h_early_count) return set_error(SPERM_ERR_ARG, "sperm_expand: NULL count outputs");
+  *h_out_count = 0;
+  *h_early_count = 0;
+  if (n < 2 || n > SPERM_EXPAND_NMAX) return set_error(SPERM_ERR_ARG, "sperm_expand: n out of range [2, 128]");
+  if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_expand: count < 0");
+  if (count == 0) return SPERM_OK;
+  if (!d_in_mats) return set_error(SPERM_ERR_ARG, "sperm_expand: d_in_mats is NULL");
+  // scratch: kid_count[count] int, early_count[count] int, offsets 2*count int64, err int, totals
+  int* kc = nullptr;
+  SPERM_CUDA(cudaMallocAsync((void**)&kc, sizeof(int) * (3 * count + 4), st));
+  int* ec = kc + count;
+  int* km = kc + 2 * count;
+  int* err = kc + 3 * count;
+  int64_t* off = nullptr;
+  SPERM_CUDA(cudaMallocAsync((void**)&off, sizeof(int64_t) * (2 * count + 2), st));
+  int64_t* eoff = off + count + 1;
+  SPERM_CUDA(cudaMemsetAsync(err, 0, sizeof(int) * 4, st));
+  const unsigned blocks = (unsigned)((count * 32 + kExpThreads - 1) / kExpThreads);
+  int rc = SPERM_OK;
+  auto cleanup = [&]() {
+    cudaFreeAsync(kc, st);
+    cudaFreeAsync(off, st);
+  };
+  {
+    TimingScope ts("expand", st);
+    expand_count_kernel<<<blocks, kExpThreads, 0, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err);
+  }
+  cudaError_t le = cudaGetLastError();
+  if (le != cudaSuccess) { cleanup(); return cuda_check(le, "expand_count_kernel"); }
+  // exclusive scans (count+1 entries: the last one is the total)
+  SPERM_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * (2 * count + 2), st));
+  size_t tmp_bytes = 0, tmp2 = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, kc, off + 1, count, st);
+  cub::DeviceScan::InclusiveSum(nullptr, tmp2, ec, eoff + 1, count, st);
+  tmp_bytes = std::max(tmp_bytes, tmp2);
+  void* tmp = nullptr;
+  SPERM_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, kc, off + 1, count, st);
+  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, ec, eoff + 1, count, st);
+  cudaFreeAsync(tmp, st);
+  int64_t tot[2] = {0, 0};
+  int herr = 0;
+  SPERM_CUDA(cudaMemcpyAsync(&tot[0], off + count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SPERM_CUDA(cudaMemcpyAsync(&tot[1], eoff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SPERM_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  le = cudaStreamSynchronize(st);
+  if (le != cudaSuccess) { cleanup(); return cuda_check(le, "sperm_expand count readback"); }
+  *h_out_count = tot[0];
+  *h_early_count = tot[1];
+  if (herr) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_expand: merged entry or coefficient overflow"); }
+  if (tot[0] > cap_out || tot[1] > cap_early) {
+    cleanup();
+    return set_error(SPERM_ERR_CAPACITY, "sperm_expand: output capacity too small");
+  }
+  if ((tot[0] > 0 && (!d_out_mats || !d_out_coef || !d_out_job)) ||
+      (tot[1] > 0 && (!d_early_mats || !d_early_coef || !d_early_job))) {
+    cleanup();
+    return set_error(SPERM_ERR_ARG, "sperm_expand: NULL output buffer");
+  }
+  {
+    TimingScope ts("expand", st);
+    expand_emit_kernel<<<blocks, kExpThreads, 0, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
+                                                       d_out_mats, d_out_coef, d_out_job, d_early_mats,
+                                                       d_early_coef, d_early_job);
+  }
+  le = cudaGetLastError();
+  cleanup();
+  if (le != cudaSuccess) return cuda_check(le, "expand_emit_kernel");
+  return rc;
+}

@@ -1,0 +1,238 @@
+// host.cu — host-side parts of libsperm.so: errors, primes, CRT (Garner),
+// the improved Step 3 scheduler and the kernel timing registry.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sperm {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  return set_error(SPERM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int sm_count() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
+      cached = 148;
+  }
+  return cached;
+}
+
+// ------------------------------------------------------------------ timing
+namespace {
+struct TimingEntry {
+  double ms = 0.0;
+  int64_t launches = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+std::mutex g_tmu;
+std::map<std::string, TimingEntry> g_timing;
+bool g_timing_on = false;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t get_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+TimingScope::TimingScope(const char* name, cudaStream_t s) : name_(name), s_(s), ev0_(nullptr), ev1_(nullptr) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (!g_timing_on) return;
+  cudaEvent_t e0 = get_event(), e1 = get_event();
+  ev0_ = e0;
+  ev1_ = e1;
+  cudaEventRecord(e0, s);
+}
+
+TimingScope::~TimingScope() {
+  if (!ev0_) return;
+  cudaEventRecord((cudaEvent_t)ev1_, s_);
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing[name_].pending.emplace_back((cudaEvent_t)ev0_, (cudaEvent_t)ev1_);
+}
+
+}  // namespace sperm
+
+using namespace sperm;
+
+extern "C" {
+
+int sperm_version(void) { return 1; }
+
+const char* sperm_last_error(void) { return g_err.c_str(); }
+
+uint32_t sperm_prime(int i) { return (i >= 0 && i < SPERM_KMAX) ? kPrimes[i] : 0u; }
+
+void sperm_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing_on = on != 0;
+}
+
+void sperm_timing_reset(void) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (auto& kv : g_timing) {
+    for (auto& pr : kv.second.pending) {
+      cudaEventSynchronize(pr.second);
+      g_event_pool.push_back(pr.first);
+      g_event_pool.push_back(pr.second);
+    }
+  }
+  g_timing.clear();
+}
+
+int sperm_timing_get(const char* name, double* h_ms, int64_t* h_launches) {
+  if (!name || !h_ms || !h_launches) return set_error(SPERM_ERR_ARG, "sperm_timing_get: NULL argument");
+  std::lock_guard<std::mutex> lk(g_tmu);
+  auto it = g_timing.find(name);
+  if (it == g_timing.end()) {
+    *h_ms = 0.0;
+    *h_launches = 0;
+    return SPERM_OK;
+  }
+  TimingEntry& t = it->second;
+  for (auto& pr : t.pending) {
+    cudaError_t e = cudaEventSynchronize(pr.second);
+    if (e != cudaSuccess) return cuda_check(e, "cudaEventSynchronize");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    t.ms += ms;
+    t.launches += 1;
+    g_event_pool.push_back(pr.first);
+    g_event_pool.push_back(pr.second);
+  }
+  t.pending.clear();
+  *h_ms = t.ms;
+  *h_launches = t.launches;
+  return SPERM_OK;
+}
+
+// ------------------------------------------------------------------ CRT
+// Garner's algorithm: mixed-radix digits v_i with x = v_0 + p_0 (v_1 + p_1 (v_2 + ...)),
+// then x is expanded into base-2^32 limbs; the symmetric representative is taken.
+int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int* h_sign) {
+  if (!h_residues || !h_mag || !h_sign || k < 1 || k > SPERM_KMAX || limbs < k + 1)
+    return set_error(SPERM_ERR_ARG, "sperm_crt: bad arguments");
+  uint64_t v[SPERM_KMAX];
+  for (int i = 0; i < k; ++i) {
+    uint64_t p = kPrimes[i];
+    uint64_t x = h_residues[i] % p;
+    for (int j = 0; j < i; ++j) {
+      // x = (x - v_j) * inverse(p_j) mod p
+      uint64_t pj = kPrimes[j] % p;
+      uint64_t inv = 1, b = pj, e = p - 2;  // Fermat
+      while (e) {
+        if (e & 1) inv = inv * b % p;
+        b = b * b % p;
+        e >>= 1;
+      }
+      x = (x + p - v[j] % p) % p * inv % p;
+    }
+    v[i] = x;
+  }
+  // x = Horner over the mixed radix, in limbs
+  std::vector<uint32_t> X(limbs + 1, 0), M(limbs + 1, 0);
+  auto mul_add = [&](std::vector<uint32_t>& a, uint32_t m, uint32_t add) {
+    uint64_t carry = add;
+    for (size_t t = 0; t < a.size(); ++t) {
+      uint64_t cur = (uint64_t)a[t] * m + carry;
+      a[t] = (uint32_t)cur;
+      carry = cur >> 32;
+    }
+  };
+  X[0] = (uint32_t)v[k - 1];
+  for (int i = k - 2; i >= 0; --i) mul_add(X, kPrimes[i], (uint32_t)v[i]);
+  M[0] = 1;
+  for (int i = 0; i < k; ++i) mul_add(M, kPrimes[i], 0);
+  // compare 2X with M
+  std::vector<uint32_t> X2(X);
+  mul_add(X2, 2, 0);
+  int cmp = 0;
+  for (int t = (int)X2.size() - 1; t >= 0 && cmp == 0; --t)
+    if (X2[t] != M[t]) cmp = X2[t] > M[t] ? 1 : -1;
+  int sign = 1;
+  if (cmp > 0) {  // x - M < 0: magnitude M - X
+    int64_t borrow = 0;
+    for (size_t t = 0; t < X.size(); ++t) {
+      int64_t d = (int64_t)M[t] - X[t] - borrow;
+      borrow = d < 0;
+      X[t] = (uint32_t)(d + (borrow ? (int64_t)1 << 32 : 0));
+    }
+    sign = -1;
+  }
+  bool zero = true;
+  for (int t = 0; t < limbs; ++t) {
+    h_mag[t] = X[t];
+    if (X[t]) zero = false;
+  }
+  if (X[limbs] != 0) return set_error(SPERM_ERR_ARG, "sperm_crt: too few limbs");
+  *h_sign = zero ? 0 : sign;
+  return SPERM_OK;
+}
+
+// ------------------------------------------------------------------ schedule
+// The improved Step 3: order jobs by non-increasing weight and
+// give each to the currently least-loaded machine (LPT); or the
+// natural order of Algorithm PH Step 3; or a seeded random order.
+int sperm_schedule(const double* h_weights, int64_t count, int machines, int policy, uint64_t seed,
+                   int32_t* h_machine, int32_t* h_order, double* h_loads) {
+  if (count < 0 || machines < 1 || (count > 0 && (!h_weights || !h_machine || !h_order)))
+    return set_error(SPERM_ERR_ARG, "sperm_schedule: bad arguments");
+  std::vector<int32_t> order(count);
+  for (int64_t i = 0; i < count; ++i) order[i] = (int32_t)i;
+  if (policy == 0) {
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return h_weights[a] > h_weights[b];  // stable: ties keep the lower job id first
+    });
+  } else if (policy == 2) {
+    uint64_t s = seed;
+    auto next = [&]() {
+      uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return z ^ (z >> 31);
+    };
+    for (int64_t i = count - 1; i > 0; --i) {
+      int64_t j = (int64_t)(next() % (uint64_t)(i + 1));
+      std::swap(order[i], order[j]);
+    }
+  } else if (policy != 1) {
+    return set_error(SPERM_ERR_ARG, "sperm_schedule: unknown policy");
+  }
+  std::vector<double> loads(machines, 0.0);
+  for (int64_t r = 0; r < count; ++r) {
+    int32_t j = order[r];
+    int best = 0;
+    for (int m = 1; m < machines; ++m)
+      if (loads[m] < loads[best]) best = m;
+    h_machine[j] = best;
+    loads[best] += h_weights[j];
+    h_order[r] = j;
+  }
+  if (h_loads)
+    for (int m = 0; m < machines; ++m) h_loads[m] = loads[m];
+  return SPERM_OK;
+}
+
+}  // extern "C"

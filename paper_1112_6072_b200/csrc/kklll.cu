@@ -1,0 +1,157 @@
+// kklll.cu — Algorithm KKLLL: approximate permanents used as the
+// job weights of the improved Step 3.
+//
+// One warp per (job, trial).  B lives in shared memory as two fp64 planes (re, im):
+//   Step 1: B_ij = 0 where a_ij = 0, else the cube root of unity w_r, r = root_index(
+//           trial_key(seed, id, trial), i, j)  (counter-based SplitMix64; K1)
+//   Step 2: X = |det B|^2 by LU with partial pivoting (first maximal |b_ik|^2), every real
+//           operation a single IEEE round-to-nearest fp64 op in a fixed order with no
+//           contraction (__dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn; K2), so the
+//           value equals the reference evaluation bit for bit.
+// The estimate is the trial-order sum of X divided by N (K3).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sperm {
+namespace {
+
+constexpr int kKNmax = 112;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t trial_key(uint64_t seed, uint64_t job, uint64_t trial) {
+  const uint64_t h = mix64(seed + 0x9E3779B97F4A7C15ull * (job + 1));
+  return mix64(h ^ (trial * 0xD1B54A32D192ED03ull));
+}
+__device__ __forceinline__ int root_index(uint64_t key, uint64_t i, uint64_t j) {
+  const uint64_t h = mix64(key ^ ((i << 32) | j));
+  return (int)(((h >> 32) * 3ull) >> 32);
+}
+
+__global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+                                   const int32_t* __restrict__ ids, int trials, uint64_t seed,
+                                   double* __restrict__ xout) {
+  extern __shared__ double ksm[];
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  double* re = ksm + (size_t)(threadIdx.x >> 5) * 2 * n * n;
+  double* im = re + n * n;
+  const double S32 = 0.8660254037844386;  // nearest double to sqrt(3)/2
+  const int64_t items = count * (int64_t)trials;
+  for (int64_t item = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); item < items;
+       item += (int64_t)gridDim.x * wpb) {
+    const int64_t job = item / trials;
+    const int trial = (int)(item % trials);
+    const int32_t* a = mats + job * (int64_t)n * n;
+    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
+    __syncwarp();
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, j = e - (e / n) * n;
+      double r = 0.0, s = 0.0;
+      if (a[e] != 0) {
+        const int ri = root_index(key, (uint64_t)i, (uint64_t)j);
+        r = ri == 0 ? 1.0 : -0.5;
+        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
+      }
+      re[e] = r;
+      im[e] = s;
+    }
+    __syncwarp();
+    double x = 1.0;
+    for (int k = 0; k < n; ++k) {
+      // pivot: first row i >= k with maximal re^2 + im^2
+      double bm = -1.0;
+      int bi = n;
+      for (int i = k + lane; i < n; i += 32) {
+        const double m = __dadd_rn(__dmul_rn(re[i * n + k], re[i * n + k]), __dmul_rn(im[i * n + k], im[i * n + k]));
+        if (m > bm) { bm = m; bi = i; }  // ascending i per lane: strict > keeps the first
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, bm, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (om > bm || (om == bm && oi < bi)) { bm = om; bi = oi; }
+      }
+      const double d = bm;
+      if (d == 0.0) { x = 0.0; break; }
+      if (bi != k) {
+        for (int j = lane; j < n; j += 32) {
+          double t = re[k * n + j]; re[k * n + j] = re[bi * n + j]; re[bi * n + j] = t;
+          t = im[k * n + j]; im[k * n + j] = im[bi * n + j]; im[bi * n + j] = t;
+        }
+        __syncwarp();
+      }
+      x = __dmul_rn(x, d);
+      if (k + 1 == n) break;
+      const double pr = re[k * n + k], pi = im[k * n + k];
+      for (int i = k + 1 + lane; i < n; i += 32) {
+        const double xr = re[i * n + k], xi = im[i * n + k];
+        re[i * n + k] = __ddiv_rn(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d);
+        im[i * n + k] = __ddiv_rn(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d);
+      }
+      __syncwarp();
+      const int w = n - k - 1;
+      for (int e = lane; e < w * w; e += 32) {
+        const int i = k + 1 + e / w, j = k + 1 + (e - (e / w) * w);
+        const double lr = re[i * n + k], li = im[i * n + k];
+        const double ur = re[k * n + j], ui = im[k * n + j];
+        re[i * n + j] = __dsub_rn(re[i * n + j], __dsub_rn(__dmul_rn(lr, ur), __dmul_rn(li, ui)));
+        im[i * n + j] = __dsub_rn(im[i * n + j], __dadd_rn(__dmul_rn(lr, ui), __dmul_rn(li, ur)));
+      }
+      __syncwarp();
+    }
+    if (lane == 0) xout[item] = x;
+  }
+}
+
+__global__ void kklll_mean_kernel(const double* __restrict__ xs, int64_t count, int trials,
+                                  double* __restrict__ est) {
+  const int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (job >= count) return;
+  const double* x = xs + job * (int64_t)trials;
+  double s = 0.0;
+  for (int t = 0; t < trials; ++t) s = __dadd_rn(s, x[t]);
+  est[job] = __ddiv_rn(s, (double)trials);
+}
+
+}  // namespace
+}  // namespace sperm
+
+using namespace sperm;
+
+extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d_ids, int trials,
+                              uint64_t seed, double* d_est, double* d_trials_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || n > kKNmax) return set_error(SPERM_ERR_ARG, "sperm_estimate: n out of range [1, 112]");
+  if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_estimate: count < 0");
+  if (trials <= 0) trials = n * n;
+  if (count == 0) return SPERM_OK;
+  if (!d_mats || !d_est) return set_error(SPERM_ERR_ARG, "sperm_estimate: NULL pointer");
+  double* xs = d_trials_out;
+  if (!xs) SPERM_CUDA(cudaMallocAsync((void**)&xs, sizeof(double) * count * trials, st));
+  const size_t per_warp = sizeof(double) * 2 * n * n;
+  int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
+  const size_t smem = per_warp * wpb;
+  SPERM_CUDA(cudaFuncSetAttribute(kklll_trial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_trial_kernel, wpb * 32, smem));
+  const int64_t items = count * (int64_t)trials;
+  int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+  const int64_t need = (items + wpb - 1) / wpb;
+  if (grid > need) grid = need;
+  {
+    TimingScope ts("kklll", st);
+    kklll_trial_kernel<<<(unsigned)grid, wpb * 32, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+  }
+  cudaError_t le = cudaGetLastError();
+  if (le == cudaSuccess) {
+    kklll_mean_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(xs, count, trials, d_est);
+    le = cudaGetLastError();
+  }
+  if (!d_trials_out) cudaFreeAsync(xs, st);
+  if (le != cudaSuccess) return cuda_check(le, "kklll kernels");
+  return SPERM_OK;
+}

@@ -1,0 +1,192 @@
+"""Host orchestration of the hot path (Algorithm PH with the improved Step 3).
+
+    per(A) = PH(A):  pre-expand (Step 2)  -> sperm_expand per level
+                     weights   (improved Step 3) -> sperm_estimate (KKLLL)
+                     schedule  (LPT over GPUs)  -> sperm_schedule
+                     per GPU: expand each job to leaves of order <= L (H_per)
+                              and evaluate the leaves by R-NW        -> sperm_expand, sperm_permanent
+                     sum       (Step 4): residue accumulators summed over GPUs by
+                               one NCCL all-reduce, then host CRT   -> torch.distributed, sperm_crt
+
+This module only sequences C-ABI calls and moves tensors; every arithmetic step of
+the method runs inside libsperm.so.  Nodes are kept grouped by order (one dense
+[count, n, n] int32 tensor per order), which is how the kernels take them.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from . import sperm as S
+
+
+@dataclass
+class NodeSet:
+    """Nodes of one order n: mats [count,n,n] int32, coef [count] int64, job [count] int32."""
+    n: int
+    mats: "object"
+    coef: "object"
+    job: "object"
+
+    @property
+    def count(self) -> int:
+        return int(self.mats.shape[0])
+
+
+@dataclass
+class PHResult:
+    value: int
+    job_values: List[int]
+    num_jobs: int
+    job_order_n: Dict[int, int]
+    leaves: int
+    terms: float
+    estimates: Optional[np.ndarray] = None
+    machine: Optional[np.ndarray] = None
+    stats: Dict[str, float] = field(default_factory=dict)
+
+
+def root_nodeset(a, device="cuda") -> NodeSet:
+    import torch
+    a = np.asarray(a, dtype=np.int64)
+    if np.abs(a).max(initial=0) >= 2**31:
+        raise ValueError("entries must fit int32")
+    n = a.shape[0]
+    return NodeSet(n, torch.tensor(a, dtype=torch.int32, device=device).reshape(1, n, n),
+                   torch.ones(1, dtype=torch.int64, device=device),
+                   torch.zeros(1, dtype=torch.int32, device=device))
+
+
+def _cat(sets: List[NodeSet]) -> List[NodeSet]:
+    """Merge node sets of equal order, keeping their relative order."""
+    import torch
+    by: Dict[int, List[NodeSet]] = {}
+    for s in sets:
+        if s.count:
+            by.setdefault(s.n, []).append(s)
+    out = []
+    for n in sorted(by, reverse=True):
+        ss = by[n]
+        if len(ss) == 1:
+            out.append(ss[0])
+        else:
+            out.append(NodeSet(n, torch.cat([s.mats for s in ss]), torch.cat([s.coef for s in ss]),
+                               torch.cat([s.job for s in ss])))
+    return out
+
+
+def pre_expand(root: NodeSet, jobs_at_least: int = 1, job_order: int = 1) -> List[NodeSet]:
+    """Algorithm PH Step 2 (reading R6): BFS levels in natural order until the job
+    count reaches jobs_at_least or the order reaches job_order.  Returns the job list
+    as [level nodes, early (s >= 5) nodes in order of appearance], each NodeSet
+    carrying its jobs' global ids (level jobs first, then early jobs)."""
+    import torch
+    level = root
+    early: List[NodeSet] = []
+    order = root.n
+    while (level.count and level.count + sum(e.count for e in early) < jobs_at_least
+           and order > job_order and order >= 2):
+        (km, kc, kj), (em, ec, ej) = S.sperm_expand(level.mats, level.coef, level.job)
+        if em.shape[0]:
+            early.append(NodeSet(order, em, ec, ej))
+        level = NodeSet(order - 1, km, kc, kj)
+        order -= 1
+    jobs = [level] + early
+    nid = 0
+    out = []
+    for s in jobs:
+        if s.count == 0:
+            continue
+        ids = torch.arange(nid, nid + s.count, dtype=torch.int32, device=s.mats.device)
+        out.append(NodeSet(s.n, s.mats, s.coef, ids))
+        nid += s.count
+    return out
+
+
+def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
+    """H_per's recursion applied breadth-first to a batch of jobs until every node has
+    order <= L or s >= 5 (readings R5/R6).  Job ids are inherited by the leaves."""
+    level = jobs
+    early: List[NodeSet] = []
+    while level.count and level.n > L and level.n >= 2:
+        (km, kc, kj), (em, ec, ej) = S.sperm_expand(level.mats, level.coef, level.job)
+        if em.shape[0]:
+            early.append(NodeSet(level.n, em, ec, ej))
+        level = NodeSet(level.n - 1, km, kc, kj)
+    return _cat([level] + early)
+
+
+def bound_primes(a) -> int:
+    """Primes needed for |x| <= min(prod row abs sums, prod col abs sums) (host, exact ints).
+    Used to size the accumulators of the total; each leaf sizes itself on the device."""
+    a = np.abs(np.asarray(a, dtype=object))
+    rb, cb = 1, 1
+    for i in range(a.shape[0]):
+        rb *= int(sum(a[i]))
+        cb *= int(sum(a[:, i]))
+    b = min(rb, cb)
+    M, k = 1, 0
+    while M <= 2 * b + 1:
+        M *= S.sperm_prime(k)
+        k += 1
+        if k > S.KMAX:
+            raise S.SpermError(S.ERR_PRIMES, "bound needs more than 8 primes")
+    return max(k, 1)
+
+
+def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
+              seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
+              device="cuda") -> PHResult:
+    """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
+
+    With a torch.distributed `group` of world size G, every rank replicates the
+    (cheap, deterministic) pre-expansion, estimation and scheduling, evaluates only
+    the jobs LPT assigned to it, and one all-reduce sums the residue accumulators."""
+    import torch
+    import torch.distributed as dist
+    rank, world = (dist.get_rank(group), dist.get_world_size(group)) if group is not None else (0, 1)
+    k_total = bound_primes(a)
+    root = root_nodeset(a, device)
+    jobsets = pre_expand(root, jobs_at_least, job_order)
+    num_jobs = sum(s.count for s in jobsets)
+    # improved Step 3: KKLLL weights of every job (replicated, deterministic)
+    est = np.zeros(num_jobs)
+    for s in jobsets:
+        if s.n <= 112:
+            e = S.sperm_estimate(s.mats, trials=trials, seed=seed, ids=s.job).cpu().numpy()
+        else:
+            e = np.full(s.count, np.inf)
+        est[s.job.cpu().numpy()] = e
+    machine, order, _ = S.sperm_schedule(est, world, policy, seed=seed)
+    acc = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
+    # this rank's jobs in the order they were dealt (non-increasing estimate)
+    mine = np.array([j for j in order if machine[j] == rank], dtype=np.int64)
+    pos = np.full(num_jobs, -1, dtype=np.int64)
+    pos[mine] = np.arange(len(mine))
+    leaves = 0
+    terms = 0.0
+    for s in jobsets:
+        ids = s.job.cpu().numpy()
+        sel = np.nonzero(pos[ids] >= 0)[0]
+        sel = sel[np.argsort(pos[ids[sel]], kind="stable")]
+        for b0 in range(0, len(sel), batch_jobs):
+            idx = torch.tensor(sel[b0:b0 + batch_jobs], dtype=torch.int64, device=device)
+            batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
+                            s.job.index_select(0, idx))
+            for lv in expand_to_leaves(batch, leaf_order):
+                if lv.n > S.NMAX:
+                    raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
+                S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
+                                  job_acc=acc)
+                leaves += lv.count
+                terms += S.sperm_rnw_terms(lv.n, lv.count)
+    if world > 1:
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    res = S.sperm_reduce_mod(acc).cpu().numpy().view(np.uint32)
+    job_values = [S.sperm_crt(res[j], k_total) for j in range(num_jobs)]
+    value = S.sperm_crt(res[num_jobs], k_total)
+    return PHResult(value=value, job_values=job_values, num_jobs=num_jobs,
+                    job_order_n={s.n: s.count for s in jobsets}, leaves=leaves, terms=terms,
+                    estimates=est, machine=machine)

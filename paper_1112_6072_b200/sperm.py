@@ -1,0 +1,250 @@
+"""Thin ctypes binding of libsperm.so (include/sperm.h), same names as the C ABI.
+
+Argument marshalling only: torch CUDA tensors are passed as raw device pointers
+together with torch's current CUDA stream; every step of the method runs in the
+library's sm_100a kernels (or, for the scheduler and CRT, in its host C++ code).
+There is NO fallback: if libsperm.so is missing or a call fails, an exception
+is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsperm.so")
+
+KMAX = 8
+NMAX = 48
+EXPAND_NMAX = 128
+
+OK, ERR_ARG, ERR_CUDA, ERR_RANGE, ERR_CAPACITY, ERR_PRIMES = 0, -1, -2, -3, -4, -5
+
+
+class SpermError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libsperm error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+
+_SIGS = {
+    "sperm_version": (_I, []),
+    "sperm_last_error": (ctypes.c_char_p, []),
+    "sperm_prime": (ctypes.c_uint32, [_I]),
+    "sperm_crt": (_I, [_P, _I, _P, _I, _P]),
+    "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _P, _P, _P, _P]),
+    "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
+    "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
+    "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
+    "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
+    "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
+    "sperm_timing_enable": (None, [_I]),
+    "sperm_timing_reset": (None, []),
+    "sperm_timing_get": (_I, [ctypes.c_char_p, _P, _P]),
+}
+SYMBOLS = tuple(_SIGS)
+
+
+def lib():
+    """Load libsperm.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_1112_6072_b200.build` "
+                              "or __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise SpermError(rc, lib().sperm_last_error().decode())
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream=None) -> Optional[int]:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _dev(t, dtype):
+    """Require a contiguous CUDA tensor of the given dtype (no silent host copies)."""
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"expected dtype {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+# --------------------------------------------------------------------- utility
+def sperm_version() -> int:
+    return lib().sperm_version()
+
+
+def sperm_prime(i: int) -> int:
+    return int(lib().sperm_prime(i))
+
+
+def primes(k: int = KMAX) -> List[int]:
+    return [sperm_prime(i) for i in range(k)]
+
+
+def sperm_crt(residues: Sequence[int], k: int) -> int:
+    """Host CRT (Garner) of residues[:k] to the symmetric-range integer."""
+    r = np.ascontiguousarray(np.asarray(residues[:k], dtype=np.uint32))
+    limbs = k + 2
+    mag = np.zeros(limbs, dtype=np.uint32)
+    sign = ctypes.c_int(0)
+    _check(lib().sperm_crt(r.ctypes.data, k, mag.ctypes.data, limbs, ctypes.byref(sign)))
+    v = 0
+    for w in mag[::-1]:
+        v = (v << 32) | int(w)
+    return sign.value * v
+
+
+# --------------------------------------------------------------------- R-NW
+def sperm_permanent(mats, coef=None, order=None, job=None, num_jobs: int = 0, min_primes: int = 1,
+                    leaf_res=None, leaf_k=None, job_acc=None, stream=None):
+    """Batched R-NW leaf permanents mod the CRT primes (see include/sperm.h).
+
+    mats: int32 CUDA tensor [count, n, n].  Outputs are allocated if not given:
+    returns (leaf_res uint32-as-int32 [count, KMAX], leaf_k int32 [count])."""
+    import torch
+    mats = _dev(mats, torch.int32)
+    count, n = int(mats.shape[0]), int(mats.shape[1]) if mats.dim() == 3 else 0
+    dev = mats.device
+    if leaf_res is None:
+        leaf_res = torch.empty((count, KMAX), dtype=torch.int32, device=dev)
+    if leaf_k is None:
+        leaf_k = torch.empty((count,), dtype=torch.int32, device=dev)
+    coef = _dev(coef, torch.int64)
+    order = _dev(order, torch.int32)
+    job = _dev(job, torch.int32)
+    _check(lib().sperm_permanent(_ptr(mats), n, count, _ptr(coef), _ptr(order), _ptr(job), int(num_jobs),
+                                 int(min_primes), _ptr(leaf_res), _ptr(leaf_k), _ptr(job_acc), _stream(stream)))
+    return leaf_res, leaf_k
+
+
+def sperm_rnw_terms(n: int, count: int) -> float:
+    return float(lib().sperm_rnw_terms(int(n), int(count)))
+
+
+def sperm_reduce_mod(acc, stream=None):
+    import torch
+    acc = _dev(acc, torch.int64)
+    rows = int(acc.shape[0])
+    out = torch.empty((rows, KMAX), dtype=torch.int32, device=acc.device)
+    _check(lib().sperm_reduce_mod(_ptr(acc), rows, _ptr(out), _stream(stream)))
+    return out
+
+
+def residues_to_ints(res, k) -> List[int]:
+    """CRT every row of a host/device residue table (uint32 stored as int32)."""
+    import torch
+    if isinstance(res, torch.Tensor):
+        res = res.cpu().numpy()
+    if isinstance(k, torch.Tensor):
+        k = k.cpu().numpy()
+    res = np.asarray(res).view(np.uint32)
+    k = np.broadcast_to(np.asarray(k), (res.shape[0],))
+    return [sperm_crt(res[i], int(k[i])) for i in range(res.shape[0])]
+
+
+# --------------------------------------------------------------------- expansion
+def sperm_expand(mats, coef=None, job=None, stream=None):
+    """One BFS level of Algorithm PH Step 2.  Returns ((mats, coef, job) of the
+    children of order n-1, (mats, coef, job) of the unsplit s >= 5 nodes)."""
+    import torch
+    mats = _dev(mats, torch.int32)
+    count, n = int(mats.shape[0]), int(mats.shape[1])
+    dev = mats.device
+    coef = _dev(coef, torch.int64)
+    job = _dev(job, torch.int32)
+    oc, ec = ctypes.c_int64(0), ctypes.c_int64(0)
+    L = lib()
+    # first call with zero capacity learns the sizes (count pass only)
+    rc = L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, None, None, None, 0, None, None, None, 0,
+                        ctypes.byref(oc), ctypes.byref(ec), _stream(stream))
+    if rc not in (OK, ERR_CAPACITY):
+        _check(rc)
+    no, ne = oc.value, ec.value
+    out = (torch.empty((no, n - 1, n - 1), dtype=torch.int32, device=dev),
+           torch.empty((no,), dtype=torch.int64, device=dev), torch.empty((no,), dtype=torch.int32, device=dev))
+    early = (torch.empty((ne, n, n), dtype=torch.int32, device=dev),
+             torch.empty((ne,), dtype=torch.int64, device=dev), torch.empty((ne,), dtype=torch.int32, device=dev))
+    if rc == ERR_CAPACITY:
+        _check(L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]),
+                              _ptr(out[2]), no, _ptr(early[0]), _ptr(early[1]), _ptr(early[2]), ne,
+                              ctypes.byref(oc), ctypes.byref(ec), _stream(stream)))
+    return out, early
+
+
+# --------------------------------------------------------------------- estimator
+def sperm_estimate(mats, trials: int = 0, seed: int = 1, ids=None, keep_trials: bool = False, stream=None):
+    """KKLLL estimates (fp64) of the 0/1 patterns of mats [count, n, n]."""
+    import torch
+    mats = _dev(mats, torch.int32)
+    count, n = int(mats.shape[0]), int(mats.shape[1])
+    if trials <= 0:
+        trials = n * n
+    est = torch.empty((count,), dtype=torch.float64, device=mats.device)
+    xs = torch.empty((count, trials), dtype=torch.float64, device=mats.device) if keep_trials else None
+    ids = _dev(ids, torch.int32)
+    _check(lib().sperm_estimate(_ptr(mats), n, count, _ptr(ids), int(trials), int(seed) & (2**64 - 1),
+                                _ptr(est), _ptr(xs), _stream(stream)))
+    return (est, xs) if keep_trials else est
+
+
+# --------------------------------------------------------------------- schedule
+POLICY = {"estimate": 0, "natural": 1, "random": 2}
+
+
+def sperm_schedule(weights, machines: int, policy: str = "estimate", seed: int = 0):
+    """Host LPT / list scheduling.  Returns (machine[count], order[count], loads[machines])."""
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    count = w.shape[0]
+    machine = np.zeros(count, dtype=np.int32)
+    order = np.zeros(count, dtype=np.int32)
+    loads = np.zeros(machines, dtype=np.float64)
+    _check(lib().sperm_schedule(w.ctypes.data if count else None, count, int(machines), POLICY[policy],
+                                int(seed) & (2**64 - 1), machine.ctypes.data if count else None,
+                                order.ctypes.data if count else None, loads.ctypes.data))
+    return machine, order, loads
+
+
+# --------------------------------------------------------------------- timing
+def sperm_timing_enable(on: bool = True):
+    lib().sperm_timing_enable(1 if on else 0)
+
+
+def sperm_timing_reset():
+    lib().sperm_timing_reset()
+
+
+def sperm_timing_get(name: str) -> Tuple[float, int]:
+    ms, n = ctypes.c_double(0), ctypes.c_int64(0)
+    _check(lib().sperm_timing_get(name.encode(), ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value

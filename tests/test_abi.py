@@ -1,0 +1,124 @@
+"""CPU-only checks of the C-ABI library (-m "not gpu"): it loads, exports every
+symbol include/sperm.h declares, and its host-side functions (CRT, scheduler)
+agree with the oracle.  No kernel is launched here."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1112_6072_b200 as P
+from paper_1112_6072_b200 import sperm as S
+from oracle.crt import crt as oracle_crt
+from oracle.schedule import lpt, ls, makespan, order_by_key
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    txt = open(os.path.join(ROOT, "include", "sperm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sperm_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    L = P.lib()
+    names = _header_functions()
+    assert len(names) >= 12
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(names) == set(S.SYMBOLS), "binding and header disagree"
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(ROOT, "paper_1112_6072_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                src = open(os.path.join(dp, f)).read()
+                assert "oracle" not in re.findall(r"(?:import|from)\s+(\w+)", src), f
+
+
+def test_primes():
+    ps = P.primes(8)
+    assert ps == sorted(ps, reverse=True) and len(set(ps)) == 8
+    for p in ps:
+        assert 2**30 < p < 2**31
+        assert all(p % d for d in range(2, int(math.isqrt(p)) + 1, 1 if p < 100 else 2) if d == 2 or d % 2)
+    assert P.sperm_prime(8) == 0 and P.sperm_prime(-1) == 0
+
+
+def test_crt_matches_oracle():
+    rng = np.random.default_rng(5)
+    for k in range(1, 9):
+        ps = P.primes(k)
+        M = math.prod(ps)
+        for _ in range(40):
+            x = int(rng.integers(-2**62, 2**62)) * int(rng.integers(0, 2**60)) ** (k // 2 + 1) % M
+            if x > M // 2:
+                x -= M
+            res = [x % p for p in ps]
+            assert P.sperm_crt(res, k) == x == oracle_crt(res, ps)
+        # extremes of the symmetric range
+        for x in (M // 2, -(M // 2) + (M % 2 == 0), 0, 1, -1):
+            assert P.sperm_crt([x % p for p in ps], k) == x
+
+
+def test_crt_bad_args():
+    with pytest.raises(S.SpermError):
+        S.sperm_crt([1, 2, 3], 0)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 8, 32])
+def test_schedule_lpt_matches_oracle(m):
+    rng = np.random.default_rng(m)
+    for _ in range(20):
+        w = list(rng.integers(1, 50, size=int(rng.integers(1, 60))).astype(float))
+        w[0] = w[-1]  # ties
+        mach, order, loads = P.sperm_schedule(w, m, "estimate")
+        assign, oloads = lpt(w, m)
+        assert list(order) == order_by_key(w)
+        assert list(mach) == assign
+        assert np.allclose(loads, oloads)
+
+
+def test_schedule_natural_is_ls():
+    w = [5.0, 1.0, 1.0, 2.0, 7.0, 3.0]
+    mach, order, loads = P.sperm_schedule(w, 3, "natural")
+    assign, oloads = ls(w, range(len(w)), 3)
+    assert list(order) == list(range(6)) and list(mach) == assign and np.allclose(loads, oloads)
+
+
+def test_schedule_graham_tight():
+    _, _, loads = P.sperm_schedule([3, 3, 2, 2, 2], 2, "estimate")
+    assert makespan(list(loads)) == 7  # 4/3 - 1/(3m) instance
+    _, _, loads = P.sperm_schedule([1, 1, 2], 2, "natural")
+    assert makespan(list(loads)) == 3  # 2 - 1/m instance
+
+
+def test_schedule_random_is_permutation_and_seeded():
+    w = list(range(100))
+    _, o1, _ = P.sperm_schedule(w, 4, "random", seed=3)
+    _, o2, _ = P.sperm_schedule(w, 4, "random", seed=3)
+    _, o3, _ = P.sperm_schedule(w, 4, "random", seed=4)
+    assert sorted(o1) == w and list(o1) == list(o2) and list(o1) != list(o3)
+
+
+def test_schedule_empty():
+    mach, order, loads = P.sperm_schedule([], 4)
+    assert len(mach) == 0 and list(loads) == [0, 0, 0, 0]
+
+
+def test_rnw_terms():
+    assert P.sperm_rnw_terms(24, 256) == 256 * 2**23
+    assert P.sperm_rnw_terms(1, 3) == 3
+
+
+def test_cuda_entry_points_fail_loudly_without_device():
+    """No GPU here: a compute call must raise, never fall back to the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(TypeError):
+        P.sperm_permanent(torch.zeros((1, 3, 3), dtype=torch.int32))

@@ -1,0 +1,211 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI against the CPU
+oracle, element by element, on seeded inputs.  Exact (bit-for-bit) for every
+permanent, job list and schedule; KKLLL estimates bit-identical (the 1e-12
+relative tolerance of north_star is asserted as the bar)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1112_6072_b200 as P  # noqa: E402
+from paper_1112_6072_b200 import pipeline  # noqa: E402
+from oracle.cryser import per_ryser_nw_c  # noqa: E402
+from oracle.hybrid import expand_to_leaves, h_per, node_permanent, pre_expand, to_dense, to_rows  # noqa: E402
+from oracle.kklll import kklll_estimate, kklll_trial  # noqa: E402
+from oracle.permanent import per_bruteforce, per_ryser_nw_gray  # noqa: E402
+from workloads import dodecahedron, random_3perm, random_3perm_batch, truncated_icosahedron  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def golden(name):
+    for ln in open(os.path.join(GOLD, "oracle_values.txt")):
+        if ln.startswith(name + " "):
+            return int(ln.split()[1])
+    raise KeyError(name)
+
+
+def dev(x, dtype=torch.int32):
+    return torch.tensor(np.asarray(x), dtype=dtype, device="cuda")
+
+
+def gpu_per(mats, coef=None, min_primes=1, order=None):
+    res, k = P.sperm_permanent(dev(mats), coef=None if coef is None else dev(coef, torch.int64),
+                               min_primes=min_primes, order=None if order is None else dev(order))
+    return P.residues_to_ints(res, k)
+
+
+# ------------------------------------------------------------------ R-NW
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 13, 16, 17])
+def test_rnw_random_signed_small(n):
+    rng = np.random.default_rng(100 + n)
+    cnt = 37  # ragged batch
+    mats = (rng.integers(-4, 6, size=(cnt, n, n)) * (rng.random((cnt, n, n)) < 0.5)).astype(np.int64)
+    mats[0] = 0
+    if n > 1:
+        mats[1, n // 2] = 0  # zero row
+    got = gpu_per(mats)
+    want = [per_ryser_nw_gray(m) if n <= 13 else h_per(m) for m in mats]
+    assert got == want
+
+
+def test_rnw_config2_full_batch():
+    """configs[1]: 256 seeded n=24 3-regular matrices, half 0/1, half weighted in [1,7]."""
+    mats = random_3perm_batch(256, 24, seed=2024)
+    got = gpu_per(mats)
+    want = [h_per(m) for m in mats]
+    assert got == want
+    for i in (0, 200):  # and the oracle's own R-NW on samples
+        assert got[i] == per_ryser_nw_c(mats[i])
+
+
+def test_rnw_closed_forms_large_orders():
+    """per(J_n) = n!, per(J_n - I_n) = D_n at orders spanning every register tile size."""
+    D = [1, 0]
+    for k in range(2, 41):
+        D.append((k - 1) * (D[-1] + D[-2]))
+    for n in (10, 20, 23, 24, 25, 31, 32, 33):
+        J = np.ones((1, n, n), dtype=np.int64)
+        assert gpu_per(J) == [math.factorial(n)]
+        assert gpu_per(J - np.eye(n, dtype=np.int64)) == [D[n]]
+
+
+def test_rnw_block_diagonal_n40():
+    """n = 40 (the NP = 40 tile): per of a block-diagonal matrix = product of the blocks'."""
+    rng = np.random.default_rng(40)
+    blocks = [rng.integers(-3, 4, size=(8, 8)) for _ in range(5)]
+    a = np.zeros((40, 40), dtype=np.int64)
+    for b, blk in enumerate(blocks):
+        a[8 * b:8 * b + 8, 8 * b:8 * b + 8] = blk
+    p = rng.permutation(40)
+    want = math.prod(per_bruteforce(b) for b in blocks)
+    assert gpu_per(a[p][:, rng.permutation(40)][None]) == [want]
+
+
+def test_rnw_edge_cases():
+    # empty batch
+    res, k = P.sperm_permanent(torch.zeros((0, 5, 5), dtype=torch.int32, device="cuda"))
+    assert res.shape == (0, P.KMAX)
+    # order 0: per of the empty matrix is 1 (times coef)
+    assert gpu_per(np.zeros((2, 0, 0)), coef=[1, -3]) == [1, -3]
+    # huge entries: many primes and small groups (k up to 8)
+    rng = np.random.default_rng(8)
+    a = rng.integers(-2**21, 2**21, size=(3, 10, 10))
+    assert gpu_per(a) == [h_per(m) for m in a]
+    # coefficients and min_primes
+    mats = random_3perm_batch(5, 11, seed=3)
+    cf = [1, -2, 7, 10**12, -(10**15)]
+    assert gpu_per(mats, coef=cf, min_primes=4) == [c * per_ryser_nw_c(m) for c, m in zip(cf, mats)]
+    # row abs sum >= 2^30 is refused, not wrapped
+    with pytest.raises(P.SpermError):
+        gpu_per(np.full((1, 4, 4), 2**28))
+
+
+def test_rnw_order_and_job_accumulators():
+    mats = random_3perm_batch(40, 14, seed=9)
+    want = [per_ryser_nw_c(m) for m in mats]
+    order = np.random.default_rng(1).permutation(40)
+    assert gpu_per(mats, order=order) == want
+    job = np.arange(40) % 7
+    acc = torch.zeros((8, P.KMAX), dtype=torch.int64, device="cuda")
+    P.sperm_permanent(dev(mats), job=dev(job), num_jobs=7, min_primes=2, job_acc=acc)
+    red = P.sperm_reduce_mod(acc).cpu().numpy().view(np.uint32)
+    for j in range(7):
+        assert P.sperm_crt(red[j], 2) == sum(w for w, jj in zip(want, job) if jj == j)
+    assert P.sperm_crt(red[7], 2) == sum(want)
+
+
+# ------------------------------------------------------------------ expansion
+def _gpu_jobs(a, J):
+    sets = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=J)
+    out = []
+    for s in sets:
+        m, c = s.mats.cpu().numpy(), s.coef.cpu().numpy()
+        for i in range(s.count):
+            out.append((int(c[i]), m[i].tolist()))
+    return out
+
+
+def _oracle_jobs(a, J):
+    return [(c, to_dense(m, k)) for c, m, k in pre_expand(a, jobs_at_least=J)]
+
+
+def test_expand_c20_identical_job_lists():
+    a = dodecahedron()
+    for J in (1, 2, 5, 17, 64, 200):
+        assert _gpu_jobs(a, J) == _oracle_jobs(a, J)
+
+
+def test_expand_random_signed_identical():
+    """Row and column pivots, s = 1..4, zero-line children, s >= 5 early nodes."""
+    rng = np.random.default_rng(77)
+    for t in range(60):
+        n = int(rng.integers(3, 13))
+        dens = float(rng.uniform(0.2, 0.8))
+        a = (rng.integers(-3, 5, size=(n, n)) * (rng.random((n, n)) < dens)).astype(np.int64)
+        a += np.diag(rng.integers(1, 3, size=n))
+        J = int(rng.integers(1, 40))
+        assert _gpu_jobs(a, J) == _oracle_jobs(a, J), t
+
+
+def test_expand_conserves_permanent():
+    a = truncated_icosahedron()
+    sets = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=64)
+    tot = 0
+    for s in sets:
+        for lv in pipeline.expand_to_leaves(s, 22):
+            res, k = P.sperm_permanent(lv.mats, coef=lv.coef, min_primes=2)
+            tot += sum(P.residues_to_ints(res, k))
+    assert tot == golden("C60_truncated_icosahedron")
+
+
+# ------------------------------------------------------------------ KKLLL
+def test_kklll_bit_exact_trials():
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 3, 5, 8, 13, 24):
+        mats = (rng.random((3, n, n)) < 0.4).astype(np.int64)
+        mats[:, np.arange(n), np.arange(n)] = 1
+        est, xs = P.sperm_estimate(dev(mats), trials=25, seed=11, keep_trials=True)
+        xs = xs.cpu().numpy()
+        for j in range(3):
+            ref = [kklll_trial(mats[j], 11, j, t) for t in range(25)]
+            assert np.array_equal(xs[j], np.array(ref)), (n, j)
+            e = kklll_estimate(mats[j], 25, 11, j)
+            assert abs(float(est[j]) - e) <= 1e-12 * abs(e)
+
+
+def test_kklll_ids_and_default_trials():
+    a = dodecahedron()
+    est = P.sperm_estimate(dev(a[None]), trials=0, seed=3, ids=dev([5]))
+    assert abs(float(est[0]) - kklll_estimate(a, 0, 3, 5)) <= 1e-12 * float(est[0])
+
+
+# ------------------------------------------------------------------ whole path
+@pytest.mark.parametrize("policy", ["estimate", "natural", "random"])
+def test_pipeline_c20(policy):
+    a = dodecahedron()
+    for J, L in ((1, 20), (8, 12), (30, 8), (200, 4)):
+        r = pipeline.permanent(a, jobs_at_least=J, leaf_order=L, policy=policy)
+        assert r.value == golden("C20_dodecahedron")
+        oj = pre_expand(a, jobs_at_least=J)
+        assert r.job_values == [node_permanent(j) for j in oj]
+
+
+def test_pipeline_random_sparse_vs_hper():
+    rng = np.random.default_rng(31)
+    for _ in range(12):
+        n = int(rng.integers(8, 19))
+        a = (rng.random((n, n)) < 0.25).astype(np.int64) * rng.integers(1, 4, size=(n, n))
+        a += np.eye(n, dtype=np.int64)
+        r = pipeline.permanent(a, jobs_at_least=int(rng.integers(1, 30)), leaf_order=int(rng.integers(3, 12)))
+        assert r.value == h_per(a)
+
+
+def test_pipeline_c60_leaf16():
+    a = truncated_icosahedron()
+    r = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
+    assert r.value == golden("C60_truncated_icosahedron")

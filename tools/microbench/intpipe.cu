@@ -141,6 +141,55 @@ __global__ void k_mers(uint32_t* out, uint32_t seed) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+
+// signed Montgomery (Seiler): a,b in (-p,p), p < 2^31 odd, pinv = p^-1 mod 2^32; result in (-p,p) = a*b*2^-32
+__device__ __forceinline__ int32_t smont(int32_t a, int32_t b, int32_t p, int32_t pinv) {
+  int64_t t = (int64_t)a * b;
+  int32_t m = (int32_t)t * pinv;
+  int32_t h = __mulhi(m, p);
+  return (int32_t)(t >> 32) - h;
+}
+__global__ void k_smont(int32_t* out, int32_t seed, int32_t p, int32_t pinv) {
+  int32_t a[CH]; int32_t m = seed % p;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) a[c] = (threadIdx.x + c * 7 + seed) % p;
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) a[c] = smont(a[c], m, p, pinv);
+  }
+  int32_t s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s ^= a[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_imadhi(uint32_t* out, uint32_t seed) {
+  uint32_t a[CH]; uint32_t m = seed | 1u;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) a[c] = threadIdx.x + c * 7 + seed;
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) a[c] = __umulhi(a[c], m) + (uint32_t)c;
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s ^= a[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// mixed: 1 IMAD + 1 IADD3 + 1 LOP3 per chain step (pipe balance probe)
+__global__ void k_mix(uint32_t* out, uint32_t seed) {
+  uint32_t a[CH]; uint32_t m = seed | 1u;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) a[c] = threadIdx.x + c * 7 + seed;
+  for (int i = 0; i < ITERS; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { uint32_t x = a[c] * m; x = x + a[(c+1)%CH] + m; a[c] = x ^ (a[(c+3)%CH] & 0x5555u); }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s ^= a[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 void run(const char* name, F launch, double ops_per_thread_iter) {
   int blocks = 148 * 8, threads = 256;
@@ -168,6 +217,10 @@ int main() {
   run("ffma", [&](int b, int t) { k_ffma<<<b, t>>>((float*)buf, 1.0001f); }, 1.0);
   run("dfma", [&](int b, int t) { k_dfma<<<b, t>>>((double*)buf, 1.0001); }, 1.0);
   run("mont", [&](int b, int t) { k_mont<<<b, t>>>((uint32_t*)buf, 12345u, p, pinv); }, 1.0);
+  { int32_t ps = 2147483629; int32_t iv = 1; for (int i = 0; i < 5; ++i) iv *= 2 - ps * iv;
+    run("smont", [&](int b, int t) { k_smont<<<b, t>>>((int32_t*)buf, 12345, ps, iv); }, 1.0); }
+  run("imadhi", [&](int b, int t) { k_imadhi<<<b, t>>>((uint32_t*)buf, 12345u); }, 1.0);
+  run("mix3", [&](int b, int t) { k_mix<<<b, t>>>((uint32_t*)buf, 12345u); }, 3.0);
   run("mersenne", [&](int b, int t) { k_mers<<<b, t>>>((uint32_t*)buf, 12345u); }, 1.0);
   cudaError_t err = cudaDeviceSynchronize();
   printf("status: %s\n", cudaGetErrorString(err));
