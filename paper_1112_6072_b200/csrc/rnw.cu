@@ -2,24 +2,39 @@
 // leaf permanents in exact multi-prime modular arithmetic, sm_100a.
 //
 //   per(A) = (-1)^(n-1) 2^(1-n) sum_{t=0}^{2^(n-1)-1} (-1)^t prod_i w_i(g(t))
-//   w_i(S) = 2 a_{i,n-1} - sum_j a_ij + 2 sum_{j in S} a_ij        (doubled NW row sums)
-//   g(t)   = t ^ (t >> 1); going from t-1 to t flips Gray bit / column ctz(t).
+//   w_i(S) = 2 a_{i,nw} - sum_j a_ij + 2 sum_{j in S} a_ij        (doubled NW row sums)
+//   g(t)   = t ^ (t >> 1); going from t-1 to t flips Gray bit ctz(t); (-1)^{|g(t)|} = (-1)^t.
 //
-// Work decomposition: a work item is (leaf, chunk) where a chunk is
-// 32 lanes x 2^m consecutive terms; lane l of a chunk owns t in [t0, t0 + 2^m) with
-// t0 = (chunk*32 + l) * 2^m.  Because every lane's range is aligned to 2^m, the flipped
-// column ctz(t) = ctz(t - t0) is the same in all 32 lanes at every step (warp-uniform
-// shared-memory broadcast of the column).  A persistent grid pulls work items from one
-// atomic counter in the given leaf order (improved Step 3).
+// Work decomposition.  A work item is (leaf, chunk): 32 lanes x 2^m
+// consecutive terms; lane l owns t in [t0, t0 + 2^m), t0 = (chunk*32 + l) 2^m.  Every lane
+// range is aligned to 2^m, so the Gray bit flipped at each step is the same in all 32 lanes
+// (a warp-uniform shared-memory broadcast of the column).  Persistent CTAs pull work items
+// from one atomic counter in the caller's leaf order (improved Step 3).
+// Terms are summed exactly (int64 per lane), reduced mod p per chunk and added to the leaf's
+// uint64 accumulator (exact and order-independent, so results are bit-reproducible).
 //
-// Per term: the row-sum vector w[NP] lives in registers (static indexing: the column
-// update is dense over NP rows, 4 rows per 128-bit broadcast load); rows are multiplied
-// in groups of G inside exact int32 (|group| < 2^30 is guaranteed by the per-leaf bound
-// pass), then the NP/G group values are chained with signed Montgomery multiplication
-// modulo each of the leaf's k primes.  Terms are summed exactly (int64 per lane), reduced
-// mod p per chunk and added to the leaf's uint64 accumulator (exact, order-independent).
+// Two kernels evaluate the same sum; a per-leaf prep pass picks one (the "plan"):
+//
+//  * generic (plan 0): the row-sum vector w[NP] lives in registers; each Gray step adds the
+//    flipped column densely (4 rows per 128-bit broadcast load); the n-fold product is formed
+//    as NP/G exact int32 group products chained by signed Montgomery products mod each prime.
+//
+//  * tree (plans 1-5): rows and columns are renumbered (per(A) is invariant) so that the B
+//    lowest Gray bits belong to columns with pairwise disjoint supports of <= 3 rows ("slot"
+//    rows).  The 2^B terms of an aligned block share every row sum except the slot rows of
+//    their low columns, and a slot row of low column c takes one of two values (bit c clear
+//    or set).  Each term's product is therefore
+//        prod_i w_i = X_u * Y_v,  X_u = prod_{c<B1} Q_c^{u_c} (exact int32),
+//                                 Y_v = P_F * prod_{c>=B1} Q_c^{v_c}  (mod p),
+//    with Q_c^0/Q_c^1 the products of column c's slot rows and P_F the product of the other
+//    ("fixed") rows.  The kernel forms X_u * Y_v for every one of the 2^B terms with one
+//    32x32->64 multiply-add (IMAD.WIDE) per term and prime, and reduces once per 2^B1 terms.
+//    The signs (-1)^{|u|+|v|} are folded into X and Y by negating Q_c^1.  Only the per-block
+//    row-sum update (a high Gray bit flip) touches all rows.
 #include <algorithm>
 #include <cmath>
+#include <cub/device/device_radix_sort.cuh>
+#include <vector>
 
 #include "common.cuh"
 
@@ -28,61 +43,79 @@ namespace {
 
 constexpr int kRnwThreads = 256;  // 8 warps per CTA
 constexpr int kMaxLaneBits = 14;  // terms per lane <= 2^14
+constexpr int KS = 3;             // slot rows per low column (tree plans)
+constexpr int kNumNFix = 7;
+constexpr int kPermRows = 64;     // per-leaf permutation record: 64 row bytes + 64 column bytes
+constexpr int kPermW = 128;
+constexpr int kNumKeys = 48;      // plan * 8 + nfix index
 
-struct PrimeSet {
-  int32_t p[SPERM_KMAX];
-  int32_t pinv[SPERM_KMAX];  // p^-1 mod 2^32
-  uint32_t r2[SPERM_KMAX];   // unused by the kernels (kept for layout stability)
-};
-
-PrimeSet make_primes() {
-  PrimeSet s;
-  for (int q = 0; q < SPERM_KMAX; ++q) {
-    uint32_t p = kPrimes[q];
-    uint32_t inv = p;  // Newton: inv = p^-1 mod 2^32 (p*p = 1 mod 8 start)
-    for (int it = 0; it < 5; ++it) inv *= 2u - p * inv;
-    s.p[q] = (int32_t)p;
-    s.pinv[q] = (int32_t)inv;
-    s.r2[q] = 0;
-  }
-  return s;
+__host__ __device__ constexpr int nfix_of(int i) {
+  return i == 0 ? 4 : i == 1 ? 8 : i == 2 ? 12 : i == 3 ? 16 : i == 4 ? 24 : i == 5 ? 32 : 40;
 }
+// tree plans: (B1, B2, GF) — B1 low bits in the exact X tree, B2 in the modular Y tree,
+// GF fixed rows per exact group.  Plan 0 = generic kernel.
+__host__ __device__ constexpr int plan_b1(int p) { return p == 1 ? 4 : p == 2 ? 3 : p == 3 ? 2 : p == 4 ? 2 : p == 5 ? 1 : 0; }
+__host__ __device__ constexpr int plan_b2(int p) { return p == 1 ? 2 : p == 2 ? 2 : p == 3 ? 2 : p == 4 ? 1 : p == 5 ? 1 : 0; }
+__host__ __device__ constexpr int plan_gf(int p) { return (p >= 1 && p <= 3) ? 4 : 2; }
+constexpr int kNumPlans = 6;
 
-// Signed Montgomery product (a*b*2^-32 mod p) for |a|,|b| < p < 2^31; result in (-p, p).
+// the CRT primes (kPrimes, common.cuh) and p^-1 mod 2^32
+__constant__ int32_t c_p[SPERM_KMAX] = {2147483647, 2147483629, 2147483587, 2147483579,
+                                        2147483563, 2147483549, 2147483543, 2147483497};
+__constant__ int32_t c_pinv[SPERM_KMAX] = {2147483647, 1469330917, -1091344149, -591336077,
+                                           -2096954621, -1062895947, -1493012441, -1066630951};
+
+// Signed Montgomery product a*b*2^-32 mod p for |a|,|b| < p < 2^31; result in (-p, p).
 __device__ __forceinline__ int32_t smont(int32_t a, int32_t b, int32_t p, int32_t pinv) {
-  int64_t t = (int64_t)a * b;
-  int32_t m = (int32_t)t * pinv;
+  const int64_t t = (int64_t)a * b;
+  const int32_t m = (int32_t)t * pinv;
+  return (int32_t)(t >> 32) - __mulhi(m, p);
+}
+// Signed Montgomery reduction T*2^-32 mod p for |T| < p*2^31; result in (-p, p).
+__device__ __forceinline__ int32_t redc(int64_t t, int32_t p, int32_t pinv) {
+  const int32_t m = (int32_t)t * pinv;
   return (int32_t)(t >> 32) - __mulhi(m, p);
 }
 
-template <int NP>
-struct Layout {
-  static constexpr int kPos = 0;                                  // dpos[col][NP]
-  static constexpr int kNeg = ((NP * NP + 31) / 32) * 32 + 16;    // dneg[col][NP], bank-shifted
-  static constexpr int kW0 = kNeg + NP * NP;                      // w0[NP]
-  static constexpr int kWords = ((kW0 + NP + 3) / 4) * 4;         // per warp, 16-byte aligned
-};
+// per-leaf metadata: x = k | plan << 8 | nfix_idx << 16 | G << 24, y = Montgomery exponent
+__device__ __forceinline__ int meta_k(int2 m) { return m.x & 0xff; }
+__device__ __forceinline__ int meta_plan(int2 m) { return (m.x >> 8) & 0xff; }
+__device__ __forceinline__ int meta_G(int2 m) { return (m.x >> 24) & 0xff; }
 
-// ----------------------------------------------------------------------------- prep
-// One warp per leaf: row / column abs sums -> number of primes k and group size G.
-__global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NP, int64_t count,
-                                const int64_t* __restrict__ coef, int min_primes,
-                                int2* __restrict__ meta, int* __restrict__ err) {
+// ============================================================================ prep
+// One warp per leaf.  Row / column abs sums -> number of primes k, generic group size G;
+// then the tree plan: 32 lanes run the greedy disjoint-support column pick from 32
+// rotations of the start column, the best (lowest lane on ties) wins; the first plan whose
+// exact-arithmetic bounds hold is taken.
+__global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
+                                const int64_t* __restrict__ coef, int min_primes, int allow_tree,
+                                int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
   const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (leaf >= count) return;
   const int32_t* a = mats + leaf * (int64_t)n * n;
-  __shared__ int64_t srow[8][SPERM_NMAX];
-  int64_t* R = srow[threadIdx.x >> 5];
+  __shared__ int64_t sR[8][SPERM_NMAX];
+  __shared__ unsigned long long sSupp[8][SPERM_NMAX];
+  __shared__ int sCnt[8][SPERM_NMAX];
+  int64_t* R = sR[wib];
+  unsigned long long* supp = sSupp[wib];
+  int* cnt = sCnt[wib];
   double lr = 0.0, lc = 0.0;
   bool zero = false, range_bad = false;
   for (int i = lane; i < n; i += 32) {
     int64_t r = 0, c = 0;
+    unsigned long long sm = 0;
+    int nz = 0;
     for (int j = 0; j < n; ++j) {
       r += llabs((long long)a[i * n + j]);
-      c += llabs((long long)a[j * n + i]);
+      const int32_t v = a[j * n + i];
+      c += llabs((long long)v);
+      if (v != 0) { sm |= 1ull << j; ++nz; }
     }
     R[i] = r;
+    supp[i] = sm;  // support of column i (rows j with a_ji != 0)
+    cnt[i] = nz;
     if (r == 0 || c == 0) zero = true;
     if (r >= (1ll << 30)) range_bad = true;
     if (r > 0) lr += log2((double)r);
@@ -95,28 +128,50 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NP,
   zero = __any_sync(0xffffffffu, zero);
   range_bad = __any_sync(0xffffffffu, range_bad);
   __syncwarp();
+
+  // ---- tree plan: greedy pick of up to 6 low columns with disjoint supports of <= 3 rows
+  int picks[6] = {-1, -1, -1, -1, -1, -1};
+  int np = 0;
+  if (allow_tree && n >= 8 && !range_bad) {
+    unsigned long long used = 0;
+    for (int lvl = 1; lvl <= KS; ++lvl)
+      for (int t = 0; t < n; ++t) {
+        const int j = (t + lane) % n;
+        if (cnt[j] == lvl && !(supp[j] & used) && np < 6 && np < n - 2) {
+          picks[np++] = j;
+          used |= supp[j];
+        }
+      }
+  }
+  // best lane: most picks, lowest lane on ties
+  int key = (np << 8) | (31 - lane);
+  for (int o = 16; o; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+  const int best = 31 - (key & 0xff);
+  np = key >> 8;
+  for (int c = 0; c < 6; ++c) picks[c] = __shfl_sync(0xffffffffu, c < np ? picks[min(c, 5)] : -1, best);
+
   if (lane == 0) {
     if (range_bad) atomicOr(err, 1);
     double lb = zero ? -1.0 : fmin(lr, lc);
-    int64_t cf = coef ? coef[leaf] : 1;
+    const int64_t cf = coef ? coef[leaf] : 1;
     if (cf == 0) lb = -1.0;
     else if (lb >= 0.0) lb += log2(fabs((double)cf));
     // need prod p_q > 2 * bound; each p_q > 2^30.99999; margin for log2 rounding
-    double need = lb + 1.0 + 1e-6 * fabs(lb) + 1e-6;
+    const double need = lb + 1.0 + 1e-6 * fabs(lb) + 1e-6;
     int k = min_primes;
     while (k <= SPERM_KMAX && 30.99999 * k <= need) ++k;
     if (k > SPERM_KMAX) {
       atomicOr(err, 2);
       k = SPERM_KMAX;
     }
-    // largest group size G in {8,4,2,1} with every group product of row bounds < 2^30
+    // generic: largest group size G in {8,4,2,1} with every group product of row bounds < 2^30
     int G = 1;
     for (int g = 8; g >= 2; g >>= 1) {
       bool ok = true;
-      for (int s = 0; s < NP && ok; s += g) {
+      for (int s = 0; s < NPg && ok; s += g) {
         int64_t prod = 1;
         for (int r = s; r < s + g; ++r) {
-          int64_t b = r < n ? R[r] : 1;
+          const int64_t b = r < n ? R[r] : 1;
           if (b == 0) { prod = 0; break; }
           if (prod > ((1ll << 30) - 1) / b) { ok = false; break; }
           prod *= b;
@@ -125,14 +180,83 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NP,
       }
       if (ok) { G = g; break; }
     }
-    meta[leaf] = make_int2(k, G);
+    int plan = 0, nfi = 0, mexp = NPg / G - 1;
+    for (int pl = allow_tree; pl >= 1 && pl < kNumPlans && np > 0; ++pl) {
+      const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
+      if (np < B || n - 6 < B) continue;
+      // exact bounds: |X| < 2^(31-B1), |Z| < 2^30, fixed groups < 2^30
+      auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
+        if (x == 0 || y == 0) return 0;
+        if (x > ((int64_t)1 << 40) / y) return (int64_t)1 << 40;
+        return x * y;
+      };
+      int64_t X = 1, Z = 1;
+      unsigned long long slot_rows = 0;
+      for (int c = 0; c < B; ++c) {
+        int64_t q = 1;
+        for (int i = 0; i < n; ++i)
+          if ((supp[picks[c]] >> i) & 1ull) q = sat_mul(q, R[i]);
+        slot_rows |= supp[picks[c]];
+        if (c < B1) X = sat_mul(X, q);
+        else Z = sat_mul(Z, q);
+      }
+      if (X >= ((int64_t)1 << (31 - B1)) || Z >= ((int64_t)1 << 30)) continue;
+      const int nf = n - __popcll(slot_rows);
+      int fi = 0;
+      while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
+      if (fi == kNumNFix) continue;
+      const int NF = nfix_of(fi);
+      bool ok = true;
+      int pos = 0;
+      int64_t g = 1;
+      for (int i = 0; i < n && ok; ++i) {
+        if ((slot_rows >> i) & 1ull) continue;
+        g = sat_mul(g, R[i]);
+        if (++pos % GF == 0) {
+          if (g >= ((int64_t)1 << 30)) ok = false;
+          g = 1;
+        }
+      }
+      if (g >= ((int64_t)1 << 30)) ok = false;
+      if (!ok) continue;
+      plan = pl;
+      nfi = fi;
+      mexp = NF / GF + 1;
+      // permutation record: rows [slot rows of low column c (ascending, -1 padded to KS)...,
+      // fixed rows ascending, -1 to NS + NF]; columns [low columns, high columns ascending, nw]
+      int8_t* pr = perm + leaf * kPermW;
+      int r = 0;
+      for (int c = 0; c < B; ++c) {
+        int s = 0;
+        for (int i = 0; i < n; ++i)
+          if ((supp[picks[c]] >> i) & 1ull) { pr[r++] = (int8_t)i; ++s; }
+        for (; s < KS; ++s) pr[r++] = -1;
+      }
+      int f = 0;
+      for (int i = 0; i < n; ++i)
+        if (!((slot_rows >> i) & 1ull)) { pr[r++] = (int8_t)i; ++f; }
+      for (; f < NF; ++f) pr[r++] = -1;
+      // nw column: the non-low column with most nonzeros (highest index on ties)
+      unsigned long long low = 0;
+      for (int c = 0; c < B; ++c) low |= 1ull << picks[c];
+      int nw = -1;
+      for (int j = 0; j < n; ++j)
+        if (!((low >> j) & 1ull) && (nw < 0 || cnt[j] >= cnt[nw])) nw = j;
+      int8_t* pc = pr + kPermRows;
+      int cc = 0;
+      for (int c = 0; c < B; ++c) pc[cc++] = (int8_t)picks[c];
+      for (int j = 0; j < n; ++j)
+        if (!((low >> j) & 1ull) && j != nw) pc[cc++] = (int8_t)j;
+      pc[cc++] = (int8_t)nw;
+      break;
+    }
+    meta[leaf] = make_int2(k | (plan << 8) | (nfi << 16) | (G << 24), mexp);
   }
 }
 
-// ----------------------------------------------------------------------------- main
+// ============================================================================ generic kernel
 template <int NP, int G>
-__device__ __forceinline__ void term_product(const int32_t (&w)[NP], int k, const PrimeSet& ps,
-                                             int32_t (&out)[SPERM_KMAX]) {
+__device__ __forceinline__ void term_product(const int32_t (&w)[NP], int k, int32_t (&out)[SPERM_KMAX]) {
   constexpr int NG = NP / G;
   int32_t gp[NG];
 #pragma unroll
@@ -147,22 +271,29 @@ __device__ __forceinline__ void term_product(const int32_t (&w)[NP], int k, cons
     if (q < k) {
       int32_t pr = gp[0];
 #pragma unroll
-      for (int g = 1; g < NG; ++g) pr = smont(pr, gp[g], ps.p[q], ps.pinv[q]);
+      for (int g = 1; g < NG; ++g) pr = smont(pr, gp[g], c_p[q], c_pinv[q]);
       out[q] = pr;
     }
   }
 }
 
-// Runs one lane's 2^m terms starting at t0 (t0 a multiple of 2^m, m >= 1).
+template <int NP>
+struct GLayout {
+  static constexpr int kPos = 0;                                // dpos[col][NP]
+  static constexpr int kNeg = ((NP * NP + 31) / 32) * 32 + 16;  // dneg[col][NP], bank-shifted
+  static constexpr int kW0 = kNeg + NP * NP;                    // w0[NP]
+  static constexpr int kWords = ((kW0 + NP + 3) / 4) * 4;       // per warp, 16-byte aligned
+};
+
+// One lane's 2^m terms starting at t0 (t0 a multiple of 2^m, m >= 1).
 template <int NP, int G>
-__device__ __forceinline__ void lane_range(int32_t (&w)[NP], const int32_t* __restrict__ sm, int m,
-                                        uint64_t t0, int k, const PrimeSet& ps,
-                                        int64_t (&acc)[SPERM_KMAX]) {
-  using L = Layout<NP>;
+__device__ __forceinline__ void lane_range(int32_t (&w)[NP], const int32_t* __restrict__ sm, int m, uint64_t t0,
+                                           int k, int64_t (&acc)[SPERM_KMAX]) {
+  using L = GLayout<NP>;
   int32_t d0[NP];
 #pragma unroll
   for (int v = 0; v < NP / 4; ++v) {
-    int4 d = reinterpret_cast<const int4*>(sm + L::kPos)[v];
+    const int4 d = reinterpret_cast<const int4*>(sm + L::kPos)[v];
     d0[4 * v] = d.x; d0[4 * v + 1] = d.y; d0[4 * v + 2] = d.z; d0[4 * v + 3] = d.w;
   }
   int32_t pe[SPERM_KMAX], po[SPERM_KMAX];
@@ -174,11 +305,11 @@ __device__ __forceinline__ void lane_range(int32_t (&w)[NP], const int32_t* __re
       const int4* col = reinterpret_cast<const int4*>(sm + (add ? L::kPos : L::kNeg) + j * NP);
 #pragma unroll
       for (int v = 0; v < NP / 4; ++v) {
-        int4 d = col[v];
+        const int4 d = col[v];
         w[4 * v] += d.x; w[4 * v + 1] += d.y; w[4 * v + 2] += d.z; w[4 * v + 3] += d.w;
       }
     }
-    term_product<NP, G>(w, k, ps, pe);
+    term_product<NP, G>(w, k, pe);
     // odd step t0+u+1 flips column 0: added iff bit 1 of t0+u+1 is 0
     if (!(((t0 + u + 1) >> 1) & 1ull)) {
 #pragma unroll
@@ -187,7 +318,7 @@ __device__ __forceinline__ void lane_range(int32_t (&w)[NP], const int32_t* __re
 #pragma unroll
       for (int i = 0; i < NP; ++i) w[i] -= d0[i];
     }
-    term_product<NP, G>(w, k, ps, po);
+    term_product<NP, G>(w, k, po);
 #pragma unroll
     for (int q = 0; q < SPERM_KMAX; ++q)
       if (q < k) acc[q] += (int64_t)pe[q] - (int64_t)po[q];
@@ -195,11 +326,11 @@ __device__ __forceinline__ void lane_range(int32_t (&w)[NP], const int32_t* __re
 }
 
 template <int NP>
-__global__ void __launch_bounds__(kRnwThreads) rnw_main_kernel(
-    const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ order,
+__global__ void __launch_bounds__(kRnwThreads) rnw_generic_kernel(
+    const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, unsigned long long* __restrict__ queue, uint64_t total_items,
-    unsigned long long* __restrict__ leaf_acc, PrimeSet ps) {
-  using L = Layout<NP>;
+    unsigned long long* __restrict__ leaf_acc) {
+  using L = GLayout<NP>;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   int32_t* sm = reinterpret_cast<int32_t*>(smem4) + (threadIdx.x >> 5) * L::kWords;
@@ -210,11 +341,10 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_main_kernel(
     if (lane == 0) item = atomicAdd(queue, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= total_items) break;
-    const int64_t slot = (int64_t)(item >> cbits);
+    const int64_t leaf = leaves[(int64_t)(item >> cbits)];
     const uint64_t chunk = item & ((1ull << cbits) - 1);
-    const int64_t leaf = order ? (int64_t)order[slot] : slot;
     const int2 mt = meta[leaf];
-    const int k = mt.x, G = mt.y;
+    const int k = meta_k(mt), G = meta_G(mt);
     if (leaf != cur_leaf) {
       __syncwarp();
       const int32_t* a = mats + leaf * (int64_t)n * n;
@@ -255,10 +385,10 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_main_kernel(
       if (m == 0) {  // one term per lane (tiny leaves)
         int32_t pr[SPERM_KMAX];
         switch (G) {
-          case 8: term_product<NP, 8>(w, k, ps, pr); break;
-          case 4: term_product<NP, 4>(w, k, ps, pr); break;
-          case 2: term_product<NP, 2>(w, k, ps, pr); break;
-          default: term_product<NP, 1>(w, k, ps, pr); break;
+          case 8: term_product<NP, 8>(w, k, pr); break;
+          case 4: term_product<NP, 4>(w, k, pr); break;
+          case 2: term_product<NP, 2>(w, k, pr); break;
+          default: term_product<NP, 1>(w, k, pr); break;
         }
         const bool neg = t0 & 1ull;
 #pragma unroll
@@ -266,10 +396,10 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_main_kernel(
           if (q < k) acc[q] = neg ? -(int64_t)pr[q] : (int64_t)pr[q];
       } else {
         switch (G) {
-          case 8: lane_range<NP, 8>(w, sm, m, t0, k, ps, acc); break;
-          case 4: lane_range<NP, 4>(w, sm, m, t0, k, ps, acc); break;
-          case 2: lane_range<NP, 2>(w, sm, m, t0, k, ps, acc); break;
-          default: lane_range<NP, 1>(w, sm, m, t0, k, ps, acc); break;
+          case 8: lane_range<NP, 8>(w, sm, m, t0, k, acc); break;
+          case 4: lane_range<NP, 4>(w, sm, m, t0, k, acc); break;
+          case 2: lane_range<NP, 2>(w, sm, m, t0, k, acc); break;
+          default: lane_range<NP, 1>(w, sm, m, t0, k, acc); break;
         }
       }
     }
@@ -279,8 +409,8 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_main_kernel(
         int64_t v = acc[q];
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) {
-          int64_t r = v % ps.p[q];
-          if (r < 0) r += ps.p[q];
+          int64_t r = v % c_p[q];
+          if (r < 0) r += c_p[q];
           atomicAdd(leaf_acc + leaf * SPERM_KMAX + q, (unsigned long long)r);
         }
       }
@@ -288,7 +418,185 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_main_kernel(
   }
 }
 
-// ----------------------------------------------------------------------------- finalize
+// ============================================================================ tree kernel
+// shared memory per warp (words): colpos[nh][S4] | colneg[nh][S4] (bank-shifted) | w0[S4] |
+// delta[NS] | sacc int64[KMAX][32]
+struct TreeSmem {
+  int S4, nh, pos, neg, w0, delta, sacc, words;
+};
+__host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
+  TreeSmem t;
+  t.S4 = (NRT + 3) / 4 * 4;
+  t.nh = n - 1 - B;
+  t.pos = 0;
+  t.neg = ((t.nh * t.S4 + 31) / 32) * 32 + 16;
+  t.w0 = ((t.neg + t.nh * t.S4 + 3) / 4) * 4;
+  t.delta = t.w0 + t.S4;
+  t.sacc = ((t.delta + NS + 1) / 2) * 2;
+  t.words = ((t.sacc + 2 * SPERM_KMAX * 32 + 3) / 4) * 4;
+  return t;
+}
+
+template <int NFIX, int PLAN>
+__global__ void __launch_bounds__(kRnwThreads) rnw_tree_kernel(
+    const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
+    const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
+    uint64_t total_items, unsigned long long* __restrict__ leaf_acc) {
+  constexpr int B1 = plan_b1(PLAN), B2 = plan_b2(PLAN), B = B1 + B2, GF = plan_gf(PLAN);
+  constexpr int NS = B * KS;       // slot rows
+  constexpr int NRT = NS + NFIX;   // row sums held in registers
+  constexpr int S4 = (NRT + 3) / 4 * 4;
+  constexpr int NGF = NFIX / GF;   // exact fixed-row groups
+  constexpr int NX = 1 << B1, NZ = 1 << B2;
+  extern __shared__ int4 smem4[];
+  const int lane = threadIdx.x & 31;
+  const TreeSmem L = tree_smem(NRT, NS, n, B);
+  int32_t* sm = reinterpret_cast<int32_t*>(smem4) + (threadIdx.x >> 5) * L.words;
+  long long* sacc = reinterpret_cast<long long*>(sm + L.sacc);
+  int64_t cur_leaf = -1;
+  while (true) {
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(queue, 1ull);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= total_items) break;
+    const int64_t leaf = leaves[(int64_t)(item >> cbits)];
+    const uint64_t chunk = item & ((1ull << cbits) - 1);
+    const int k = meta_k(meta[leaf]);
+    if (leaf != cur_leaf) {
+      __syncwarp();
+      const int32_t* a = mats + leaf * (int64_t)n * n;
+      const int8_t* pr = perm + leaf * kPermW;
+      const int8_t* pc = pr + kPermRows;
+      for (int e = lane; e < L.nh * S4; e += 32) {
+        const int h = e / S4, r = e - (e / S4) * S4;
+        const int row = r < NRT ? pr[r] : -1;
+        const int32_t v = row >= 0 ? 2 * a[row * n + pc[B + h]] : 0;
+        sm[L.pos + e] = v;
+        sm[L.neg + e] = -v;
+      }
+      const int nw = pc[n - 1];
+      for (int r = lane; r < S4; r += 32) {
+        const int row = r < NRT ? pr[r] : -1;
+        int32_t w0 = 1;
+        if (row >= 0) {
+          int32_t s = 0;
+          for (int j = 0; j < n; ++j) s += a[row * n + j];
+          w0 = 2 * a[row * n + nw] - s;
+        }
+        sm[L.w0 + r] = w0;
+      }
+      for (int s = lane; s < NS; s += 32) {
+        const int row = pr[s];
+        sm[L.delta + s] = row >= 0 ? 2 * a[row * n + pc[s / KS]] : 0;
+      }
+      __syncwarp();
+      cur_leaf = leaf;
+    }
+    for (int q = 0; q < k; ++q) sacc[q * 32 + lane] = 0;
+    const uint64_t t0 = ((chunk << 5) + (uint64_t)lane) << m;
+    // base row sums (low bits clear) of the lane's first block
+    int32_t W[S4];
+#pragma unroll
+    for (int r = 0; r < S4; ++r) W[r] = sm[L.w0 + r];
+    {
+      const uint64_t g0 = t0 ^ (t0 >> 1);
+      for (int h = max(m - 1 - B, 0); h < L.nh; ++h)
+        if ((g0 >> (B + h)) & 1ull) {
+#pragma unroll
+          for (int r = 0; r < S4; ++r) W[r] += sm[L.pos + h * S4 + r];
+        }
+    }
+    int32_t D[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) D[s] = sm[L.delta + s];
+    const uint64_t O0 = t0 >> B;
+    const uint32_t nblk = 1u << (m - B);
+    for (uint32_t ob = 0; ob < nblk; ++ob) {
+      if (ob) {  // flip high Gray bit B + hh (warp-uniform column)
+        const int hh = __ffs(ob) - 1;
+        const bool add = !(((O0 + ob) >> (hh + 1)) & 1ull);
+        const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
+#pragma unroll
+        for (int v = 0; v < S4 / 4; ++v) {
+          const int4 d = col[v];
+          W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
+        }
+      }
+      // slot products: Q0 (bit clear), Q1 = -(bit set)  (sign (-1)^{|u|+|v|} folded in)
+      int32_t Q0[B], Q1[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
+#pragma unroll
+        for (int s = 1; s < KS; ++s) {
+          x0 *= W[c * KS + s];
+          x1 *= W[c * KS + s] + D[c * KS + s];
+        }
+        Q0[c] = x0;
+        Q1[c] = -x1;
+      }
+      int32_t X[NX], Z[NZ];
+      X[0] = Q0[0];
+      X[1] = Q1[0];
+#pragma unroll
+      for (int c = 1; c < B1; ++c)
+#pragma unroll
+        for (int s = 0; s < (1 << c); ++s) {
+          X[s + (1 << c)] = X[s] * Q1[c];
+          X[s] = X[s] * Q0[c];
+        }
+      Z[0] = Q0[B1];
+      Z[1] = Q1[B1];
+#pragma unroll
+      for (int c = 1; c < B2; ++c)
+#pragma unroll
+        for (int s = 0; s < (1 << c); ++s) {
+          Z[s + (1 << c)] = Z[s] * Q1[B1 + c];
+          Z[s] = Z[s] * Q0[B1 + c];
+        }
+      int32_t FG[NGF];
+#pragma unroll
+      for (int g = 0; g < NGF; ++g) {
+        int32_t x = W[NS + g * GF];
+#pragma unroll
+        for (int r = 1; r < GF; ++r) x *= W[NS + g * GF + r];
+        FG[g] = x;
+      }
+      const bool neg = (O0 + ob) & 1ull;  // (-1)^{|high Gray bits|}
+      for (int q = 0; q < k; ++q) {
+        const int32_t p = c_p[q], pinv = c_pinv[q];
+        int32_t pf = FG[0];
+#pragma unroll
+        for (int g = 1; g < NGF; ++g) pf = smont(pf, FG[g], p, pinv);
+        int64_t blk = 0;
+#pragma unroll
+        for (int v = 0; v < NZ; ++v) {
+          const int32_t y = smont(pf, Z[v], p, pinv);
+          int64_t t_even = 0, t_odd = 0;
+#pragma unroll
+          for (int u = 0; u < NX; u += 2) {
+            t_even += (int64_t)X[u] * y;       // one term: X_u * Y_v
+            if (u + 1 < NX) t_odd += (int64_t)X[u + 1] * y;
+          }
+          blk += redc(t_even + t_odd, p, pinv);
+        }
+        sacc[q * 32 + lane] += neg ? -blk : blk;
+      }
+    }
+    __syncwarp();
+    for (int q = 0; q < k; ++q) {
+      int64_t v = sacc[q * 32 + lane];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        int64_t r = v % c_p[q];
+        if (r < 0) r += c_p[q];
+        atomicAdd(leaf_acc + leaf * SPERM_KMAX + q, (unsigned long long)r);
+      }
+    }
+  }
+}
+
+// ============================================================================ finalize
 __device__ __forceinline__ uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
   uint64_t r = 1 % p;
   b %= p;
@@ -300,7 +608,7 @@ __device__ __forceinline__ uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
   return r;
 }
 
-__global__ void rnw_finalize_kernel(int n, int NP, int64_t count, const int2* __restrict__ meta,
+__global__ void rnw_finalize_kernel(int n, int64_t count, const int2* __restrict__ meta,
                                     const unsigned long long* __restrict__ leaf_acc,
                                     const int64_t* __restrict__ coef, const int32_t* __restrict__ job,
                                     uint32_t* __restrict__ leaf_res, int32_t* __restrict__ leaf_k,
@@ -310,29 +618,25 @@ __global__ void rnw_finalize_kernel(int n, int NP, int64_t count, const int2* __
   const int64_t leaf = idx / SPERM_KMAX;
   const int q = (int)(idx % SPERM_KMAX);
   const int2 mt = meta[leaf];
-  const int k = mt.x, G = mt.y;
+  const int k = meta_k(mt);
   if (q == 0 && leaf_k) leaf_k[leaf] = k;
   if (q >= k) {
     if (leaf_res) leaf_res[idx] = 0u;
     return;
   }
-  // the primes of kPrimes (common.cuh), replicated for device code
-  const uint32_t primes[SPERM_KMAX] = {2147483647u, 2147483629u, 2147483587u, 2147483579u,
-                                       2147483563u, 2147483549u, 2147483543u, 2147483497u};
-  const uint64_t pq = primes[q];
+  const uint64_t pq = (uint64_t)c_p[q];
   uint64_t val;
   if (n == 0) {
     val = 1;
   } else {
+    // per = (-1)^(n-1) 2^(1-n) R^mexp S  (R = 2^32: Montgomery factors of the kernel)
     const uint64_t S = (uint64_t)(leaf_acc[leaf * SPERM_KMAX + q] % pq);
-    const int NG = NP / G;
-    const uint64_t inv2 = (pq + 1) / 2;
-    uint64_t f = powmod(inv2, (uint64_t)(n - 1), pq);
-    f = f * powmod(((uint64_t)1 << 32) % pq, (uint64_t)(NG - 1), pq) % pq;
+    uint64_t f = powmod((pq + 1) / 2, (uint64_t)(n - 1), pq);
+    f = f * powmod(((uint64_t)1 << 32) % pq, (uint64_t)mt.y, pq) % pq;
     if ((n - 1) & 1) f = (pq - f) % pq;
     val = S * f % pq;
   }
-  int64_t cf = coef ? coef[leaf] : 1;
+  const int64_t cf = coef ? coef[leaf] : 1;
   int64_t cm = cf % (int64_t)pq;
   if (cm < 0) cm += (int64_t)pq;
   val = val * (uint64_t)cm % pq;
@@ -347,35 +651,136 @@ __global__ void reduce_mod_kernel(const unsigned long long* __restrict__ acc, in
                                   uint32_t* __restrict__ out) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= rows * SPERM_KMAX) return;
-  const uint32_t primes[SPERM_KMAX] = {2147483647u, 2147483629u, 2147483587u, 2147483579u,
-                                       2147483563u, 2147483549u, 2147483543u, 2147483497u};
-  out[idx] = (uint32_t)(acc[idx] % primes[idx % SPERM_KMAX]);
+  out[idx] = (uint32_t)(acc[idx] % (unsigned long long)c_p[idx % SPERM_KMAX]);
+}
+
+// evaluation-order leaf ids, their plan keys, and the per-key histogram
+__global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order, const int2* __restrict__ meta,
+                                uint8_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int32_t leaf = order ? order[i] : (int32_t)i;
+  const int2 mt = meta[leaf];
+  const int plan = meta_plan(mt);
+  const int key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
+  keys[i] = (uint8_t)key;
+  ids[i] = leaf;
+  atomicAdd(hist + key, 1);
+}
+
+// ============================================================================ launch helpers
+struct Launch {
+  const int32_t* mats;
+  int n, m, cbits;
+  const int32_t* leaves;
+  int64_t nleaves;
+  const int2* meta;
+  const int8_t* perm;
+  unsigned long long* queue;
+  unsigned long long* leaf_acc;
+  cudaStream_t st;
+};
+
+template <typename K>
+int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bool tree) {
+  SPERM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRnwThreads, smem));
+  if (per_sm < 1) return set_error(SPERM_ERR_ARG, "sperm_permanent: kernel does not fit on an SM");
+  uint64_t grid = (uint64_t)sm_count() * per_sm;
+  const uint64_t blocks_needed = (total + kRnwThreads / 32 - 1) / (kRnwThreads / 32);
+  grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
+  SPERM_CUDA(cudaMemsetAsync(L.queue, 0, sizeof(unsigned long long), L.st));
+  TimingScope ts("rnw", L.st);
+  (void)tree;
+  kernel<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, L.m, L.cbits, L.leaves, L.meta, L.perm,
+                                                        L.queue, total, L.leaf_acc);
+  SPERM_LAUNCH_CHECK("rnw kernel");
+  return SPERM_OK;
 }
 
 template <int NP>
-int launch_main(const int32_t* mats, int n, int m, int cbits, const int32_t* order, const int2* meta,
-                unsigned long long* queue, uint64_t total, unsigned long long* leaf_acc, cudaStream_t st) {
-  using L = Layout<NP>;
-  const size_t smem = (size_t)L::kWords * 4 * (kRnwThreads / 32);
-  static bool attr_done = false;  // per process; single device per process in this framework
-  if (!attr_done) {
-    SPERM_CUDA(cudaFuncSetAttribute(rnw_main_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    attr_done = true;
-  }
+int launch_generic(const Launch& L) {
+  const int tb = L.n - 1;
+  const int m = std::max(0, std::min(kMaxLaneBits, tb - 5 - 6));
+  const int cbits = std::max(0, tb - 5 - m);
+  const uint64_t total = (uint64_t)L.nleaves << cbits;
+  const size_t smem = (size_t)GLayout<NP>::kWords * 4 * (kRnwThreads / 32);
+  auto kern = rnw_generic_kernel<NP>;
+  SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rnw_main_kernel<NP>, kRnwThreads, smem));
-  if (per_sm < 1) per_sm = 1;
-  uint64_t grid = (uint64_t)sm_count() * per_sm;
-  const uint64_t warps_needed = total;
-  const uint64_t blocks_needed = (warps_needed + kRnwThreads / 32 - 1) / (kRnwThreads / 32);
-  if (grid > blocks_needed) grid = blocks_needed;
-  if (grid < 1) grid = 1;
-  TimingScope ts("rnw", st);
-  rnw_main_kernel<NP><<<(unsigned)grid, kRnwThreads, smem, st>>>(mats, n, m, cbits, order, meta, queue, total,
-                                                                 leaf_acc, make_primes());
-  SPERM_LAUNCH_CHECK("rnw_main_kernel");
+  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRnwThreads, smem));
+  uint64_t grid = (uint64_t)sm_count() * std::max(per_sm, 1);
+  const uint64_t blocks_needed = (total + kRnwThreads / 32 - 1) / (kRnwThreads / 32);
+  grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
+  SPERM_CUDA(cudaMemsetAsync(L.queue, 0, sizeof(unsigned long long), L.st));
+  TimingScope ts("rnw", L.st);
+  kern<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, m, cbits, L.leaves, L.meta, L.queue, total,
+                                                    L.leaf_acc);
+  SPERM_LAUNCH_CHECK("rnw_generic_kernel");
   return SPERM_OK;
+}
+
+template <int NFIX, int PLAN>
+int launch_tree(const Launch& L) {
+  constexpr int B = plan_b1(PLAN) + plan_b2(PLAN);
+  constexpr int NS = B * KS, NRT = NS + NFIX;
+  const int tb = L.n - 1;
+  const int m = std::max(B, std::min(kMaxLaneBits, tb - 5 - 6));
+  if (m > tb - 5) return set_error(SPERM_ERR_ARG, "sperm_permanent: leaf too small for the tree plan");
+  const int cbits = tb - 5 - m;
+  const uint64_t total = (uint64_t)L.nleaves << cbits;
+  const TreeSmem ts = tree_smem(NRT, NS, L.n, B);
+  const size_t smem = (size_t)ts.words * 4 * (kRnwThreads / 32);
+  Launch l2 = L;
+  l2.m = m;
+  l2.cbits = cbits;
+  return launch_persistent(rnw_tree_kernel<NFIX, PLAN>, smem, l2, total, true);
+}
+
+template <int PLAN>
+int launch_tree_nfix(int fi, const Launch& L) {
+  switch (fi) {
+    case 0: return launch_tree<nfix_of(0), PLAN>(L);
+    case 1: return launch_tree<nfix_of(1), PLAN>(L);
+    case 2: return launch_tree<nfix_of(2), PLAN>(L);
+    case 3: return launch_tree<nfix_of(3), PLAN>(L);
+    case 4: return launch_tree<nfix_of(4), PLAN>(L);
+    case 5: return launch_tree<nfix_of(5), PLAN>(L);
+    default: return launch_tree<nfix_of(6), PLAN>(L);
+  }
+}
+
+int launch_key(int key, int NPg, const Launch& L) {
+  if (key == 0) {
+    switch (NPg) {
+      case 8: return launch_generic<8>(L);
+      case 16: return launch_generic<16>(L);
+      case 24: return launch_generic<24>(L);
+      case 32: return launch_generic<32>(L);
+      case 40: return launch_generic<40>(L);
+      case 48: return launch_generic<48>(L);
+      default: return set_error(SPERM_ERR_ARG, "sperm_permanent: unsupported order");
+    }
+  }
+  const int plan = key / 8, fi = key % 8;
+  switch (plan) {
+    case 1: return launch_tree_nfix<1>(fi, L);
+    case 2: return launch_tree_nfix<2>(fi, L);
+    case 3: return launch_tree_nfix<3>(fi, L);
+    case 4: return launch_tree_nfix<4>(fi, L);
+    case 5: return launch_tree_nfix<5>(fi, L);
+    default: return set_error(SPERM_ERR_ARG, "sperm_permanent: bad plan key");
+  }
+}
+
+// First tree plan the prep pass may choose (0 = generic kernel only).  Testing / A-B
+// measurements only: SPERM_RNW_PLAN_MIN=<p> restricts the plans to p..5.
+int first_plan() {
+  const char* e = getenv("SPERM_RNW_PLAN_MIN");
+  if (!e || !e[0]) return 1;
+  const int p = atoi(e);
+  return (p >= 0 && p < kNumPlans) ? p : 1;
 }
 
 }  // namespace
@@ -410,64 +815,88 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   if (count == 0) return SPERM_OK;
   if (n > 0 && !d_mats) return set_error(SPERM_ERR_ARG, "sperm_permanent: d_mats is NULL");
   if (d_job_acc && d_job && num_jobs <= 0) return set_error(SPERM_ERR_ARG, "sperm_permanent: num_jobs");
-  const int NP = n <= 8 ? 8 : ((n + 7) / 8) * 8;
+  const int NPg = n <= 8 ? 8 : ((n + 7) / 8) * 8;
 
+  // workspace (stream-ordered): meta | leaf_acc | perm | keys, ids, sorted keys/ids | queue, err, hist
   int2* meta = nullptr;
   unsigned long long* leaf_acc = nullptr;
-  unsigned long long* queue = nullptr;
-  int* err = nullptr;
-  SPERM_CUDA(cudaMallocAsync((void**)&meta, sizeof(int2) * count, st));
-  SPERM_CUDA(cudaMallocAsync((void**)&leaf_acc, sizeof(unsigned long long) * count * SPERM_KMAX, st));
-  SPERM_CUDA(cudaMallocAsync((void**)&queue, sizeof(unsigned long long) + sizeof(int) * 4, st));
-  err = reinterpret_cast<int*>(queue + 1);
-  SPERM_CUDA(cudaMemsetAsync(leaf_acc, 0, sizeof(unsigned long long) * count * SPERM_KMAX, st));
-  SPERM_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long) + sizeof(int) * 4, st));
-  int rc = SPERM_OK;
+  int8_t* perm = nullptr;
+  uint8_t* keys = nullptr;
+  int32_t* ids = nullptr;
+  int* small = nullptr;  // [0..1] queue (u64), [2] err, [4..4+kNumKeys) hist
+  void* sort_tmp = nullptr;
   auto cleanup = [&]() {
     cudaFreeAsync(meta, st);
     cudaFreeAsync(leaf_acc, st);
-    cudaFreeAsync(queue, st);
+    cudaFreeAsync(perm, st);
+    cudaFreeAsync(keys, st);
+    cudaFreeAsync(ids, st);
+    cudaFreeAsync(small, st);
+    if (sort_tmp) cudaFreeAsync(sort_tmp, st);
   };
+#define SPERM_TRY(call)                                 \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) { cleanup(); return cuda_check(e_, #call); } \
+  } while (0)
+  SPERM_TRY(cudaMallocAsync((void**)&meta, sizeof(int2) * count, st));
+  SPERM_TRY(cudaMallocAsync((void**)&leaf_acc, sizeof(unsigned long long) * count * SPERM_KMAX, st));
+  SPERM_TRY(cudaMallocAsync((void**)&perm, (size_t)kPermW * count, st));
+  SPERM_TRY(cudaMallocAsync((void**)&keys, 2 * (size_t)count, st));
+  SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
+  SPERM_TRY(cudaMallocAsync((void**)&small, sizeof(int) * (4 + kNumKeys), st));
+  SPERM_TRY(cudaMemsetAsync(leaf_acc, 0, sizeof(unsigned long long) * count * SPERM_KMAX, st));
+  SPERM_TRY(cudaMemsetAsync(small, 0, sizeof(int) * (4 + kNumKeys), st));
+  unsigned long long* queue = reinterpret_cast<unsigned long long*>(small);
+  int* err = small + 2;
+  int* hist = small + 4;
   {
     TimingScope ts("rnw_prep", st);
     const int64_t threads = count * 32;
-    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_mats, n, NP, count, d_coef,
-                                                                       min_primes, meta, err);
+    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_mats, n, NPg, count, d_coef, min_primes,
+                                                                       first_plan(), meta, perm, err);
+    SPERM_TRY(cudaGetLastError());
+    rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist);
+    SPERM_TRY(cudaGetLastError());
   }
-  cudaError_t le = cudaGetLastError();
-  if (le != cudaSuccess) { cleanup(); return cuda_check(le, "rnw_prep_kernel"); }
-  int herr = 0;
-  le = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (le == cudaSuccess) le = cudaStreamSynchronize(st);
-  if (le != cudaSuccess) { cleanup(); return cuda_check(le, "rnw_prep readback"); }
-  if (herr & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
-  if (herr & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
-
+  int hsmall[4 + kNumKeys];
+  SPERM_TRY(cudaMemcpyAsync(hsmall, small, sizeof(hsmall), cudaMemcpyDeviceToHost, st));
+  SPERM_TRY(cudaStreamSynchronize(st));
+  if (hsmall[2] & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
+  if (hsmall[2] & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
+  const int* h_hist = hsmall + 4;
+  int nonzero_keys = 0;
+  for (int q = 0; q < kNumKeys; ++q) nonzero_keys += h_hist[q] > 0;
+  // leaves grouped by plan key, evaluation order kept inside each group (stable sort)
+  const int32_t* sorted = ids;
+  if (nonzero_keys > 1) {
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 6, st);
+    SPERM_TRY(cudaMallocAsync(&sort_tmp, tmp_bytes, st));
+    SPERM_TRY(cub::DeviceRadixSort::SortPairs(sort_tmp, tmp_bytes, keys, keys + count, ids, ids + count,
+                                              (int)count, 0, 6, st));
+    sorted = ids + count;
+  }
+  int rc = SPERM_OK;
   if (n > 0) {
-    const int tb = n - 1;  // log2 of the number of terms
-    int m = std::max(0, std::min(kMaxLaneBits, tb - 5 - 6));
-    int cbits = std::max(0, tb - 5 - m);
-    const uint64_t total = (uint64_t)count << cbits;
-    switch (NP) {
-      case 8: rc = launch_main<8>(d_mats, n, m, cbits, d_order, meta, queue, total, leaf_acc, st); break;
-      case 16: rc = launch_main<16>(d_mats, n, m, cbits, d_order, meta, queue, total, leaf_acc, st); break;
-      case 24: rc = launch_main<24>(d_mats, n, m, cbits, d_order, meta, queue, total, leaf_acc, st); break;
-      case 32: rc = launch_main<32>(d_mats, n, m, cbits, d_order, meta, queue, total, leaf_acc, st); break;
-      case 40: rc = launch_main<40>(d_mats, n, m, cbits, d_order, meta, queue, total, leaf_acc, st); break;
-      case 48: rc = launch_main<48>(d_mats, n, m, cbits, d_order, meta, queue, total, leaf_acc, st); break;
-      default: rc = set_error(SPERM_ERR_ARG, "sperm_permanent: unsupported order");
+    int64_t off = 0;
+    for (int key = 0; key < kNumKeys && rc == SPERM_OK; ++key) {
+      if (!h_hist[key]) continue;
+      Launch L{d_mats, n, 0, 0, sorted + off, h_hist[key], meta, perm, queue, leaf_acc, st};
+      rc = launch_key(key, NPg, L);
+      off += h_hist[key];
     }
-    if (rc != SPERM_OK) { cleanup(); return rc; }
   }
+  if (rc != SPERM_OK) { cleanup(); return rc; }
   {
     TimingScope ts("rnw_finalize", st);
     const int64_t tot = count * SPERM_KMAX;
     rnw_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        n, NP, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k,
-        (unsigned long long*)d_job_acc, num_jobs);
+        n, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k, (unsigned long long*)d_job_acc, num_jobs);
   }
-  le = cudaGetLastError();
+  cudaError_t le = cudaGetLastError();
   cleanup();
+#undef SPERM_TRY
   if (le != cudaSuccess) return cuda_check(le, "rnw_finalize_kernel");
-  return rc;
+  return SPERM_OK;
 }

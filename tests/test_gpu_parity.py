@@ -209,3 +209,43 @@ def test_pipeline_c60_leaf16():
     a = truncated_icosahedron()
     r = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
     assert r.value == golden("C60_truncated_icosahedron")
+
+
+# ------------------------------------------------------------------ R-NW kernel variants
+def _plans_agree(mats, want):
+    """Every tree plan (forced via SPERM_RNW_PLAN_MIN) and the generic kernel agree with the oracle."""
+    for pmin in ("1", "2", "3", "4", "5", "0"):
+        os.environ["SPERM_RNW_PLAN_MIN"] = pmin
+        try:
+            got = gpu_per(mats)
+        finally:
+            os.environ.pop("SPERM_RNW_PLAN_MIN", None)
+        assert got == want, pmin
+
+
+def test_rnw_tree_plans_3regular():
+    for n, seed in ((12, 1), (17, 2), (20, 3), (26, 4)):
+        mats = random_3perm_batch(12, n, seed=seed)
+        _plans_agree(mats, [h_per(m) for m in mats])
+
+
+def test_rnw_tree_plans_fullerene_leaves():
+    """Leaves of the C60 expansion (merged entries, uneven row/column counts)."""
+    a = truncated_icosahedron()
+    sets = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=8)
+    lv = pipeline.expand_to_leaves(sets[0], 24)[0]
+    idx = torch.arange(0, lv.count, max(1, lv.count // 16), device="cuda")[:16]
+    mats = lv.mats.index_select(0, idx).cpu().numpy()
+    _plans_agree(mats, [h_per(m) for m in mats])
+
+
+def test_rnw_tree_plans_signed_sparse():
+    rng = np.random.default_rng(12)
+    mats = []
+    for _ in range(10):
+        n = int(rng.integers(14, 23))
+        a = random_3perm(n, rng) * rng.integers(-5, 6, size=(n, n))
+        a[np.arange(n), np.arange(n)] += rng.integers(1, 3, size=n)
+        mats.append(a)
+    for a in mats:
+        _plans_agree(a[None], [h_per(a)])

@@ -1,0 +1,82 @@
+"""Summarise ncu outputs into small text files for profiles/ (run here, no GPU).
+
+    python tools/ncu_summary.py launches <launches.csv>          # per-kernel share of the step
+    python tools/ncu_summary.py report <file.ncu-rep> [...]      # key counters of a --set full capture
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    "gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "launch__occupancy_limit_registers", "launch__shared_mem_per_block_dynamic",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "smsp__average_warp_latency_issue_stalled_short_scoreboard", "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    t, c = defaultdict(float), defaultdict(int)
+    for r in rows[hdr + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", ""))
+        v = v / 1e3 if r[ui] == "ns" else (v * 1e3 if r[ui] == "ms" else v)
+        name = r[ki].split("(")[0]
+        t[name] += v
+        c[name] += 1
+    tot = sum(t.values())
+    out = [f"# ncu --metrics gpu__time_duration.sum --clock-control none ({path}); cold-cache, serialised",
+           f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s}"]
+    for k in sorted(t, key=lambda k: -t[k]):
+        out.append(f"{k[-70:]:70s} {c[k]:8d} {t[k]:12.1f} {100 * t[k] / tot:6.1f}%")
+    return "\n".join(out)
+
+
+def report(path):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, units = rows[0], rows[1]
+    out = [f"# ncu --set full summary of {path}"]
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        out.append(f"## {name[:120]}")
+        for k in KEYS:
+            if k in h:
+                i = h.index(k)
+                out.append(f"{k:80s} {r[i]:>20s} {units[i]}")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        print(launches(sys.argv[2]))
+    else:
+        print("\n\n".join(report(p) for p in sys.argv[2:]))
