@@ -105,6 +105,12 @@ int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* 
  * order n: count * 2^(n-1) (as double; exact for n <= 53). */
 double sperm_rnw_terms(int n, int64_t count);
 
+/* Cumulative work model of the sperm_permanent calls since the last reset (host):
+ * Gray-code terms evaluated, multiply-pipe units (IMAD = 1, IMAD.WIDE / IMAD.HI = 2)
+ * and ALU-pipe lane-operations of the kernels' formulation, for the
+ * roofline.  reset != 0 clears the counters after reading. */
+int sperm_rnw_stats(double* h_terms, double* h_fma_units, double* h_alu_ops, int reset);
+
 /* Reduce accumulators mod the primes: out[r][q] = acc[r][q] mod p_q (device). */
 int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d_out, void* stream);
 
@@ -172,6 +178,10 @@ int sperm_schedule(const double* h_weights, int64_t count, int machines, int pol
                    uint64_t seed, int32_t* h_machine, int32_t* h_order, double* h_loads);
 
 /* ---------------------------------------------------------------- timing */
+/* Number of libsperm kernels launched (its own kernels; CUB scans/sorts it calls are not
+ * counted) since the last reset; reset != 0 clears the counter after reading. */
+int64_t sperm_launch_count(int reset);
+
 /* Device-side kernel timing: when enabled, the library records CUDA events
  * around each launch of its kernels (on the launching stream).
  * sperm_timing_get synchronizes those events and returns the summed

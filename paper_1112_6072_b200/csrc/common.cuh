@@ -38,5 +38,6 @@ struct TimingScope {
 };
 
 int sm_count();
+void count_launch(int k = 1);  // own-kernel launch counter (sperm_launch_count)
 
 }  // namespace sperm

@@ -303,6 +303,7 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   };
   {
     TimingScope ts("expand", st);
+    count_launch();
     expand_count_kernel<<<blocks, kExpThreads, 0, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err);
   }
   cudaError_t le = cudaGetLastError();
@@ -339,6 +340,7 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   }
   {
     TimingScope ts("expand", st);
+    count_launch();
     expand_emit_kernel<<<blocks, kExpThreads, 0, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
                                                        d_out_mats, d_out_coef, d_out_job, d_early_mats,
                                                        d_early_coef, d_early_job);

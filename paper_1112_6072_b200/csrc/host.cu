@@ -2,6 +2,7 @@
 // the improved Step 3 scheduler and the kernel timing registry.
 #include <algorithm>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -21,6 +22,9 @@ int set_error(int code, const std::string& msg) {
 int cuda_check(cudaError_t e, const char* what) {
   return set_error(SPERM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int k) { g_launches += k; }
 
 int sm_count() {
   static int cached = 0;
@@ -80,6 +84,11 @@ using namespace sperm;
 extern "C" {
 
 int sperm_version(void) { return 1; }
+
+int64_t sperm_launch_count(int reset) {
+  const long long v = reset ? g_launches.exchange(0) : g_launches.load();
+  return (int64_t)v;
+}
 
 const char* sperm_last_error(void) { return g_err.c_str(); }
 

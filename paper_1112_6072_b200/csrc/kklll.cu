@@ -107,6 +107,90 @@ __global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int6
   }
 }
 
+
+// Register variant for n <= NC <= 32: lane i holds row i of B (re/im in registers, every
+// index static because the elimination loop is fully unrolled).  Rows are never moved: each
+// lane tracks its row's current position, so "swap rows k and p" is a position exchange and
+// the pivot tie-break "first maximal |b_ik|^2" compares positions — the same arithmetic, in
+// the same order, as the shared-memory kernel and the reference.  The pivot row is
+// broadcast through shared memory (one 16-byte broadcast load per column).
+template <int NC>
+__global__ void __launch_bounds__(256) kklll_reg_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+                                                        const int32_t* __restrict__ ids, int trials, uint64_t seed,
+                                                        double* __restrict__ xout) {
+  __shared__ double2 prow_all[8][NC];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  double2* prow = prow_all[wib];
+  const int wpb = blockDim.x >> 5;
+  const double S32 = 0.8660254037844386;
+  const int64_t items = count * (int64_t)trials;
+  for (int64_t item = (int64_t)blockIdx.x * wpb + wib; item < items; item += (int64_t)gridDim.x * wpb) {
+    const int64_t job = item / trials;
+    const int trial = (int)(item % trials);
+    const int32_t* a = mats + job * (int64_t)n * n;
+    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
+    double re[NC], im[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      double r = 0.0, s = 0.0;
+      if (lane < n && j < n && a[lane * n + j] != 0) {
+        const int ri = root_index(key, (uint64_t)lane, (uint64_t)j);
+        r = ri == 0 ? 1.0 : -0.5;
+        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
+      }
+      re[j] = r;
+      im[j] = s;
+    }
+    int pos = lane;
+    bool active = lane < n;
+    double x = 1.0;
+    bool done = false;
+#pragma unroll NC
+    for (int k = 0; k < NC; ++k) {
+      if (done || k >= n) continue;
+      double bm = active ? __dadd_rn(__dmul_rn(re[k], re[k]), __dmul_rn(im[k], im[k])) : -1.0;
+      int bp = active ? pos : 0x7fffffff;
+      int bl = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, bm, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (om > bm || (om == bm && op < bp)) { bm = om; bp = op; bl = ol; }
+      }
+      const double d = bm;
+      if (d == 0.0) { x = 0.0; done = true; continue; }
+      if (lane == bl) pos = k;
+      else if (active && pos == k) pos = bp;
+      x = __dmul_rn(x, d);
+      if (k + 1 == n) { done = true; continue; }
+      if (lane == bl) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          if (j >= k) prow[j] = make_double2(re[j], im[j]);
+      }
+      __syncwarp();
+      active = active && pos > k;
+      if (active) {
+        const double2 pk = prow[k];
+        const double xr = re[k], xi = im[k];
+        const double lr = __ddiv_rn(__dadd_rn(__dmul_rn(xr, pk.x), __dmul_rn(xi, pk.y)), d);
+        const double li = __ddiv_rn(__dsub_rn(__dmul_rn(xi, pk.x), __dmul_rn(xr, pk.y)), d);
+#pragma unroll
+        for (int j = 1; j < NC; ++j) {  // j > k (static trip count keeps re/im in registers)
+          if (j <= k) continue;
+          const double2 u = prow[j];
+          re[j] = __dsub_rn(re[j], __dsub_rn(__dmul_rn(lr, u.x), __dmul_rn(li, u.y)));
+          im[j] = __dsub_rn(im[j], __dadd_rn(__dmul_rn(lr, u.y), __dmul_rn(li, u.x)));
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) xout[item] = x;
+  }
+}
+
 __global__ void kklll_mean_kernel(const double* __restrict__ xs, int64_t count, int trials,
                                   double* __restrict__ est) {
   const int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -132,22 +216,35 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
   if (!d_mats || !d_est) return set_error(SPERM_ERR_ARG, "sperm_estimate: NULL pointer");
   double* xs = d_trials_out;
   if (!xs) SPERM_CUDA(cudaMallocAsync((void**)&xs, sizeof(double) * count * trials, st));
-  const size_t per_warp = sizeof(double) * 2 * n * n;
-  int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
-  const size_t smem = per_warp * wpb;
-  SPERM_CUDA(cudaFuncSetAttribute(kklll_trial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_trial_kernel, wpb * 32, smem));
   const int64_t items = count * (int64_t)trials;
-  int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
-  const int64_t need = (items + wpb - 1) / wpb;
-  if (grid > need) grid = need;
-  {
+  if (n <= 32) {
+    const int NC = n <= 8 ? 8 : n <= 16 ? 16 : n <= 24 ? 24 : 32;
+    auto kern = NC == 8 ? kklll_reg_kernel<8> : NC == 16 ? kklll_reg_kernel<16> : NC == 24 ? kklll_reg_kernel<24>
+                                                                                          : kklll_reg_kernel<32>;
+    int per_sm = 0;
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+    grid = std::max<int64_t>(1, std::min(grid, (items + 7) / 8));
     TimingScope ts("kklll", st);
+    count_launch();
+    kern<<<(unsigned)grid, 256, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+  } else {
+    const size_t per_warp = sizeof(double) * 2 * n * n;
+    int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
+    const size_t smem = per_warp * wpb;
+    SPERM_CUDA(cudaFuncSetAttribute(kklll_trial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_trial_kernel, wpb * 32, smem));
+    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+    const int64_t need = (items + wpb - 1) / wpb;
+    if (grid > need) grid = need;
+    TimingScope ts("kklll", st);
+    count_launch();
     kklll_trial_kernel<<<(unsigned)grid, wpb * 32, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   }
   cudaError_t le = cudaGetLastError();
   if (le == cudaSuccess) {
+    count_launch();
     kklll_mean_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(xs, count, trials, d_est);
     le = cudaGetLastError();
   }

@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cub/device/device_radix_sort.cuh>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -656,7 +657,8 @@ __global__ void reduce_mod_kernel(const unsigned long long* __restrict__ acc, in
 
 // evaluation-order leaf ids, their plan keys, and the per-key histogram
 __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order, const int2* __restrict__ meta,
-                                uint8_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist) {
+                                uint8_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist,
+                                int* __restrict__ hist_k) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   const int32_t leaf = order ? order[i] : (int32_t)i;
@@ -666,6 +668,7 @@ __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order
   keys[i] = (uint8_t)key;
   ids[i] = leaf;
   atomicAdd(hist + key, 1);
+  atomicAdd(hist_k + key, meta_k(mt));
 }
 
 // ============================================================================ launch helpers
@@ -693,6 +696,7 @@ int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bo
   SPERM_CUDA(cudaMemsetAsync(L.queue, 0, sizeof(unsigned long long), L.st));
   TimingScope ts("rnw", L.st);
   (void)tree;
+  count_launch();
   kernel<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, L.m, L.cbits, L.leaves, L.meta, L.perm,
                                                         L.queue, total, L.leaf_acc);
   SPERM_LAUNCH_CHECK("rnw kernel");
@@ -715,6 +719,7 @@ int launch_generic(const Launch& L) {
   grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
   SPERM_CUDA(cudaMemsetAsync(L.queue, 0, sizeof(unsigned long long), L.st));
   TimingScope ts("rnw", L.st);
+  count_launch();
   kern<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, m, cbits, L.leaves, L.meta, L.queue, total,
                                                     L.leaf_acc);
   SPERM_LAUNCH_CHECK("rnw_generic_kernel");
@@ -783,10 +788,66 @@ int first_plan() {
   return (p >= 0 && p < kNumPlans) ? p : 1;
 }
 
+// ---------------------------------------------------------------------------- op model
+// Algorithmic 32-bit integer lane-operations of one evaluation, per the kernels' own
+// formulation.  IMAD.WIDE and IMAD.HI occupy the multiply (FMA) pipe twice
+// as long as IMAD (tools/microbench), so they count 2 "fma units"; IADD/LOP/shift count on
+// the ALU pipe.  Used for the roofline in bench.py; cross-checked against ncu pipe counters.
+struct RnwStats {
+  double terms = 0, fma = 0, alu = 0;
+};
+std::mutex g_stats_mu;
+RnwStats g_stats;
+
+void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k) {
+  const double T = std::ldexp(1.0, n - 1);
+  double fma_leaf = 0, alu_leaf = 0, fma_prime = 0, alu_prime = 0;  // per term
+  if (key == 0) {
+    int G = 1;  // group size is per leaf; model with the config-typical G of the bound (8 if NPg<=8)
+    (void)G;
+    // generic: NP adds, NP-NP/G products, (NP/G-1) smont per prime (6 units: WIDE 2, IMAD, HI 2,
+    // + IADD on alu), accumulate 2 alu per prime; G taken as 4 (weighted) - conservative
+    const int NG = NPg / 4;
+    alu_leaf = NPg;
+    fma_leaf = NPg - NG;
+    fma_prime = (NG - 1) * 5.0;
+    alu_prime = (NG - 1) * 1.0 + 2.0;
+  } else {
+    const int plan = key / 8, fi = key % 8;
+    const int B1 = plan_b1(plan), B2 = plan_b2(plan), B = B1 + B2, GF = plan_gf(plan);
+    const int NS = B * KS, NFIX = nfix_of(fi), S4 = (NS + NFIX + 3) / 4 * 4, NGF = NFIX / GF;
+    const double blk = std::ldexp(1.0, B), NZ = std::ldexp(1.0, B2);
+    // shared per block: W update (S4 adds), Q products and slot adds, X/Z trees, fixed groups
+    const double f_sh = B * 2.0 * (KS - 1) + (std::ldexp(1.0, B1 + 1) - 4) + (std::ldexp(1.0, B2 + 1) - 4) +
+                        NGF * (GF - 1.0);
+    const double a_sh = S4 + B * (double)KS + 8;
+    // per prime per block: (NGF-1+NZ) smont, NZ redc (IMAD + HI 2), 2^B IMAD.WIDE (2 each)
+    const double f_pr = (NGF - 1 + NZ) * 5.0 + NZ * 3.0 + blk * 2.0;
+    const double a_pr = (NGF - 1 + NZ) * 1.0 + NZ * 3.0 + 6.0;
+    fma_leaf = f_sh / blk;
+    alu_leaf = a_sh / blk;
+    fma_prime = f_pr / blk;
+    alu_prime = a_pr / blk;
+  }
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  g_stats.terms += T * leaves;
+  g_stats.fma += T * (fma_leaf * leaves + fma_prime * sum_k);
+  g_stats.alu += T * (alu_leaf * leaves + alu_prime * sum_k);
+}
+
 }  // namespace
 }  // namespace sperm
 
 using namespace sperm;
+
+extern "C" int sperm_rnw_stats(double* h_terms, double* h_fma_units, double* h_alu_ops, int reset) {
+  std::lock_guard<std::mutex> lk(g_stats_mu);
+  if (h_terms) *h_terms = g_stats.terms;
+  if (h_fma_units) *h_fma_units = g_stats.fma;
+  if (h_alu_ops) *h_alu_ops = g_stats.alu;
+  if (reset) g_stats = RnwStats();
+  return SPERM_OK;
+}
 
 extern "C" double sperm_rnw_terms(int n, int64_t count) {
   if (n <= 0) return (double)count;
@@ -797,6 +858,7 @@ extern "C" int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d
   if (rows < 0 || (rows > 0 && (!d_acc || !d_out))) return set_error(SPERM_ERR_ARG, "sperm_reduce_mod: bad args");
   if (rows == 0) return SPERM_OK;
   const int64_t tot = rows * SPERM_KMAX;
+  count_launch();
   reduce_mod_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       (const unsigned long long*)d_acc, rows, d_out);
   SPERM_LAUNCH_CHECK("reduce_mod_kernel");
@@ -823,7 +885,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   int8_t* perm = nullptr;
   uint8_t* keys = nullptr;
   int32_t* ids = nullptr;
-  int* small = nullptr;  // [0..1] queue (u64), [2] err, [4..4+kNumKeys) hist
+  int* small = nullptr;  // [0..1] queue (u64), [2] err, [4..) hist, then hist_k
   void* sort_tmp = nullptr;
   auto cleanup = [&]() {
     cudaFreeAsync(meta, st);
@@ -844,27 +906,33 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   SPERM_TRY(cudaMallocAsync((void**)&perm, (size_t)kPermW * count, st));
   SPERM_TRY(cudaMallocAsync((void**)&keys, 2 * (size_t)count, st));
   SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
-  SPERM_TRY(cudaMallocAsync((void**)&small, sizeof(int) * (4 + kNumKeys), st));
+  SPERM_TRY(cudaMallocAsync((void**)&small, sizeof(int) * (4 + 2 * kNumKeys), st));
   SPERM_TRY(cudaMemsetAsync(leaf_acc, 0, sizeof(unsigned long long) * count * SPERM_KMAX, st));
-  SPERM_TRY(cudaMemsetAsync(small, 0, sizeof(int) * (4 + kNumKeys), st));
+  SPERM_TRY(cudaMemsetAsync(small, 0, sizeof(int) * (4 + 2 * kNumKeys), st));
   unsigned long long* queue = reinterpret_cast<unsigned long long*>(small);
   int* err = small + 2;
   int* hist = small + 4;
   {
     TimingScope ts("rnw_prep", st);
     const int64_t threads = count * 32;
+    count_launch();
     rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_mats, n, NPg, count, d_coef, min_primes,
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
-    rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist);
+    count_launch();
+    rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist, hist + kNumKeys);
     SPERM_TRY(cudaGetLastError());
   }
-  int hsmall[4 + kNumKeys];
+  int hsmall[4 + 2 * kNumKeys];
   SPERM_TRY(cudaMemcpyAsync(hsmall, small, sizeof(hsmall), cudaMemcpyDeviceToHost, st));
   SPERM_TRY(cudaStreamSynchronize(st));
   if (hsmall[2] & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
   if (hsmall[2] & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
   const int* h_hist = hsmall + 4;
+  if (n > 0) {
+    for (int key = 0; key < kNumKeys; ++key)
+      if (h_hist[key]) record_stats(key, NPg, n, h_hist[key], hsmall[4 + kNumKeys + key]);
+  }
   int nonzero_keys = 0;
   for (int q = 0; q < kNumKeys; ++q) nonzero_keys += h_hist[q] > 0;
   // leaves grouped by plan key, evaluation order kept inside each group (stable sort)
@@ -891,6 +959,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   {
     TimingScope ts("rnw_finalize", st);
     const int64_t tot = count * SPERM_KMAX;
+    count_launch();
     rnw_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
         n, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k, (unsigned long long*)d_job_acc, num_jobs);
   }

@@ -42,10 +42,12 @@ _SIGS = {
     "sperm_crt": (_I, [_P, _I, _P, _I, _P]),
     "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _P, _P, _P, _P]),
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
+    "sperm_rnw_stats": (_I, [_P, _P, _P, _I]),
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
     "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
+    "sperm_launch_count": (_I64, [_I]),
     "sperm_timing_enable": (None, [_I]),
     "sperm_timing_reset": (None, []),
     "sperm_timing_get": (_I, [ctypes.c_char_p, _P, _P]),
@@ -152,6 +154,13 @@ def sperm_rnw_terms(n: int, count: int) -> float:
     return float(lib().sperm_rnw_terms(int(n), int(count)))
 
 
+def sperm_rnw_stats(reset: bool = False):
+    """(terms, fma_units, alu_ops) of the sperm_permanent calls since the last reset."""
+    t, f, a = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().sperm_rnw_stats(ctypes.byref(t), ctypes.byref(f), ctypes.byref(a), 1 if reset else 0))
+    return t.value, f.value, a.value
+
+
 def sperm_reduce_mod(acc, stream=None):
     import torch
     acc = _dev(acc, torch.int64)
@@ -236,6 +245,10 @@ def sperm_schedule(weights, machines: int, policy: str = "estimate", seed: int =
 
 
 # --------------------------------------------------------------------- timing
+def sperm_launch_count(reset: bool = False) -> int:
+    return int(lib().sperm_launch_count(1 if reset else 0))
+
+
 def sperm_timing_enable(on: bool = True):
     lib().sperm_timing_enable(1 if on else 0)
 
