@@ -115,7 +115,7 @@ __global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int6
 // the same order, as the shared-memory kernel and the reference.  The pivot row is
 // broadcast through shared memory (one 16-byte broadcast load per column).
 template <int NC>
-__global__ void __launch_bounds__(256) kklll_reg_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+__global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
                                                         const int32_t* __restrict__ ids, int trials, uint64_t seed,
                                                         double* __restrict__ xout) {
   __shared__ double2 prow_all[8][NC];
@@ -130,17 +130,29 @@ __global__ void __launch_bounds__(256) kklll_reg_kernel(const int32_t* __restric
     const int trial = (int)(item % trials);
     const int32_t* a = mats + job * (int64_t)n * n;
     const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
+    // Step 1: the lane's row of B.  Only the row's nonzeros draw a root (one round per
+    // nonzero, warp-uniform trip count), then land in their static register slot.
+    uint32_t nzmask = 0;
+    if (lane < n) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j)
+        if (j < n && a[lane * n + j] != 0) nzmask |= 1u << j;
+    }
     double re[NC], im[NC];
 #pragma unroll
-    for (int j = 0; j < NC; ++j) {
+    for (int j = 0; j < NC; ++j) re[j] = im[j] = 0.0;
+    while (__any_sync(0xffffffffu, nzmask != 0)) {
+      const int jn = nzmask ? __ffs(nzmask) - 1 : -1;
+      nzmask &= nzmask - 1;
       double r = 0.0, s = 0.0;
-      if (lane < n && j < n && a[lane * n + j] != 0) {
-        const int ri = root_index(key, (uint64_t)lane, (uint64_t)j);
+      if (jn >= 0) {
+        const int ri = root_index(key, (uint64_t)lane, (uint64_t)jn);
         r = ri == 0 ? 1.0 : -0.5;
         s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
       }
-      re[j] = r;
-      im[j] = s;
+#pragma unroll
+      for (int j = 0; j < NC; ++j)
+        if (j == jn) { re[j] = r; im[j] = s; }
     }
     int pos = lane;
     bool active = lane < n;
@@ -149,17 +161,18 @@ __global__ void __launch_bounds__(256) kklll_reg_kernel(const int32_t* __restric
 #pragma unroll NC
     for (int k = 0; k < NC; ++k) {
       if (done || k >= n) continue;
-      double bm = active ? __dadd_rn(__dmul_rn(re[k], re[k]), __dmul_rn(im[k], im[k])) : -1.0;
-      int bp = active ? pos : 0x7fffffff;
-      int bl = lane;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double om = __shfl_xor_sync(0xffffffffu, bm, o);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        if (om > bm || (om == bm && op < bp)) { bm = om; bp = op; bl = ol; }
-      }
-      const double d = bm;
+      // pivot: maximal |b_ik|^2 over active rows, first (lowest position) on ties.  A
+      // non-negative double orders like its bit pattern, so warp max = two 32-bit REDUX.
+      const double mag = active ? __dadd_rn(__dmul_rn(re[k], re[k]), __dmul_rn(im[k], im[k])) : 0.0;
+      const unsigned mh = active ? (unsigned)__double2hiint(mag) : 0u;
+      const unsigned ml = active ? (unsigned)__double2loint(mag) : 0u;
+      const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
+      const bool c1 = active && mh == bh;
+      const unsigned bl_ = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
+      const bool c2 = c1 && ml == bl_;
+      const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)pos : 0xffffffffu);
+      const int bl = __ffs(__ballot_sync(0xffffffffu, c2 && pos == bp)) - 1;
+      const double d = __hiloint2double((int)bh, (int)bl_);
       if (d == 0.0) { x = 0.0; done = true; continue; }
       if (lane == bl) pos = k;
       else if (active && pos == k) pos = bp;
@@ -222,12 +235,12 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     auto kern = NC == 8 ? kklll_reg_kernel<8> : NC == 16 ? kklll_reg_kernel<16> : NC == 24 ? kklll_reg_kernel<24>
                                                                                           : kklll_reg_kernel<32>;
     int per_sm = 0;
-    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
     int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
-    grid = std::max<int64_t>(1, std::min(grid, (items + 7) / 8));
+    grid = std::max<int64_t>(1, std::min(grid, (items + 3) / 4));
     TimingScope ts("kklll", st);
     count_launch();
-    kern<<<(unsigned)grid, 256, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+    kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else {
     const size_t per_warp = sizeof(double) * 2 * n * n;
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));

@@ -185,7 +185,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     for (int pl = allow_tree; pl >= 1 && pl < kNumPlans && np > 0; ++pl) {
       const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
       if (np < B || n - 6 < B) continue;
-      // exact bounds: |X| < 2^(31-B1), |Z| < 2^30, fixed groups < 2^30
+      // exact bounds: |X| < 2^(31-B), |Z| < 2^30, fixed groups < 2^30
       auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
         if (x == 0 || y == 0) return 0;
         if (x > ((int64_t)1 << 40) / y) return (int64_t)1 << 40;
@@ -201,7 +201,8 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
         if (c < B1) X = sat_mul(X, q);
         else Z = sat_mul(Z, q);
       }
-      if (X >= ((int64_t)1 << (31 - B1)) || Z >= ((int64_t)1 << 30)) continue;
+      // |X| * 2^B < p_min keeps the block's sum of 2^B products X_u*Y_v below p*2^31 (one REDC)
+      if (X >= ((int64_t)1 << (31 - B)) || Z >= ((int64_t)1 << 30)) continue;
       const int nf = n - __popcll(slot_rows);
       int fi = 0;
       while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
@@ -569,18 +570,23 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_tree_kernel(
         int32_t pf = FG[0];
 #pragma unroll
         for (int g = 1; g < NGF; ++g) pf = smont(pf, FG[g], p, pinv);
-        int64_t blk = 0;
+        int32_t y[NZ];
 #pragma unroll
-        for (int v = 0; v < NZ; ++v) {
-          const int32_t y = smont(pf, Z[v], p, pinv);
-          int64_t t_even = 0, t_odd = 0;
+        for (int v = 0; v < NZ; ++v) y[v] = smont(pf, Z[v], p, pinv);
+        // one 32x32->64 multiply-add per term (X_u * Y_v); NX independent accumulator chains.
+        // |X| < 2^(31-B) (prep bound) keeps |sum of all 2^B terms| < p * 2^31 for one REDC.
+        int64_t acc[NX];
 #pragma unroll
-          for (int u = 0; u < NX; u += 2) {
-            t_even += (int64_t)X[u] * y;       // one term: X_u * Y_v
-            if (u + 1 < NX) t_odd += (int64_t)X[u + 1] * y;
-          }
-          blk += redc(t_even + t_odd, p, pinv);
+        for (int u = 0; u < NX; ++u) {
+          acc[u] = (int64_t)X[u] * y[0];
+#pragma unroll
+          for (int v = 1; v < NZ; ++v) acc[u] += (int64_t)X[u] * y[v];
         }
+#pragma unroll
+        for (int s = NX / 2; s >= 1; s >>= 1)
+#pragma unroll
+          for (int u = 0; u < s; ++u) acc[u] += acc[u + s];
+        const int64_t blk = redc(acc[0], p, pinv);
         sacc[q * 32 + lane] += neg ? -blk : blk;
       }
     }
@@ -684,6 +690,50 @@ struct Launch {
   cudaStream_t st;
 };
 
+// A per-process pool of non-blocking streams and reusable events for the plan groups.
+struct StreamPool {
+  std::mutex mu;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> events;
+  size_t next_event = 0;
+  cudaStream_t stream(int g) {
+    std::lock_guard<std::mutex> lk(mu);
+    while ((int)streams.size() <= g % 8) {
+      cudaStream_t s;
+      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      streams.push_back(s);
+    }
+    return streams[g % 8];
+  }
+  cudaEvent_t event() {  // round robin over 64 events (a call uses at most ~2 per group)
+    std::lock_guard<std::mutex> lk(mu);
+    if (events.size() < 64) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      events.push_back(e);
+      return e;
+    }
+    return events[next_event++ % events.size()];
+  }
+};
+StreamPool& stream_pool() {
+  static StreamPool p;
+  return p;
+}
+
+// Terms per lane 2^m: small enough that a group has >= ~8 work items per resident warp of the
+// GPU (fine-grained tail), at least mmin (the tree block size), at most 2^14 and such that a
+// leaf holds at least one 32-lane chunk.
+int choose_m(int n, int64_t nleaves, int mmin) {
+  const int tb = n - 1;
+  const double target_items = (double)sm_count() * 16.0 * 8.0;
+  const double per_lane = std::ldexp((double)nleaves, tb) / (32.0 * target_items);
+  int m = per_lane >= 1.0 ? (int)std::floor(std::log2(per_lane)) : 0;
+  m = std::min(m, kMaxLaneBits);
+  m = std::min(m, std::max(0, tb - 5));
+  return std::max(m, mmin);
+}
+
 template <typename K>
 int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bool tree) {
   SPERM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -693,8 +743,6 @@ int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bo
   uint64_t grid = (uint64_t)sm_count() * per_sm;
   const uint64_t blocks_needed = (total + kRnwThreads / 32 - 1) / (kRnwThreads / 32);
   grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
-  SPERM_CUDA(cudaMemsetAsync(L.queue, 0, sizeof(unsigned long long), L.st));
-  TimingScope ts("rnw", L.st);
   (void)tree;
   count_launch();
   kernel<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, L.m, L.cbits, L.leaves, L.meta, L.perm,
@@ -706,7 +754,7 @@ int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bo
 template <int NP>
 int launch_generic(const Launch& L) {
   const int tb = L.n - 1;
-  const int m = std::max(0, std::min(kMaxLaneBits, tb - 5 - 6));
+  const int m = choose_m(L.n, L.nleaves, tb >= 6 ? 1 : 0);
   const int cbits = std::max(0, tb - 5 - m);
   const uint64_t total = (uint64_t)L.nleaves << cbits;
   const size_t smem = (size_t)GLayout<NP>::kWords * 4 * (kRnwThreads / 32);
@@ -717,8 +765,6 @@ int launch_generic(const Launch& L) {
   uint64_t grid = (uint64_t)sm_count() * std::max(per_sm, 1);
   const uint64_t blocks_needed = (total + kRnwThreads / 32 - 1) / (kRnwThreads / 32);
   grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
-  SPERM_CUDA(cudaMemsetAsync(L.queue, 0, sizeof(unsigned long long), L.st));
-  TimingScope ts("rnw", L.st);
   count_launch();
   kern<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, m, cbits, L.leaves, L.meta, L.queue, total,
                                                     L.leaf_acc);
@@ -731,7 +777,7 @@ int launch_tree(const Launch& L) {
   constexpr int B = plan_b1(PLAN) + plan_b2(PLAN);
   constexpr int NS = B * KS, NRT = NS + NFIX;
   const int tb = L.n - 1;
-  const int m = std::max(B, std::min(kMaxLaneBits, tb - 5 - 6));
+  const int m = choose_m(L.n, L.nleaves, B);
   if (m > tb - 5) return set_error(SPERM_ERR_ARG, "sperm_permanent: leaf too small for the tree plan");
   const int cbits = tb - 5 - m;
   const uint64_t total = (uint64_t)L.nleaves << cbits;
@@ -822,8 +868,10 @@ void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k) {
                         NGF * (GF - 1.0);
     const double a_sh = S4 + B * (double)KS + 8;
     // per prime per block: (NGF-1+NZ) smont, NZ redc (IMAD + HI 2), 2^B IMAD.WIDE (2 each)
-    const double f_pr = (NGF - 1 + NZ) * 5.0 + NZ * 3.0 + blk * 2.0;
-    const double a_pr = (NGF - 1 + NZ) * 1.0 + NZ * 3.0 + 6.0;
+    // per prime per block: (NGF-1+NZ) smont, 2^B IMAD.WIDE (2 each), one REDC (IMAD + HI 2);
+    // ALU: smont/REDC subtractions, 2^B1 - 1 64-bit adds (2 each), accumulate
+    const double f_pr = (NGF - 1 + NZ) * 5.0 + 3.0 + blk * 2.0;
+    const double a_pr = (NGF - 1 + NZ) * 1.0 + 1.0 + 2.0 * (std::ldexp(1.0, B1) - 1) + 6.0;
     fma_leaf = f_sh / blk;
     alu_leaf = a_sh / blk;
     fma_prime = f_pr / blk;
@@ -906,10 +954,11 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   SPERM_TRY(cudaMallocAsync((void**)&perm, (size_t)kPermW * count, st));
   SPERM_TRY(cudaMallocAsync((void**)&keys, 2 * (size_t)count, st));
   SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
-  SPERM_TRY(cudaMallocAsync((void**)&small, sizeof(int) * (4 + 2 * kNumKeys), st));
+  SPERM_TRY(cudaMallocAsync((void**)&small, sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * kNumKeys, st));
   SPERM_TRY(cudaMemsetAsync(leaf_acc, 0, sizeof(unsigned long long) * count * SPERM_KMAX, st));
-  SPERM_TRY(cudaMemsetAsync(small, 0, sizeof(int) * (4 + 2 * kNumKeys), st));
-  unsigned long long* queue = reinterpret_cast<unsigned long long*>(small);
+  SPERM_TRY(cudaMemsetAsync(small, 0, sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * kNumKeys, st));
+  // per-group work counters after the histograms (8-byte aligned: 4 + 2*48 ints = 400 bytes)
+  unsigned long long* queue = reinterpret_cast<unsigned long long*>(small + 4 + 2 * kNumKeys);
   int* err = small + 2;
   int* hist = small + 4;
   {
@@ -947,12 +996,28 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   }
   int rc = SPERM_OK;
   if (n > 0) {
+    // One persistent launch per plan group, each on its own stream of a small pool forked
+    // from `st` (a later group's CTAs fill the SMs freed by an earlier group's tail), joined
+    // back into `st`.  Each group has its own work counter.
+    TimingScope ts("rnw", st);
+    StreamPool& pool = stream_pool();
+    cudaEvent_t fork = pool.event();
+    SPERM_TRY(cudaEventRecord(fork, st));
     int64_t off = 0;
+    int g = 0;
     for (int key = 0; key < kNumKeys && rc == SPERM_OK; ++key) {
       if (!h_hist[key]) continue;
-      Launch L{d_mats, n, 0, 0, sorted + off, h_hist[key], meta, perm, queue, leaf_acc, st};
+      cudaStream_t gs = nonzero_keys > 1 ? pool.stream(g) : st;
+      if (gs != st) SPERM_TRY(cudaStreamWaitEvent(gs, fork, 0));
+      Launch L{d_mats, n, 0, 0, sorted + off, h_hist[key], meta, perm, queue + key, leaf_acc, gs};
       rc = launch_key(key, NPg, L);
+      if (gs != st) {
+        cudaEvent_t join = pool.event();
+        SPERM_TRY(cudaEventRecord(join, gs));
+        SPERM_TRY(cudaStreamWaitEvent(st, join, 0));
+      }
       off += h_hist[key];
+      ++g;
     }
   }
   if (rc != SPERM_OK) { cleanup(); return rc; }
