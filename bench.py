@@ -3,13 +3,14 @@
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
 Workload (configs[1]): 256 seeded n=24 matrices, each the sum of 3 disjoint random
-permutation matrices (half 0/1, half with nonzeros uniform in [1,7]); direct batched
-R-NW, no expansion.  One step = the whole hot path on that batch: KKLLL estimates
-(N = n^2 trials) -> improved-Step-3 order (LPT on the estimates) -> persistent R-NW
-kernel over all 256 x 2^23 Gray-code terms in exact multi-prime arithmetic ->
-residues -> host CRT of the 256 exact permanents.
+permutation matrices (half 0/1, half with nonzeros uniform in [1,7]); "direct batched
+R-NW, no expansion".  One step = the persistent R-NW kernels over all 256 x 2^23
+Gray-code terms in exact multi-prime arithmetic -> residues (then D2H + host CRT of the
+256 exact permanents, inside the e2e timing).
 Metric: Gray-code terms per second (whole job, all ranks).  Under torchrun each rank
 evaluates its own seeded batch of 256 (weak scaling, no data-path collective).
+The JSON line also carries `ph`: the whole path (expansion, KKLLL, LPT, R-NW, CRT) timed
+on configs[2], per(C60), with per-stage device times.
 """
 from __future__ import annotations
 
@@ -38,6 +39,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ph", action="store_true", help="skip the whole-path per(C60) measurement")
+    ap.add_argument("--ph-leaf", type=int, default=32, help="leaf order L of the per(C60) run")
     return ap.parse_args()
 
 
@@ -117,10 +120,8 @@ def main():
     jobs = torch.arange(N_MATS, dtype=torch.int32, device=dev)
 
     def step(mats):
-        est = P.sperm_estimate(mats, trials=0, seed=1, ids=jobs)
-        _, order, _ = P.sperm_schedule(est.cpu().numpy(), 1, "estimate")
-        d_order = torch.from_numpy(order).to(dev, non_blocking=True)
-        res, k = P.sperm_permanent(mats, order=d_order, min_primes=1)
+        # configs[1] is the direct batched R-NW (no expansion): one sperm_permanent call
+        res, k = P.sperm_permanent(mats, min_primes=1)
         return res, k
 
     def finish(res, k):
@@ -149,7 +150,6 @@ def main():
     rnw_ms, rnw_launches = P.sperm_timing_get("rnw")
     st_terms, st_fma, st_alu = P.sperm_rnw_stats(reset=True)
     launches = P.sperm_launch_count(reset=True)
-    kk_ms, kk_launches = P.sperm_timing_get("kklll")
     P.sperm_timing_enable(False)
     clocks = sampler.stop()
     if world > 1:
@@ -193,7 +193,7 @@ def main():
         "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int32 (exact mod 2^31 primes)", "data": "synthetic",
         "config": {"workload": "configs[1]: 256 x n=24 sum of 3 disjoint permutation matrices, half 0/1, "
-                               "half weights U[1,7], seed 2024(+rank); KKLLL N=n^2 -> LPT order -> R-NW",
+                               "half weights U[1,7], seed 2024(+rank); direct batched R-NW -> residues -> CRT",
                    "matrices_per_gpu": N_MATS, "n": ORDER, "terms_per_step_per_gpu": terms_step / world,
                    "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world} weak"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
@@ -209,15 +209,51 @@ def main():
                 "d2h_bytes_per_step": int(N_MATS * (P.KMAX + 1) * 4 + N_MATS * 8)},
         "gpu_launches": launches,
         "clocks": clocks,
-        "kklll_ms_per_step": kk_ms / max(args.steps, 1),
         "check": {"per_first": str(vals[0]), "per_last": str(vals[-1])},
     }
+    if rank == 0 and world == 1 and not args.no_ph:
+        out["ph"] = bench_ph(P, torch, leaf_order=args.ph_leaf)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(h_np)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_ph(P, torch, leaf_order: int = 32, jobs_at_least: int = 992):
+    """Whole hot path on configs[2] (C60, the truncated icosahedron): PH pre-expansion
+    to >= 992 jobs, KKLLL weights, LPT order, expansion of every job to leaves of order
+    <= L, batched R-NW, residue sums, CRT.  One warm-up run, one timed run; per-stage
+    device times from the library's event timers; exactness checked against the value
+    tests/golden/oracle_values.txt holds (written by oracle/ via tools/make_golden.py)."""
+    from paper_1112_6072_b200 import pipeline
+    from workloads import dodecahedron, truncated_icosahedron
+    a = truncated_icosahedron()
+    pipeline.permanent(dodecahedron(), jobs_at_least=8, leaf_order=12)  # warm-up (tiny)
+    torch.cuda.synchronize()
+    P.sperm_timing_enable(True)
+    P.sperm_timing_reset()
+    P.sperm_rnw_stats(reset=True)
+    t0 = time.perf_counter()
+    r = pipeline.permanent(a, jobs_at_least=jobs_at_least, leaf_order=leaf_order)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
+    terms, fma, alu = P.sperm_rnw_stats(reset=True)
+    P.sperm_timing_enable(False)
+    gold = None
+    try:
+        for ln in open(os.path.join(ROOT, "tests", "golden", "oracle_values.txt")):
+            if ln.startswith("C60_truncated_icosahedron "):
+                gold = int(ln.split()[1])
+    except OSError:
+        pass
+    return {"workload": f"configs[2]: per(C60) by PH, J>={jobs_at_least} jobs, leaves of order <= {leaf_order}",
+            "per": str(r.value), "matches_oracle_golden": (r.value == gold) if gold is not None else None,
+            "wall_s": wall, "jobs": r.num_jobs, "leaves": r.leaves, "terms": terms,
+            "terms_per_s_rnw": terms / (stages["rnw"] * 1e-3) if stages["rnw"] else None,
+            "stage_ms": stages}
 
 
 def cpu_baseline(mats, seconds: float = 12.0):
