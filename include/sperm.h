@@ -58,6 +58,12 @@ uint32_t sperm_prime(int i);
  * (limbs >= k+1 suffices).  Garner's algorithm. */
 int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int* h_sign);
 
+/* Number of CRT primes that reconstruct per(A) of one HOST matrix h_mat [n][n] (host,
+ * synchronous): |per(A)| <= min(prod_i sum_j |a_ij|, prod_j sum_i |a_ij|), and for a 0/1
+ * matrix the Bregman-Minc bound prod_i (r_i!)^(1/r_i) (rows and columns).  SPERM_ERR_PRIMES
+ * if more than SPERM_KMAX primes would be needed. */
+int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
+
 /* ---------------------------------------------------------------- R-NW */
 /* sperm_permanent — batched exact permanents of the leaves of Algorithm
  * H_per ("return by R-NW(A)"), by Ryser's formula with the
@@ -80,8 +86,13 @@ int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int
  *  num_jobs   size of d_job_acc's first dimension (>= 1 when d_job_acc is set).
  *  min_primes every leaf uses at least this many primes (so that sums over
  *             leaves can be reconstructed); each leaf also uses as many as
- *             its own bound  |coef| * min(prod_i sum_j |a_ij|, prod_j sum_i |a_ij|)
- *             requires.  1 <= min_primes <= SPERM_KMAX.
+ *             its own bound |coef| * B(leaf) requires, B = the Bregman-Minc bound
+ *             prod_i (r_i!)^(1/r_i) for a 0/1 leaf, else min(prod_i sum_j |a_ij|,
+ *             prod_j sum_i |a_ij|).  1 <= min_primes <= SPERM_KMAX.
+ *  max_primes 0, or a cap (>= min_primes) on the primes per leaf: the caller
+ *             asserts that only sums it knows to be small (e.g. the total of a
+ *             nonnegative matrix) will be reconstructed, so an individual leaf
+ *             above the cap is then known only modulo the capped primes.
  *  d_leaf_res [count][SPERM_KMAX] uint32 out (device) or NULL:
  *             coef * per(leaf) mod p_q for q < d_leaf_k[m], 0 beyond.
  *  d_leaf_k   [count] int32 out (device) or NULL: primes used per leaf.
@@ -98,7 +109,7 @@ int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int
  * `stream` once after the bound pass). */
 int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* d_coef,
                     const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
-                    int min_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
+                    int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
                     uint64_t* d_job_acc, void* stream);
 
 /* Number of Gray-code terms sperm_permanent evaluates for `count` leaves of

@@ -85,6 +85,36 @@ extern "C" {
 
 int sperm_version(void) { return 1; }
 
+// Primes needed to reconstruct per(A) of one host matrix: |per(A)| <= min(prod of row abs
+// sums, prod of column abs sums) and, for a 0/1 matrix, the Bregman-Minc bound
+// prod_i (r_i!)^(1/r_i) (by rows and by columns).  Logarithms with a safety margin.
+int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k) {
+  if (!h_k || n < 0 || (n > 0 && !h_mat)) return set_error(SPERM_ERR_ARG, "sperm_bound_primes: bad arguments");
+  double lr = 0, lc = 0, br = 0, bc = 0;
+  bool binary = true, zero = false;
+  for (int i = 0; i < n; ++i) {
+    double r = 0, c = 0;
+    for (int j = 0; j < n; ++j) {
+      const int32_t u = h_mat[(size_t)i * n + j];
+      if (u != 0 && u != 1) binary = false;
+      r += std::fabs((double)u);
+      c += std::fabs((double)h_mat[(size_t)j * n + i]);
+    }
+    if (r == 0 || c == 0) zero = true;
+    if (r > 0) { lr += std::log2(r); br += std::lgamma(r + 1.0) / (r * std::log(2.0)); }
+    if (c > 0) { lc += std::log2(c); bc += std::lgamma(c + 1.0) / (c * std::log(2.0)); }
+  }
+  double lb = std::min(lr, lc);
+  if (binary) lb = std::min(lb, std::min(br, bc));
+  if (zero) lb = -1.0;
+  const double need = lb + 1.0 + 1e-9 * std::fabs(lb) + 1e-6;  // prod p > 2 * bound
+  int k = 1;
+  while (k <= SPERM_KMAX && 30.99999 * k <= need) ++k;
+  if (k > SPERM_KMAX) return set_error(SPERM_ERR_PRIMES, "sperm_bound_primes: bound needs more than 8 primes");
+  *h_k = k;
+  return SPERM_OK;
+}
+
 int64_t sperm_launch_count(int reset) {
   const long long v = reset ? g_launches.exchange(0) : g_launches.load();
   return (int64_t)v;

@@ -89,7 +89,7 @@ __device__ __forceinline__ int meta_G(int2 m) { return (m.x >> 24) & 0xff; }
 // rotations of the start column, the best (lowest lane on ties) wins; the first plan whose
 // exact-arithmetic bounds hold is taken.
 __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
-                                const int64_t* __restrict__ coef, int min_primes, int allow_tree,
+                                const int64_t* __restrict__ coef, int min_primes, int max_primes, int allow_tree,
                                 int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -102,14 +102,16 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   int64_t* R = sR[wib];
   unsigned long long* supp = sSupp[wib];
   int* cnt = sCnt[wib];
-  double lr = 0.0, lc = 0.0;
-  bool zero = false, range_bad = false;
+  double lr = 0.0, lc = 0.0, br = 0.0, bc = 0.0;  // log2 of row/col sum bounds, Bregman-Minc
+  bool zero = false, range_bad = false, binary = true;
   for (int i = lane; i < n; i += 32) {
     int64_t r = 0, c = 0;
     unsigned long long sm = 0;
     int nz = 0;
     for (int j = 0; j < n; ++j) {
-      r += llabs((long long)a[i * n + j]);
+      const int32_t u = a[i * n + j];
+      r += llabs((long long)u);
+      if (u != 0 && u != 1) binary = false;
       const int32_t v = a[j * n + i];
       c += llabs((long long)v);
       if (v != 0) { sm |= 1ull << j; ++nz; }
@@ -119,15 +121,29 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     cnt[i] = nz;
     if (r == 0 || c == 0) zero = true;
     if (r >= (1ll << 30)) range_bad = true;
-    if (r > 0) lr += log2((double)r);
-    if (c > 0) lc += log2((double)c);
+    if (r > 0) {
+      lr += log2((double)r);
+      br += lgamma((double)r + 1.0) / ((double)r * 0.6931471805599453);
+    }
+    if (c > 0) {
+      lc += log2((double)c);
+      bc += lgamma((double)c + 1.0) / ((double)c * 0.6931471805599453);
+    }
   }
   for (int o = 16; o; o >>= 1) {
     lr += __shfl_xor_sync(0xffffffffu, lr, o);
     lc += __shfl_xor_sync(0xffffffffu, lc, o);
+    br += __shfl_xor_sync(0xffffffffu, br, o);
+    bc += __shfl_xor_sync(0xffffffffu, bc, o);
   }
   zero = __any_sync(0xffffffffu, zero);
   range_bad = __any_sync(0xffffffffu, range_bad);
+  binary = __all_sync(0xffffffffu, binary);
+  // Bregman-Minc: per(A) <= prod_i (r_i!)^(1/r_i) for a 0/1 matrix (and by columns)
+  if (binary) {
+    lr = fmin(lr, br);
+    lc = fmin(lc, bc);
+  }
   __syncwarp();
 
   // ---- tree plan: greedy pick of up to 6 low columns with disjoint supports of <= 3 rows
@@ -160,10 +176,11 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     // need prod p_q > 2 * bound; each p_q > 2^30.99999; margin for log2 rounding
     const double need = lb + 1.0 + 1e-6 * fabs(lb) + 1e-6;
     int k = min_primes;
+    const int kcap = max_primes > 0 ? max_primes : SPERM_KMAX;
     while (k <= SPERM_KMAX && 30.99999 * k <= need) ++k;
-    if (k > SPERM_KMAX) {
-      atomicOr(err, 2);
-      k = SPERM_KMAX;
+    if (k > kcap) {
+      if (max_primes <= 0) atomicOr(err, 2);
+      k = kcap;
     }
     // generic: largest group size G in {8,4,2,1} with every group product of row bounds < 2^30
     int G = 1;
@@ -915,13 +932,15 @@ extern "C" int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d
 
 extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* d_coef,
                                const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
-                               int min_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
+                               int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
                                uint64_t* d_job_acc, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0 || n > SPERM_NMAX) return set_error(SPERM_ERR_ARG, "sperm_permanent: n out of range [0, 48]");
   if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_permanent: count < 0");
   if (min_primes < 1 || min_primes > SPERM_KMAX)
     return set_error(SPERM_ERR_ARG, "sperm_permanent: min_primes out of range");
+  if (max_primes != 0 && (max_primes < min_primes || max_primes > SPERM_KMAX))
+    return set_error(SPERM_ERR_ARG, "sperm_permanent: max_primes must be 0 or in [min_primes, 8]");
   if (count == 0) return SPERM_OK;
   if (n > 0 && !d_mats) return set_error(SPERM_ERR_ARG, "sperm_permanent: d_mats is NULL");
   if (d_job_acc && d_job && num_jobs <= 0) return set_error(SPERM_ERR_ARG, "sperm_permanent: num_jobs");
@@ -965,7 +984,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     TimingScope ts("rnw_prep", st);
     const int64_t threads = count * 32;
     count_launch();
-    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_mats, n, NPg, count, d_coef, min_primes,
+    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
     count_launch();

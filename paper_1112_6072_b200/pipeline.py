@@ -119,21 +119,9 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
 
 
 def bound_primes(a) -> int:
-    """Primes needed for |x| <= min(prod row abs sums, prod col abs sums) (host, exact ints).
-    Used to size the accumulators of the total; each leaf sizes itself on the device."""
-    a = np.abs(np.asarray(a, dtype=object))
-    rb, cb = 1, 1
-    for i in range(a.shape[0]):
-        rb *= int(sum(a[i]))
-        cb *= int(sum(a[:, i]))
-    b = min(rb, cb)
-    M, k = 1, 0
-    while M <= 2 * b + 1:
-        M *= S.sperm_prime(k)
-        k += 1
-        if k > S.KMAX:
-            raise S.SpermError(S.ERR_PRIMES, "bound needs more than 8 primes")
-    return max(k, 1)
+    """Primes needed to reconstruct per(A): host C (sperm_bound_primes) — the row/column
+    abs-sum bound, and Bregman-Minc for 0/1 matrices."""
+    return S.sperm_bound_primes(a)
 
 
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
@@ -148,6 +136,9 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     import torch.distributed as dist
     rank, world = (dist.get_rank(group), dist.get_world_size(group)) if group is not None else (0, 1)
     k_total = bound_primes(a)
+    # nonnegative A: every leaf term is >= 0, so each job value and the total lie in
+    # [0, per(A)] and k_total primes reconstruct all of them; leaves may be capped at k_total
+    nonneg = bool((np.asarray(a) >= 0).all())
     root = root_nodeset(a, device)
     jobsets = pre_expand(root, jobs_at_least, job_order)
     num_jobs = sum(s.count for s in jobsets)
@@ -179,7 +170,7 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
                 if lv.n > S.NMAX:
                     raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
                 S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
-                                  job_acc=acc)
+                                  max_primes=k_total if nonneg else 0, job_acc=acc)
                 leaves += lv.count
                 terms += S.sperm_rnw_terms(lv.n, lv.count)
     if world > 1:

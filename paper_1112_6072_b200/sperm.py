@@ -40,7 +40,8 @@ _SIGS = {
     "sperm_last_error": (ctypes.c_char_p, []),
     "sperm_prime": (ctypes.c_uint32, [_I]),
     "sperm_crt": (_I, [_P, _I, _P, _I, _P]),
-    "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _P, _P, _P, _P]),
+    "sperm_bound_primes": (_I, [_P, _I, _P]),
+    "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P]),
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
     "sperm_rnw_stats": (_I, [_P, _P, _P, _I]),
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
@@ -127,9 +128,18 @@ def sperm_crt(residues: Sequence[int], k: int) -> int:
     return sign.value * v
 
 
+def sperm_bound_primes(a) -> int:
+    """CRT primes that reconstruct per(A) of a host matrix (row/col sums, Bregman-Minc)."""
+    m = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    k = ctypes.c_int(0)
+    _check(lib().sperm_bound_primes(m.ctypes.data if m.size else None, int(m.shape[0]) if m.ndim == 2 else 0,
+                                    ctypes.byref(k)))
+    return k.value
+
+
 # --------------------------------------------------------------------- R-NW
 def sperm_permanent(mats, coef=None, order=None, job=None, num_jobs: int = 0, min_primes: int = 1,
-                    leaf_res=None, leaf_k=None, job_acc=None, stream=None):
+                    max_primes: int = 0, leaf_res=None, leaf_k=None, job_acc=None, stream=None):
     """Batched R-NW leaf permanents mod the CRT primes (see include/sperm.h).
 
     mats: int32 CUDA tensor [count, n, n].  Outputs are allocated if not given:
@@ -146,7 +156,8 @@ def sperm_permanent(mats, coef=None, order=None, job=None, num_jobs: int = 0, mi
     order = _dev(order, torch.int32)
     job = _dev(job, torch.int32)
     _check(lib().sperm_permanent(_ptr(mats), n, count, _ptr(coef), _ptr(order), _ptr(job), int(num_jobs),
-                                 int(min_primes), _ptr(leaf_res), _ptr(leaf_k), _ptr(job_acc), _stream(stream)))
+                                 int(min_primes), int(max_primes), _ptr(leaf_res), _ptr(leaf_k), _ptr(job_acc),
+                                 _stream(stream)))
     return leaf_res, leaf_k
 
 

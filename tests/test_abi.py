@@ -122,3 +122,27 @@ def test_cuda_entry_points_fail_loudly_without_device():
         pytest.skip("GPU present")
     with pytest.raises(TypeError):
         P.sperm_permanent(torch.zeros((1, 3, 3), dtype=torch.int32))
+
+
+def test_bound_primes_sufficient_and_tight():
+    """sperm_bound_primes: product of the primes > 2 * bound (oracle.crt bounds, exact ints),
+    and one prime fewer would not cover the bound."""
+    from oracle.crt import bregman_log2, row_sum_bound
+    from workloads import dodecahedron, paper_graph, random_3perm_batch, truncated_icosahedron
+    rng = np.random.default_rng(3)
+    mats = [dodecahedron(), truncated_icosahedron(), paper_graph("C100"), np.ones((7, 7), int),
+            np.zeros((3, 3), int)] + list(random_3perm_batch(256, 24, seed=2024)[[0, 1, 130, 131]])
+    mats += [rng.integers(-9, 10, size=(10, 10)) for _ in range(5)]
+    for a in mats:
+        k = P.sperm_bound_primes(a)
+        b = min(row_sum_bound(a), row_sum_bound(np.asarray(a).T))
+        lb = math.log2(b) if b > 0 else -1
+        if np.isin(a, (0, 1)).all() and b > 0:
+            lb = min(lb, bregman_log2(a), bregman_log2(np.asarray(a).T))
+        M = math.prod(P.primes(k))
+        assert math.log2(M) > lb + 1
+        if k > 1:
+            assert math.log2(math.prod(P.primes(k - 1))) <= lb + 1 + 1e-6
+    # C100: per = 149364113290700 (Table T12) < 2^48 needs 2 primes; Bregman 6^(100/3) -> 3
+    assert P.sperm_bound_primes(paper_graph("C100")) == 3
+    assert P.sperm_bound_primes(truncated_icosahedron()) == 2

@@ -249,3 +249,22 @@ def test_rnw_tree_plans_signed_sparse():
         mats.append(a)
     for a in mats:
         _plans_agree(a[None], [h_per(a)])
+
+
+def test_rnw_prime_count_bregman_and_cap():
+    """0/1 leaves size their prime count by Bregman-Minc (configs[1] 0/1 half: 1 prime);
+    max_primes caps it, leaving every residue correct modulo the primes kept."""
+    mats = random_3perm_batch(256, 24, seed=2024)[[0, 1, 2, 200, 201]]
+    res, k = P.sperm_permanent(dev(mats))
+    k = k.cpu().numpy()
+    assert list(k[:3]) == [1, 1, 1] and all(x >= 3 for x in k[3:])
+    want = [h_per(m) for m in mats]
+    assert P.residues_to_ints(res, k) == want
+    res2, k2 = P.sperm_permanent(dev(mats), min_primes=1, max_primes=2)
+    r2 = res2.cpu().numpy().view(np.uint32)
+    assert list(k2.cpu().numpy()) == [1, 1, 1, 2, 2]
+    for i, w in enumerate(want):
+        for q in range(int(k2[i])):
+            assert int(r2[i, q]) == w % P.sperm_prime(q)
+    with pytest.raises(P.SpermError):
+        P.sperm_permanent(dev(mats), min_primes=3, max_primes=2)
