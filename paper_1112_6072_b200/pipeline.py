@@ -124,6 +124,32 @@ def bound_primes(a) -> int:
     return S.sperm_bound_primes(a)
 
 
+def rank_positions(machine, order, rank: int) -> np.ndarray:
+    """Position of every job in this rank's queue (-1 if another rank's): the jobs LPT
+    dealt to `rank`, in the order they were dealt (non-increasing estimate, S1)."""
+    machine = np.asarray(machine)
+    order = np.asarray(order)
+    mine = order[machine[order] == rank].astype(np.int64)
+    pos = np.full(len(machine), -1, dtype=np.int64)
+    pos[mine] = np.arange(len(mine))
+    return pos
+
+
+def allreduce_accumulators(acc, group=None):
+    """Algorithm PH Step 4 across GPUs: one SUM all-reduce of the
+    [jobs + 1][8] residue accumulators (NCCL on GPUs).  Each rank added residues < 2^31
+    per leaf, so the int64 (wrap-around) sum equals the exact uint64 sum."""
+    import torch.distributed as dist
+    if group is not None and dist.get_world_size(group) > 1:
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    return acc
+
+
+def reconstruct(res, k: int):
+    """Host CRT (sperm_crt) of the reduced accumulators: (job values, total)."""
+    return [S.sperm_crt(res[j], k) for j in range(res.shape[0] - 1)], S.sperm_crt(res[-1], k)
+
+
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
               device="cuda") -> PHResult:
@@ -152,10 +178,7 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
         est[s.job.cpu().numpy()] = e
     machine, order, _ = S.sperm_schedule(est, world, policy, seed=seed)
     acc = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
-    # this rank's jobs in the order they were dealt (non-increasing estimate)
-    mine = np.array([j for j in order if machine[j] == rank], dtype=np.int64)
-    pos = np.full(num_jobs, -1, dtype=np.int64)
-    pos[mine] = np.arange(len(mine))
+    pos = rank_positions(machine, order, rank)
     leaves = 0
     terms = 0.0
     for s in jobsets:
@@ -173,11 +196,9 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
                                   max_primes=k_total if nonneg else 0, job_acc=acc)
                 leaves += lv.count
                 terms += S.sperm_rnw_terms(lv.n, lv.count)
-    if world > 1:
-        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    allreduce_accumulators(acc, group)
     res = S.sperm_reduce_mod(acc).cpu().numpy().view(np.uint32)
-    job_values = [S.sperm_crt(res[j], k_total) for j in range(num_jobs)]
-    value = S.sperm_crt(res[num_jobs], k_total)
+    job_values, value = reconstruct(res, k_total)
     return PHResult(value=value, job_values=job_values, num_jobs=num_jobs,
                     job_order_n={s.n: s.count for s in jobsets}, leaves=leaves, terms=terms,
                     estimates=est, machine=machine)

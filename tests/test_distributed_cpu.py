@@ -1,0 +1,85 @@
+"""Multi-rank host logic of the hot path on CPU (-m "not gpu"): world_size 2 over gloo.
+
+Each rank replicates the LPT schedule (host C++, sperm_schedule), takes the jobs dealt to
+it (pipeline.rank_positions), adds its jobs' residues to the [jobs + 1][8] accumulators,
+and one all-reduce (pipeline.allreduce_accumulators — NCCL on GPUs, gloo here) forms
+Algorithm PH Step 4; host CRT (pipeline.reconstruct) must give the exact total and every
+job value.  The per-job values come from the oracle (test infrastructure) in place of the
+GPU R-NW, so the test isolates the distributed logic."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_1112_6072_b200 as P
+from paper_1112_6072_b200 import pipeline
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, policy, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.hybrid import node_permanent, pre_expand, to_dense
+        from oracle.kklll import kklll_estimate
+        from workloads import dodecahedron
+        a = dodecahedron()
+        jobs = pre_expand(a, jobs_at_least=30)
+        J = len(jobs)
+        vals = [node_permanent(j) for j in jobs]
+        est = [kklll_estimate((np.array(to_dense(m, k)) != 0).astype(int), 16, 7, i)
+               for i, (c, m, k) in enumerate(jobs)]
+        machine, order, _ = P.sperm_schedule(est, world, policy, seed=5)
+        pos = pipeline.rank_positions(machine, order, rank)
+        k = P.sperm_bound_primes(a)
+        acc = torch.zeros((J + 1, P.KMAX), dtype=torch.int64)
+        for j in range(J):
+            if pos[j] >= 0:
+                for qq in range(k):
+                    r = vals[j] % P.sperm_prime(qq)
+                    acc[j, qq] += r
+                    acc[J, qq] += r
+        pipeline.allreduce_accumulators(acc, dist.group.WORLD)
+        red = np.zeros((J + 1, P.KMAX), dtype=np.uint32)
+        for qq in range(k):
+            red[:, qq] = (acc[:, qq].numpy() % P.sperm_prime(qq)).astype(np.uint32)
+        job_values, total = pipeline.reconstruct(red, k)
+        owned = torch.tensor((pos >= 0).astype(np.int64))
+        dist.all_reduce(owned)
+        sched = torch.tensor(np.asarray(machine, dtype=np.int64))
+        gathered = [torch.zeros_like(sched) for _ in range(world)]
+        dist.all_gather(gathered, sched)
+        q.put((rank, total, job_values == vals, bool((owned == 1).all()),
+               all(torch.equal(g, gathered[0]) for g in gathered)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", ["estimate", "natural", "random"])
+def test_two_rank_partition_and_residue_allreduce(policy):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, policy, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, total, jobs_ok, owned_once, same_sched in out:
+        assert total == 1392  # per(C20) (tests/golden/oracle_values.txt)
+        assert jobs_ok and owned_once and same_sched

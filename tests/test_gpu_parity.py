@@ -205,6 +205,24 @@ def test_pipeline_random_sparse_vs_hper():
         assert r.value == h_per(a)
 
 
+def test_pipeline_fullerenes_config4():
+    """configs[3]: seeded spiral fullerenes n in {70,76,80,84}, 4 isomers each, exact per(A)
+    against the oracle's frontier-DP values (tests/golden/oracle_values.txt)."""
+    from workloads import random_fullerene
+    checked = 0
+    for n in (70, 76, 80, 84):
+        for iso in range(4):
+            try:
+                want = golden(f"fullerene_n{n}_seed2024_iso{iso}")
+            except KeyError:
+                continue
+            a, _ = random_fullerene(n, 2024, iso)
+            r = pipeline.permanent(a, jobs_at_least=256, leaf_order=22)
+            assert r.value == want, (n, iso)
+            checked += 1
+    assert checked >= 12
+
+
 def test_pipeline_c60_leaf16():
     a = truncated_icosahedron()
     r = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
