@@ -33,6 +33,8 @@
 //    row-sum update (a high Gray bit flip) touches all rows.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
 #include <mutex>
 #include <vector>
@@ -457,7 +459,7 @@ __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
 }
 
 template <int NFIX, int PLAN>
-__global__ void __launch_bounds__(kRnwThreads) rnw_tree_kernel(
+__global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
     uint64_t total_items, unsigned long long* __restrict__ leaf_acc) {
@@ -997,6 +999,14 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   if (hsmall[2] & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
   if (hsmall[2] & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
   const int* h_hist = hsmall + 4;
+  if (getenv("SPERM_DEBUG")) {  // plan histogram of this call (diagnostics)
+    fprintf(stderr, "[sperm] permanent n=%d count=%lld:", n, (long long)count);
+    for (int key = 0; key < kNumKeys; ++key)
+      if (h_hist[key])
+        fprintf(stderr, " key%d(plan%d,nfix%d)=%d sum_k=%d", key, key / 8, key ? nfix_of(key % 8) : 0, h_hist[key],
+                hsmall[4 + kNumKeys + key]);
+    fprintf(stderr, "\n");
+  }
   if (n > 0) {
     for (int key = 0; key < kNumKeys; ++key)
       if (h_hist[key]) record_stats(key, NPg, n, h_hist[key], hsmall[4 + kNumKeys + key]);
