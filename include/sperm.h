@@ -102,6 +102,10 @@ int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
  *             PAPER.md:179), so sums over many calls, GPUs (an NCCL sum) and
  *             leaves stay exact below 2^64; reduce mod p_q before sperm_crt.
  *             With d_job NULL only row 0 is used (it is the total).
+ *  d_leaf_cycles [count] uint64 in/out (device) or NULL: SM clock cycles the
+ *             R-NW kernel spent on each leaf's work items are ADDED here (the
+ *             measured job cost T_i of the paper's load-balance study,
+ *             PAPER.md:420-423).
  *  stream     cudaStream_t.
  * Errors: SPERM_ERR_ARG (n > SPERM_NMAX, count < 0), SPERM_ERR_RANGE (some
  * row or column abs sum >= 2^30), SPERM_ERR_PRIMES.  RANGE/PRIMES are
@@ -110,7 +114,7 @@ int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
 int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* d_coef,
                     const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
                     int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
-                    uint64_t* d_job_acc, void* stream);
+                    uint64_t* d_job_acc, uint64_t* d_leaf_cycles, void* stream);
 
 /* Number of Gray-code terms sperm_permanent evaluates for `count` leaves of
  * order n: count * 2^(n-1) (as double; exact for n <= 53). */

@@ -350,19 +350,27 @@ template <int NP>
 __global__ void __launch_bounds__(kRnwThreads) rnw_generic_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, unsigned long long* __restrict__ queue, uint64_t total_items,
-    unsigned long long* __restrict__ leaf_acc) {
+    unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
   using L = GLayout<NP>;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   int32_t* sm = reinterpret_cast<int32_t*>(smem4) + (threadIdx.x >> 5) * L::kWords;
   const uint64_t T = 1ull << (n - 1);
   int64_t cur_leaf = -1;
+  int64_t prev_leaf = -1;
+  long long t_item = 0;
   while (true) {
     unsigned long long item = 0;
     if (lane == 0) item = atomicAdd(queue, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
+    if (leaf_cycles && lane == 0) {  // SM cycles of the previous work item, charged to its leaf
+      const long long now = clock64();
+      if (prev_leaf >= 0) atomicAdd(leaf_cycles + prev_leaf, (unsigned long long)(now - t_item));
+      t_item = now;
+    }
     if (item >= total_items) break;
     const int64_t leaf = leaves[(int64_t)(item >> cbits)];
+    prev_leaf = leaf;
     const uint64_t chunk = item & ((1ull << cbits) - 1);
     const int2 mt = meta[leaf];
     const int k = meta_k(mt), G = meta_G(mt);
@@ -462,7 +470,7 @@ template <int NFIX, int PLAN>
 __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
-    uint64_t total_items, unsigned long long* __restrict__ leaf_acc) {
+    uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
   constexpr int B1 = plan_b1(PLAN), B2 = plan_b2(PLAN), B = B1 + B2, GF = plan_gf(PLAN);
   constexpr int NS = B * KS;       // slot rows
   constexpr int NRT = NS + NFIX;   // row sums held in registers
@@ -475,12 +483,20 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
   int32_t* sm = reinterpret_cast<int32_t*>(smem4) + (threadIdx.x >> 5) * L.words;
   long long* sacc = reinterpret_cast<long long*>(sm + L.sacc);
   int64_t cur_leaf = -1;
+  int64_t prev_leaf = -1;
+  long long t_item = 0;
   while (true) {
     unsigned long long item = 0;
     if (lane == 0) item = atomicAdd(queue, 1ull);
     item = __shfl_sync(0xffffffffu, item, 0);
+    if (leaf_cycles && lane == 0) {  // SM cycles of the previous work item, charged to its leaf
+      const long long now = clock64();
+      if (prev_leaf >= 0) atomicAdd(leaf_cycles + prev_leaf, (unsigned long long)(now - t_item));
+      t_item = now;
+    }
     if (item >= total_items) break;
     const int64_t leaf = leaves[(int64_t)(item >> cbits)];
+    prev_leaf = leaf;
     const uint64_t chunk = item & ((1ull << cbits) - 1);
     const int k = meta_k(meta[leaf]);
     if (leaf != cur_leaf) {
@@ -707,6 +723,7 @@ struct Launch {
   unsigned long long* queue;
   unsigned long long* leaf_acc;
   cudaStream_t st;
+  unsigned long long* leaf_cycles;  // optional per-leaf SM-cycle counters
 };
 
 // A per-process pool of non-blocking streams and reusable events for the plan groups.
@@ -765,7 +782,7 @@ int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bo
   (void)tree;
   count_launch();
   kernel<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, L.m, L.cbits, L.leaves, L.meta, L.perm,
-                                                        L.queue, total, L.leaf_acc);
+                                                        L.queue, total, L.leaf_acc, L.leaf_cycles);
   SPERM_LAUNCH_CHECK("rnw kernel");
   return SPERM_OK;
 }
@@ -786,7 +803,7 @@ int launch_generic(const Launch& L) {
   grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
   count_launch();
   kern<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, m, cbits, L.leaves, L.meta, L.queue, total,
-                                                    L.leaf_acc);
+                                                    L.leaf_acc, L.leaf_cycles);
   SPERM_LAUNCH_CHECK("rnw_generic_kernel");
   return SPERM_OK;
 }
@@ -935,7 +952,7 @@ extern "C" int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d
 extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* d_coef,
                                const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
                                int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
-                               uint64_t* d_job_acc, void* stream) {
+                               uint64_t* d_job_acc, uint64_t* d_leaf_cycles, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0 || n > SPERM_NMAX) return set_error(SPERM_ERR_ARG, "sperm_permanent: n out of range [0, 48]");
   if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_permanent: count < 0");
@@ -1038,7 +1055,8 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       if (!h_hist[key]) continue;
       cudaStream_t gs = nonzero_keys > 1 ? pool.stream(g) : st;
       if (gs != st) SPERM_TRY(cudaStreamWaitEvent(gs, fork, 0));
-      Launch L{d_mats, n, 0, 0, sorted + off, h_hist[key], meta, perm, queue + key, leaf_acc, gs};
+      Launch L{d_mats, n, 0, 0, sorted + off, h_hist[key], meta, perm, queue + key, leaf_acc, gs,
+               (unsigned long long*)d_leaf_cycles};
       rc = launch_key(key, NPg, L);
       if (gs != st) {
         cudaEvent_t join = pool.event();

@@ -45,7 +45,17 @@ class PHResult:
     terms: float
     estimates: Optional[np.ndarray] = None
     machine: Optional[np.ndarray] = None
+    job_cycles: Optional[np.ndarray] = None  # measured SM cycles per job (measure_jobs=True)
+    job_sizes: Optional[np.ndarray] = None   # nonzeros per job (the "size" ordering key)
     stats: Dict[str, float] = field(default_factory=dict)
+
+
+def job_sizes(jobsets: List["NodeSet"], num_jobs: int) -> np.ndarray:
+    """Number of nonzero entries of every job (a size key for the scheduling study)."""
+    out = np.zeros(num_jobs, dtype=np.int64)
+    for s in jobsets:
+        out[s.job.cpu().numpy()] = (s.mats != 0).sum(dim=(1, 2)).cpu().numpy()
+    return out
 
 
 def root_nodeset(a, device="cuda") -> NodeSet:
@@ -118,6 +128,32 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
     return _cat([level] + early)
 
 
+def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 2 << 30):
+    """The same H_per recursion as expand_to_leaves, streamed: a level whose children could
+    exceed `budget_bytes` of HBM is split into chunks that are expanded to their leaves one
+    after another (depth first over chunks), so the live node sets stay bounded however many
+    leaves a job has.  Yields NodeSets of leaves (order <= L) and of s >= 5 nodes."""
+    stack = [jobs]
+    while stack:
+        level = stack.pop()
+        if level.count == 0:
+            continue
+        if level.n <= L or level.n < 2:
+            yield level
+            continue
+        per_node = 2 * 4 * (level.n - 1) ** 2 + 4 * level.n ** 2
+        cap = max(1, budget_bytes // per_node)
+        if level.count > cap:
+            for c0 in reversed(range(0, level.count, cap)):
+                sl = slice(c0, min(level.count, c0 + cap))
+                stack.append(NodeSet(level.n, level.mats[sl], level.coef[sl], level.job[sl]))
+            continue
+        (km, kc, kj), (em, ec, ej) = S.sperm_expand(level.mats, level.coef, level.job)
+        if em.shape[0]:
+            yield NodeSet(level.n, em, ec, ej)
+        stack.append(NodeSet(level.n - 1, km, kc, kj))
+
+
 def bound_primes(a) -> int:
     """Primes needed to reconstruct per(A): host C (sperm_bound_primes) — the row/column
     abs-sum bound, and Bregman-Minc for 0/1 matrices."""
@@ -152,7 +188,7 @@ def reconstruct(res, k: int):
 
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
-              device="cuda") -> PHResult:
+              device="cuda", measure_jobs: bool = False) -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
 
     With a torch.distributed `group` of world size G, every rank replicates the
@@ -178,6 +214,7 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
         est[s.job.cpu().numpy()] = e
     machine, order, _ = S.sperm_schedule(est, world, policy, seed=seed)
     acc = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
+    job_cycles = torch.zeros(num_jobs, dtype=torch.int64, device=device) if measure_jobs else None
     pos = rank_positions(machine, order, rank)
     leaves = 0
     terms = 0.0
@@ -189,11 +226,14 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             idx = torch.tensor(sel[b0:b0 + batch_jobs], dtype=torch.int64, device=device)
             batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
                             s.job.index_select(0, idx))
-            for lv in expand_to_leaves(batch, leaf_order):
+            for lv in iter_leaves(batch, leaf_order):
                 if lv.n > S.NMAX:
                     raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
+                cyc = torch.zeros(lv.count, dtype=torch.int64, device=device) if measure_jobs else None
                 S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
-                                  max_primes=k_total if nonneg else 0, job_acc=acc)
+                                  max_primes=k_total if nonneg else 0, job_acc=acc, leaf_cycles=cyc)
+                if measure_jobs:  # measured job cost T_i = SM cycles of its leaves
+                    job_cycles.index_add_(0, lv.job.long(), cyc)
                 leaves += lv.count
                 terms += S.sperm_rnw_terms(lv.n, lv.count)
     allreduce_accumulators(acc, group)
@@ -201,4 +241,6 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     job_values, value = reconstruct(res, k_total)
     return PHResult(value=value, job_values=job_values, num_jobs=num_jobs,
                     job_order_n={s.n: s.count for s in jobsets}, leaves=leaves, terms=terms,
-                    estimates=est, machine=machine)
+                    estimates=est, machine=machine,
+                    job_cycles=job_cycles.cpu().numpy() if measure_jobs else None,
+                    job_sizes=job_sizes(jobsets, num_jobs))

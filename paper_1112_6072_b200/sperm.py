@@ -41,7 +41,7 @@ _SIGS = {
     "sperm_prime": (ctypes.c_uint32, [_I]),
     "sperm_crt": (_I, [_P, _I, _P, _I, _P]),
     "sperm_bound_primes": (_I, [_P, _I, _P]),
-    "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P]),
+    "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P]),
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
     "sperm_rnw_stats": (_I, [_P, _P, _P, _I]),
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
@@ -139,7 +139,8 @@ def sperm_bound_primes(a) -> int:
 
 # --------------------------------------------------------------------- R-NW
 def sperm_permanent(mats, coef=None, order=None, job=None, num_jobs: int = 0, min_primes: int = 1,
-                    max_primes: int = 0, leaf_res=None, leaf_k=None, job_acc=None, stream=None):
+                    max_primes: int = 0, leaf_res=None, leaf_k=None, job_acc=None, leaf_cycles=None,
+                    stream=None):
     """Batched R-NW leaf permanents mod the CRT primes (see include/sperm.h).
 
     mats: int32 CUDA tensor [count, n, n].  Outputs are allocated if not given:
@@ -157,7 +158,7 @@ def sperm_permanent(mats, coef=None, order=None, job=None, num_jobs: int = 0, mi
     job = _dev(job, torch.int32)
     _check(lib().sperm_permanent(_ptr(mats), n, count, _ptr(coef), _ptr(order), _ptr(job), int(num_jobs),
                                  int(min_primes), int(max_primes), _ptr(leaf_res), _ptr(leaf_k), _ptr(job_acc),
-                                 _stream(stream)))
+                                 _ptr(leaf_cycles), _stream(stream)))
     return leaf_res, leaf_k
 
 
