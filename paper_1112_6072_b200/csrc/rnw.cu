@@ -50,17 +50,30 @@ constexpr int KS = 3;             // slot rows per low column (tree plans)
 constexpr int kNumNFix = 7;
 constexpr int kPermRows = 64;     // per-leaf permutation record: 64 row bytes + 64 column bytes
 constexpr int kPermW = 128;
-constexpr int kNumKeys = 48;      // plan * 8 + nfix index
+constexpr int kNumKeys = 80;      // plan * 8 + nfix index
 
 __host__ __device__ constexpr int nfix_of(int i) {
   return i == 0 ? 4 : i == 1 ? 8 : i == 2 ? 12 : i == 3 ? 16 : i == 4 ? 24 : i == 5 ? 32 : 40;
 }
 // tree plans: (B1, B2, GF) — B1 low bits in the exact X tree, B2 in the modular Y tree,
 // GF fixed rows per exact group.  Plan 0 = generic kernel.
-__host__ __device__ constexpr int plan_b1(int p) { return p == 1 ? 4 : p == 2 ? 3 : p == 3 ? 2 : p == 4 ? 2 : p == 5 ? 1 : 0; }
-__host__ __device__ constexpr int plan_b2(int p) { return p == 1 ? 2 : p == 2 ? 2 : p == 3 ? 2 : p == 4 ? 1 : p == 5 ? 1 : 0; }
-__host__ __device__ constexpr int plan_gf(int p) { return (p >= 1 && p <= 3) ? 4 : 2; }
-constexpr int kNumPlans = 6;
+// Plans in order of preference (larger blocks first); the first whose bounds hold is used.
+//   plan:  1  2  3  4  5  6  7  8  9
+//   B1:    4  4  4  3  2  3  2  2  1
+//   B2:    4  3  2  4  4  2  2  1  1
+//   RU:    0  0  0  0  1  0  0  0  0   (1 = one REDC per X_u accumulator instead of per block)
+// B2 > 2 splits the Y tree: Z_lo (2 columns, exact) and Z_hi (B2-2 columns, exact), joined by
+// Montgomery products W_h = P_F Z_hi,h, y = W_h Z_lo,v.
+__host__ __device__ constexpr int plan_b1(int p) {
+  return p == 1 || p == 2 || p == 3 ? 4 : p == 4 || p == 6 ? 3 : p == 5 || p == 7 || p == 8 ? 2 : p == 9 ? 1 : 0;
+}
+__host__ __device__ constexpr int plan_b2(int p) {
+  return p == 1 || p == 4 || p == 5 ? 4 : p == 2 ? 3 : p == 3 || p == 6 || p == 7 ? 2 : p == 8 || p == 9 ? 1 : 0;
+}
+__host__ __device__ constexpr int plan_gf(int p) { return p >= 1 && p <= 7 ? 4 : 2; }
+__host__ __device__ constexpr int plan_ru(int p) { return p == 5 ? 1 : 0; }
+constexpr int kNumPlans = 10;
+constexpr int kMaxLow = 8;  // low columns picked per leaf
 
 // the CRT primes (kPrimes, common.cuh) and p^-1 mod 2^32
 __constant__ int32_t c_p[SPERM_KMAX] = {2147483647, 2147483629, 2147483587, 2147483579,
@@ -149,14 +162,14 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   __syncwarp();
 
   // ---- tree plan: greedy pick of up to 6 low columns with disjoint supports of <= 3 rows
-  int picks[6] = {-1, -1, -1, -1, -1, -1};
+  int picks[kMaxLow] = {-1, -1, -1, -1, -1, -1, -1, -1};
   int np = 0;
   if (allow_tree && n >= 8 && !range_bad) {
     unsigned long long used = 0;
     for (int lvl = 1; lvl <= KS; ++lvl)
       for (int t = 0; t < n; ++t) {
         const int j = (t + lane) % n;
-        if (cnt[j] == lvl && !(supp[j] & used) && np < 6 && np < n - 2) {
+        if (cnt[j] == lvl && !(supp[j] & used) && np < kMaxLow && np < n - 2) {
           picks[np++] = j;
           used |= supp[j];
         }
@@ -167,7 +180,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   for (int o = 16; o; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
   const int best = 31 - (key & 0xff);
   np = key >> 8;
-  for (int c = 0; c < 6; ++c) picks[c] = __shfl_sync(0xffffffffu, c < np ? picks[min(c, 5)] : -1, best);
+  for (int c = 0; c < kMaxLow; ++c) picks[c] = __shfl_sync(0xffffffffu, c < np ? picks[c] : -1, best);
 
   if (lane == 0) {
     if (range_bad) atomicOr(err, 1);
@@ -210,7 +223,8 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
         if (x > ((int64_t)1 << 40) / y) return (int64_t)1 << 40;
         return x * y;
       };
-      int64_t X = 1, Z = 1;
+      const int ZL = B2 < 2 ? B2 : 2;  // exact Z_lo columns; the rest (<= 2) form Z_hi
+      int64_t X = 1, Zlo = 1, Zhi = 1;
       unsigned long long slot_rows = 0;
       for (int c = 0; c < B; ++c) {
         int64_t q = 1;
@@ -218,10 +232,13 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
           if ((supp[picks[c]] >> i) & 1ull) q = sat_mul(q, R[i]);
         slot_rows |= supp[picks[c]];
         if (c < B1) X = sat_mul(X, q);
-        else Z = sat_mul(Z, q);
+        else if (c < B1 + ZL) Zlo = sat_mul(Zlo, q);
+        else Zhi = sat_mul(Zhi, q);
       }
-      // |X| * 2^B < p_min keeps the block's sum of 2^B products X_u*Y_v below p*2^31 (one REDC)
-      if (X >= ((int64_t)1 << (31 - B)) || Z >= ((int64_t)1 << 30)) continue;
+      // |X| * 2^B < p_min keeps a block's sum of 2^B products X_u*Y_v below p*2^31 (one REDC);
+      // with one REDC per X_u (plan_ru) only the 2^B2 products of one accumulator count
+      const int xbits = 31 - (plan_ru(pl) ? B2 : B);
+      if (X >= ((int64_t)1 << xbits) || Zlo >= ((int64_t)1 << 30) || Zhi >= ((int64_t)1 << 30)) continue;
       const int nf = n - __popcll(slot_rows);
       int fi = 0;
       while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
@@ -242,7 +259,8 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (!ok) continue;
       plan = pl;
       nfi = fi;
-      mexp = NF / GF + 1;
+      // Montgomery factors: NGF-1 (P_F chain) + [B2 > 2] (W_h) + 1 (y) + 1 (REDC)
+      mexp = NF / GF + 1 + (B2 > 2 ? 1 : 0);
       // permutation record: rows [slot rows of low column c (ascending, -1 padded to KS)...,
       // fixed rows ascending, -1 to NS + NF]; columns [low columns, high columns ascending, nw]
       int8_t* pr = perm + leaf * kPermW;
@@ -477,6 +495,9 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
   constexpr int S4 = (NRT + 3) / 4 * 4;
   constexpr int NGF = NFIX / GF;   // exact fixed-row groups
   constexpr int NX = 1 << B1, NZ = 1 << B2;
+  constexpr int ZL = B2 < 2 ? B2 : 2, ZH = B2 - ZL;  // split Y tree (see the plan table)
+  constexpr int NZL = 1 << ZL, NZH = 1 << ZH;
+  constexpr bool RU = plan_ru(PLAN) != 0;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   const TreeSmem L = tree_smem(NRT, NS, n, B);
@@ -572,7 +593,8 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
         Q0[c] = x0;
         Q1[c] = -x1;
       }
-      int32_t X[NX], Z[NZ];
+      // exact product trees: X over low columns [0, B1), Z_lo over [B1, B1+ZL), Z_hi over the rest
+      int32_t X[NX], Z[NZL], ZH_[NZH];
       X[0] = Q0[0];
       X[1] = Q1[0];
 #pragma unroll
@@ -585,12 +607,23 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
       Z[0] = Q0[B1];
       Z[1] = Q1[B1];
 #pragma unroll
-      for (int c = 1; c < B2; ++c)
+      for (int c = 1; c < ZL; ++c)
 #pragma unroll
         for (int s = 0; s < (1 << c); ++s) {
           Z[s + (1 << c)] = Z[s] * Q1[B1 + c];
           Z[s] = Z[s] * Q0[B1 + c];
         }
+      if (ZH > 0) {
+        ZH_[0] = Q0[B1 + ZL];
+        ZH_[1] = Q1[B1 + ZL];
+#pragma unroll
+        for (int c = 1; c < ZH; ++c)
+#pragma unroll
+          for (int s = 0; s < (1 << c); ++s) {
+            ZH_[s + (1 << c)] = ZH_[s] * Q1[B1 + ZL + c];
+            ZH_[s] = ZH_[s] * Q0[B1 + ZL + c];
+          }
+      }
       int32_t FG[NGF];
 #pragma unroll
       for (int g = 0; g < NGF; ++g) {
@@ -605,23 +638,35 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
         int32_t pf = FG[0];
 #pragma unroll
         for (int g = 1; g < NGF; ++g) pf = smont(pf, FG[g], p, pinv);
-        int32_t y[NZ];
+        int32_t wh[NZH];
+        if (ZH > 0) {
 #pragma unroll
-        for (int v = 0; v < NZ; ++v) y[v] = smont(pf, Z[v], p, pinv);
-        // one 32x32->64 multiply-add per term (X_u * Y_v); NX independent accumulator chains.
-        // |X| < 2^(31-B) (prep bound) keeps |sum of all 2^B terms| < p * 2^31 for one REDC.
+          for (int h = 0; h < NZH; ++h) wh[h] = smont(pf, ZH_[h], p, pinv);
+        }
+        // one 32x32->64 multiply-add per term (X_u * Y_v, v = h 2^ZL + l); NX independent
+        // accumulator chains.  The prep bound on |X| keeps every REDC input below p * 2^31.
         int64_t acc[NX];
 #pragma unroll
-        for (int u = 0; u < NX; ++u) {
-          acc[u] = (int64_t)X[u] * y[0];
+        for (int v = 0; v < NZ; ++v) {
+          const int32_t y = smont(ZH > 0 ? wh[v >> ZL] : pf, Z[v & (NZL - 1)], p, pinv);
 #pragma unroll
-          for (int v = 1; v < NZ; ++v) acc[u] += (int64_t)X[u] * y[v];
+          for (int u = 0; u < NX; ++u) {
+            if (v == 0) acc[u] = (int64_t)X[u] * y;
+            else acc[u] += (int64_t)X[u] * y;
+          }
         }
+        int64_t blk;
+        if (RU) {  // one REDC per accumulator
+          blk = 0;
 #pragma unroll
-        for (int s = NX / 2; s >= 1; s >>= 1)
+          for (int u = 0; u < NX; ++u) blk += redc(acc[u], p, pinv);
+        } else {
 #pragma unroll
-          for (int u = 0; u < s; ++u) acc[u] += acc[u + s];
-        const int64_t blk = redc(acc[0], p, pinv);
+          for (int s = NX / 2; s >= 1; s >>= 1)
+#pragma unroll
+            for (int u = 0; u < s; ++u) acc[u] += acc[u + s];
+          blk = redc(acc[0], p, pinv);
+        }
         sacc[q * 32 + lane] += neg ? -blk : blk;
       }
     }
@@ -813,7 +858,7 @@ int launch_tree(const Launch& L) {
   constexpr int B = plan_b1(PLAN) + plan_b2(PLAN);
   constexpr int NS = B * KS, NRT = NS + NFIX;
   const int tb = L.n - 1;
-  const int m = choose_m(L.n, L.nleaves, B);
+  const int m = choose_m(L.n, L.nleaves, std::min(B + 2, L.n - 6));
   if (m > tb - 5) return set_error(SPERM_ERR_ARG, "sperm_permanent: leaf too small for the tree plan");
   const int cbits = tb - 5 - m;
   const uint64_t total = (uint64_t)L.nleaves << cbits;
@@ -857,12 +902,16 @@ int launch_key(int key, int NPg, const Launch& L) {
     case 3: return launch_tree_nfix<3>(fi, L);
     case 4: return launch_tree_nfix<4>(fi, L);
     case 5: return launch_tree_nfix<5>(fi, L);
+    case 6: return launch_tree_nfix<6>(fi, L);
+    case 7: return launch_tree_nfix<7>(fi, L);
+    case 8: return launch_tree_nfix<8>(fi, L);
+    case 9: return launch_tree_nfix<9>(fi, L);
     default: return set_error(SPERM_ERR_ARG, "sperm_permanent: bad plan key");
   }
 }
 
 // First tree plan the prep pass may choose (0 = generic kernel only).  Testing / A-B
-// measurements only: SPERM_RNW_PLAN_MIN=<p> restricts the plans to p..5.
+// measurements only: SPERM_RNW_PLAN_MIN=<p> restricts the plans to p..9.
 int first_plan() {
   const char* e = getenv("SPERM_RNW_PLAN_MIN");
   if (!e || !e[0]) return 1;
@@ -903,11 +952,13 @@ void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k) {
     const double f_sh = B * 2.0 * (KS - 1) + (std::ldexp(1.0, B1 + 1) - 4) + (std::ldexp(1.0, B2 + 1) - 4) +
                         NGF * (GF - 1.0);
     const double a_sh = S4 + B * (double)KS + 8;
-    // per prime per block: (NGF-1+NZ) smont, NZ redc (IMAD + HI 2), 2^B IMAD.WIDE (2 each)
-    // per prime per block: (NGF-1+NZ) smont, 2^B IMAD.WIDE (2 each), one REDC (IMAD + HI 2);
+    // per prime per block: (NGF-1 + NZ + NZH) smont (NZH = 2^(B2-2) W_h products when B2 > 2),
+    // 2^B IMAD.WIDE (2 each), one REDC (or one per X_u, plan_ru) of 3 units;
     // ALU: smont/REDC subtractions, 2^B1 - 1 64-bit adds (2 each), accumulate
-    const double f_pr = (NGF - 1 + NZ) * 5.0 + 3.0 + blk * 2.0;
-    const double a_pr = (NGF - 1 + NZ) * 1.0 + 1.0 + 2.0 * (std::ldexp(1.0, B1) - 1) + 6.0;
+    const double NZH = B2 > 2 ? std::ldexp(1.0, B2 - 2) : 0.0, NX = std::ldexp(1.0, B1);
+    const double nred = plan_ru(plan) ? NX : 1.0;
+    const double f_pr = (NGF - 1 + NZ + NZH) * 5.0 + nred * 3.0 + blk * 2.0;
+    const double a_pr = (NGF - 1 + NZ + NZH) * 1.0 + nred + 2.0 * (NX - 1) + 6.0;
     fma_leaf = f_sh / blk;
     alu_leaf = a_sh / blk;
     fma_prime = f_pr / blk;
@@ -1034,10 +1085,10 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   const int32_t* sorted = ids;
   if (nonzero_keys > 1) {
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 6, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 7, st);
     SPERM_TRY(cudaMallocAsync(&sort_tmp, tmp_bytes, st));
     SPERM_TRY(cub::DeviceRadixSort::SortPairs(sort_tmp, tmp_bytes, keys, keys + count, ids, ids + count,
-                                              (int)count, 0, 6, st));
+                                              (int)count, 0, 7, st));
     sorted = ids + count;
   }
   int rc = SPERM_OK;

@@ -83,10 +83,11 @@ def study(P, pipeline, name, a, J, L, Gs=(1, 2, 4, 8)):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--jobs", type=int, default=2000)
+    ap.add_argument("--jobs", default="48,160,1000", help="comma-separated J values (jobs_at_least)")
     ap.add_argument("--leaf", type=int, default=22)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "scaling.json"))
     args = ap.parse_args()
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
     import paper_1112_6072_b200 as P
     from paper_1112_6072_b200 import pipeline
     from workloads import random_3perm, random_fullerene
@@ -94,13 +95,17 @@ def main():
     mats = [("random 3-regular n=96 (seed [2024,96])", random_3perm(96, rng)),
             ("spiral fullerene n=96 (seed 2024, isomer 0)", random_fullerene(96, 2024, 0)[0])]
     out = {"jobs_at_least": args.jobs, "leaf_order": args.leaf, "studies": []}
-    for name, a in mats:
-        res = study(P, pipeline, name, a, args.jobs, args.leaf)
-        out["studies"].append(res)
-        print(json.dumps({k: v for k, v in res.items() if k != "efficiency"}), flush=True)
-        for G, row in res["efficiency"].items():
-            print(f"  G={G}: " + "  ".join(f"{p}: s{v['static']:.4f}/d{v['dynamic']:.4f}" for p, v in row.items()),
-                  flush=True)
+    for J in [int(x) for x in args.jobs.split(",")]:
+        for name, a in mats:
+            res = study(P, pipeline, name, a, J, args.leaf)
+            res["jobs_at_least"] = J
+            out["studies"].append(res)
+            print(json.dumps({k: v for k, v in res.items() if k != "efficiency"}), flush=True)
+            for G, row in res["efficiency"].items():
+                print(f"  G={G}: " + "  ".join(f"{p}: s{v['static']:.4f}/d{v['dynamic']:.4f}"
+                                               for p, v in row.items()), flush=True)
+            with open(args.out, "w") as f:
+                json.dump(out, f, indent=1)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(out, f, indent=1)
