@@ -51,16 +51,21 @@ def kendall_tau(x, y):
 
 def study(P, pipeline, name, a, J, L, Gs=(1, 2, 4, 8)):
     import torch
+    P.sperm_timing_enable(True)
+    P.sperm_timing_reset()
     t0 = time.perf_counter()
     r = pipeline.permanent(a, jobs_at_least=J, leaf_order=L, measure_jobs=True)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    stage_ms = {s: P.sperm_timing_get(s)[0] for s in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
+    P.sperm_timing_enable(False)
     T = r.job_cycles.astype(np.float64)
     est = r.estimates
     size = r.job_sizes.astype(np.float64)
     rng = np.random.default_rng(11)
     res = {"workload": name, "n": int(a.shape[0]), "per": str(r.value), "jobs": r.num_jobs, "leaves": r.leaves,
-           "terms": r.terms, "wall_s_1gpu": wall, "job_orders": {str(k): v for k, v in r.job_order_n.items()},
+           "terms": r.terms, "wall_s_1gpu": wall, "stage_ms": stage_ms,
+           "job_orders": {str(k): v for k, v in r.job_order_n.items()},
            "tau_T_estimate": kendall_tau(T, est), "tau_T_size": kendall_tau(T, size),
            "cost_cv": float(T.std() / T.mean()), "efficiency": {}}
     total = T.sum()
