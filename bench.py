@@ -235,13 +235,17 @@ def bench_ph(P, torch, leaf_order: int = 32, jobs_at_least: int = 992):
     P.sperm_timing_enable(True)
     P.sperm_timing_reset()
     P.sperm_rnw_stats(reset=True)
+    P.sperm_expand_stats(reset=True)
     t0 = time.perf_counter()
     r = pipeline.permanent(a, jobs_at_least=jobs_at_least, leaf_order=leaf_order)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
     terms, fma, alu = P.sperm_rnw_stats(reset=True)
+    exp_bytes, exp_nodes = P.sperm_expand_stats(reset=True)
     P.sperm_timing_enable(False)
+    pk, pk_kind = peaks()
+    exp_gbs = exp_bytes / (stages["expand"] * 1e-3) / 1e9 if stages["expand"] else None
     gold = None
     try:
         for ln in open(os.path.join(ROOT, "tests", "golden", "oracle_values.txt")):
@@ -253,7 +257,11 @@ def bench_ph(P, torch, leaf_order: int = 32, jobs_at_least: int = 992):
             "per": str(r.value), "matches_oracle_golden": (r.value == gold) if gold is not None else None,
             "wall_s": wall, "jobs": r.num_jobs, "leaves": r.leaves, "terms": terms,
             "terms_per_s_rnw": terms / (stages["rnw"] * 1e-3) if stages["rnw"] else None,
-            "stage_ms": stages}
+            "stage_ms": stages,
+            "expand_roofline": {"bound": "hbm", "achieved": exp_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                                "frac": (exp_gbs / pk["hbm_gbs"]) if exp_gbs and pk.get("hbm_gbs") else None,
+                                "algorithmic_bytes": exp_bytes, "parents": exp_nodes,
+                                "peak_note": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy)"}}
 
 
 def cpu_baseline(mats, seconds: float = 12.0):

@@ -162,6 +162,12 @@ int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32
                  int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
                  int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
 
+/* Cumulative algorithmic traffic of the completed sperm_expand calls since the last reset
+ * (host): bytes = every parent read once + every child / early node written once (matrix,
+ * coefficient, job id); nodes = parents processed.  For the HBM roofline of the expansion.
+ * reset != 0 clears the counters after reading. */
+int sperm_expand_stats(double* h_bytes, double* h_nodes, int reset);
+
 /* ---------------------------------------------------------------- estimator */
 /* sperm_estimate — Algorithm KKLLL on the 0/1 pattern of
  * each matrix: B_ij = 0 where a_ij = 0, else an

@@ -14,6 +14,7 @@
 //   row pivot r, cofactor at p:     delete row r, column p;   coef *= a_rp
 //   column pivot c (= row pivot of A^T, reading R2): the same with rows and columns exchanged.
 #include <algorithm>
+#include <mutex>
 
 #include <cub/device/device_scan.cuh>
 
@@ -273,6 +274,9 @@ __global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
 
 using namespace sperm;
 
+static std::mutex g_exp_mu;
+static double g_exp_bytes = 0.0, g_exp_nodes = 0.0;
+
 extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job, int n,
                             int64_t count, int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job,
                             int64_t cap_out, int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
@@ -348,5 +352,21 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   le = cudaGetLastError();
   cleanup();
   if (le != cudaSuccess) return cuda_check(le, "expand_emit_kernel");
+  {
+    // algorithmic bytes of the level: every parent read once (matrix + coef + job), every
+    // child and early node written once
+    std::lock_guard<std::mutex> lk(g_exp_mu);
+    g_exp_bytes += (double)count * (4.0 * n * n + 12.0) + (double)tot[0] * (4.0 * (n - 1) * (n - 1) + 12.0) +
+                   (double)tot[1] * (4.0 * n * n + 12.0);
+    g_exp_nodes += (double)count;
+  }
   return rc;
+}
+
+extern "C" int sperm_expand_stats(double* h_bytes, double* h_nodes, int reset) {
+  std::lock_guard<std::mutex> lk(g_exp_mu);
+  if (h_bytes) *h_bytes = g_exp_bytes;
+  if (h_nodes) *h_nodes = g_exp_nodes;
+  if (reset) g_exp_bytes = g_exp_nodes = 0.0;
+  return SPERM_OK;
 }

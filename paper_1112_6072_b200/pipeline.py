@@ -128,7 +128,7 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
     return _cat([level] + early)
 
 
-def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 2 << 30):
+def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30):
     """The same H_per recursion as expand_to_leaves, streamed: a level whose children could
     exceed `budget_bytes` of HBM is split into chunks that are expanded to their leaves one
     after another (depth first over chunks), so the live node sets stay bounded however many

@@ -46,6 +46,7 @@ _SIGS = {
     "sperm_rnw_stats": (_I, [_P, _P, _P, _I]),
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
     "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
+    "sperm_expand_stats": (_I, [_P, _P, _I]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_launch_count": (_I64, [_I]),
@@ -206,21 +207,30 @@ def sperm_expand(mats, coef=None, job=None, stream=None):
     job = _dev(job, torch.int32)
     oc, ec = ctypes.c_int64(0), ctypes.c_int64(0)
     L = lib()
-    # first call with zero capacity learns the sizes (count pass only)
-    rc = L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, None, None, None, 0, None, None, None, 0,
-                        ctypes.byref(oc), ctypes.byref(ec), _stream(stream))
+    # children are at most 2 per node: allocate that once; s >= 5 (early) nodes are rare, so
+    # their buffer is sized by a second call only when the first reports them
+    cap = 2 * count
+    out = (torch.empty((cap, n - 1, n - 1), dtype=torch.int32, device=dev),
+           torch.empty((cap,), dtype=torch.int64, device=dev), torch.empty((cap,), dtype=torch.int32, device=dev))
+    rc = L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]),
+                        cap, None, None, None, 0, ctypes.byref(oc), ctypes.byref(ec), _stream(stream))
     if rc not in (OK, ERR_CAPACITY):
         _check(rc)
     no, ne = oc.value, ec.value
-    out = (torch.empty((no, n - 1, n - 1), dtype=torch.int32, device=dev),
-           torch.empty((no,), dtype=torch.int64, device=dev), torch.empty((no,), dtype=torch.int32, device=dev))
     early = (torch.empty((ne, n, n), dtype=torch.int32, device=dev),
              torch.empty((ne,), dtype=torch.int64, device=dev), torch.empty((ne,), dtype=torch.int32, device=dev))
     if rc == ERR_CAPACITY:
         _check(L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]),
-                              _ptr(out[2]), no, _ptr(early[0]), _ptr(early[1]), _ptr(early[2]), ne,
+                              _ptr(out[2]), cap, _ptr(early[0]), _ptr(early[1]), _ptr(early[2]), ne,
                               ctypes.byref(oc), ctypes.byref(ec), _stream(stream)))
-    return out, early
+    return (out[0][:no], out[1][:no], out[2][:no]), early
+
+
+def sperm_expand_stats(reset: bool = False):
+    """(algorithmic bytes, parent nodes) of the sperm_expand calls since the last reset."""
+    b, nn = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().sperm_expand_stats(ctypes.byref(b), ctypes.byref(nn), 1 if reset else 0))
+    return b.value, nn.value
 
 
 # --------------------------------------------------------------------- estimator
