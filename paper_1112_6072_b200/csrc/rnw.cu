@@ -182,6 +182,8 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   np = key >> 8;
   for (int c = 0; c < kMaxLow; ++c) picks[c] = __shfl_sync(0xffffffffu, c < np ? picks[c] : -1, best);
 
+  // ---- number of primes (lane 0) and the generic group size G (lane 31)
+  int k = min_primes, G = 1;
   if (lane == 0) {
     if (range_bad) atomicOr(err, 1);
     double lb = zero ? -1.0 : fmin(lr, lc);
@@ -190,15 +192,15 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     else if (lb >= 0.0) lb += log2(fabs((double)cf));
     // need prod p_q > 2 * bound; each p_q > 2^30.99999; margin for log2 rounding
     const double need = lb + 1.0 + 1e-6 * fabs(lb) + 1e-6;
-    int k = min_primes;
     const int kcap = max_primes > 0 ? max_primes : SPERM_KMAX;
     while (k <= SPERM_KMAX && 30.99999 * k <= need) ++k;
     if (k > kcap) {
       if (max_primes <= 0) atomicOr(err, 2);
       k = kcap;
     }
+  }
+  if (lane == 31) {
     // generic: largest group size G in {8,4,2,1} with every group product of row bounds < 2^30
-    int G = 1;
     for (int g = 8; g >= 2; g >>= 1) {
       bool ok = true;
       for (int s = 0; s < NPg && ok; s += g) {
@@ -213,11 +215,17 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       }
       if (ok) { G = g; break; }
     }
-    int plan = 0, nfi = 0, mexp = NPg / G - 1;
-    for (int pl = allow_tree; pl >= 1 && pl < kNumPlans && np > 0; ++pl) {
-      const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
-      if (np < B || n - 6 < B) continue;
-      // exact bounds: |X| < 2^(31-B), |Z| < 2^30, fixed groups < 2^30
+  }
+  k = __shfl_sync(0xffffffffu, k, 0);
+  G = __shfl_sync(0xffffffffu, G, 31);
+  // ---- tree plans: lane l tests plan l+1 (exact-arithmetic bounds); the first feasible wins
+  const int pl = lane + 1;
+  bool feasible = false;
+  int fi = 0, pmexp = 0;
+  unsigned long long slot_rows = 0;
+  if (pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0) {
+    const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
+    if (np >= B && n - 6 >= B) {
       auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
         if (x == 0 || y == 0) return 0;
         if (x > ((int64_t)1 << 40) / y) return (int64_t)1 << 40;
@@ -225,7 +233,6 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       };
       const int ZL = B2 < 2 ? B2 : 2;  // exact Z_lo columns; the rest (<= 2) form Z_hi
       int64_t X = 1, Zlo = 1, Zhi = 1;
-      unsigned long long slot_rows = 0;
       for (int c = 0; c < B; ++c) {
         int64_t q = 1;
         for (int i = 0; i < n; ++i)
@@ -238,13 +245,10 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       // |X| * 2^B < p_min keeps a block's sum of 2^B products X_u*Y_v below p*2^31 (one REDC);
       // with one REDC per X_u (plan_ru) only the 2^B2 products of one accumulator count
       const int xbits = 31 - (plan_ru(pl) ? B2 : B);
-      if (X >= ((int64_t)1 << xbits) || Zlo >= ((int64_t)1 << 30) || Zhi >= ((int64_t)1 << 30)) continue;
+      bool ok = X < ((int64_t)1 << xbits) && Zlo < ((int64_t)1 << 30) && Zhi < ((int64_t)1 << 30);
       const int nf = n - __popcll(slot_rows);
-      int fi = 0;
       while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
-      if (fi == kNumNFix) continue;
-      const int NF = nfix_of(fi);
-      bool ok = true;
+      if (fi == kNumNFix) ok = false;
       int pos = 0;
       int64_t g = 1;
       for (int i = 0; i < n && ok; ++i) {
@@ -256,41 +260,44 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
         }
       }
       if (g >= ((int64_t)1 << 30)) ok = false;
-      if (!ok) continue;
-      plan = pl;
-      nfi = fi;
+      feasible = ok;
       // Montgomery factors: NGF-1 (P_F chain) + [B2 > 2] (W_h) + 1 (y) + 1 (REDC)
-      mexp = NF / GF + 1 + (B2 > 2 ? 1 : 0);
-      // permutation record: rows [slot rows of low column c (ascending, -1 padded to KS)...,
-      // fixed rows ascending, -1 to NS + NF]; columns [low columns, high columns ascending, nw]
-      int8_t* pr = perm + leaf * kPermW;
-      int r = 0;
-      for (int c = 0; c < B; ++c) {
-        int s = 0;
-        for (int i = 0; i < n; ++i)
-          if ((supp[picks[c]] >> i) & 1ull) { pr[r++] = (int8_t)i; ++s; }
-        for (; s < KS; ++s) pr[r++] = -1;
-      }
-      int f = 0;
-      for (int i = 0; i < n; ++i)
-        if (!((slot_rows >> i) & 1ull)) { pr[r++] = (int8_t)i; ++f; }
-      for (; f < NF; ++f) pr[r++] = -1;
-      // nw column: the non-low column with most nonzeros (highest index on ties)
-      unsigned long long low = 0;
-      for (int c = 0; c < B; ++c) low |= 1ull << picks[c];
-      int nw = -1;
-      for (int j = 0; j < n; ++j)
-        if (!((low >> j) & 1ull) && (nw < 0 || cnt[j] >= cnt[nw])) nw = j;
-      int8_t* pc = pr + kPermRows;
-      int cc = 0;
-      for (int c = 0; c < B; ++c) pc[cc++] = (int8_t)picks[c];
-      for (int j = 0; j < n; ++j)
-        if (!((low >> j) & 1ull) && j != nw) pc[cc++] = (int8_t)j;
-      pc[cc++] = (int8_t)nw;
-      break;
+      if (ok) pmexp = nfix_of(fi) / GF + 1 + (B2 > 2 ? 1 : 0);
     }
-    meta[leaf] = make_int2(k | (plan << 8) | (nfi << 16) | (G << 24), mexp);
   }
+  const unsigned fmask = __ballot_sync(0xffffffffu, feasible);
+  const int win = fmask ? __ffs(fmask) - 1 : -1;  // lowest plan index = preferred
+  if (win >= 0 && lane == win) {
+    const int B = plan_b1(pl) + plan_b2(pl), NF = nfix_of(fi);
+    // permutation record: rows [slot rows of low column c (ascending, -1 padded to KS)...,
+    // fixed rows ascending, -1 to NS + NF]; columns [low columns, high columns ascending, nw]
+    int8_t* pr = perm + leaf * kPermW;
+    int r = 0;
+    for (int c = 0; c < B; ++c) {
+      int s = 0;
+      for (int i = 0; i < n; ++i)
+        if ((supp[picks[c]] >> i) & 1ull) { pr[r++] = (int8_t)i; ++s; }
+      for (; s < KS; ++s) pr[r++] = -1;
+    }
+    int f = 0;
+    for (int i = 0; i < n; ++i)
+      if (!((slot_rows >> i) & 1ull)) { pr[r++] = (int8_t)i; ++f; }
+    for (; f < NF; ++f) pr[r++] = -1;
+    // nw column: the non-low column with most nonzeros (highest index on ties)
+    unsigned long long low = 0;
+    for (int c = 0; c < B; ++c) low |= 1ull << picks[c];
+    int nw = -1;
+    for (int j = 0; j < n; ++j)
+      if (!((low >> j) & 1ull) && (nw < 0 || cnt[j] >= cnt[nw])) nw = j;
+    int8_t* pc = pr + kPermRows;
+    int cc = 0;
+    for (int c = 0; c < B; ++c) pc[cc++] = (int8_t)picks[c];
+    for (int j = 0; j < n; ++j)
+      if (!((low >> j) & 1ull) && j != nw) pc[cc++] = (int8_t)j;
+    pc[cc++] = (int8_t)nw;
+    meta[leaf] = make_int2(k | (pl << 8) | (fi << 16) | (G << 24), pmexp);
+  }
+  if (win < 0 && lane == 0) meta[leaf] = make_int2(k | (G << 24), NPg / G - 1);  // generic plan
 }
 
 // ============================================================================ generic kernel
@@ -1100,13 +1107,27 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     StreamPool& pool = stream_pool();
     cudaEvent_t fork = pool.event();
     SPERM_TRY(cudaEventRecord(fork, st));
-    int64_t off = 0;
+    // group offsets in the sorted list (key order); launch the groups largest work first so the
+    // small groups fill the SMs the large ones release in their tails
+    int64_t offs[kNumKeys];
+    std::vector<int> order_keys;
+    {
+      int64_t off = 0;
+      for (int key = 0; key < kNumKeys; ++key) {
+        offs[key] = off;
+        off += h_hist[key];
+        if (h_hist[key]) order_keys.push_back(key);
+      }
+      const int* h_sumk = hsmall + 4 + kNumKeys;
+      std::stable_sort(order_keys.begin(), order_keys.end(),
+                       [&](int a, int b) { return h_sumk[a] > h_sumk[b]; });
+    }
     int g = 0;
-    for (int key = 0; key < kNumKeys && rc == SPERM_OK; ++key) {
-      if (!h_hist[key]) continue;
+    for (int key : order_keys) {
+      if (rc != SPERM_OK) break;
       cudaStream_t gs = nonzero_keys > 1 ? pool.stream(g) : st;
       if (gs != st) SPERM_TRY(cudaStreamWaitEvent(gs, fork, 0));
-      Launch L{d_mats, n, 0, 0, sorted + off, h_hist[key], meta, perm, queue + key, leaf_acc, gs,
+      Launch L{d_mats, n, 0, 0, sorted + offs[key], h_hist[key], meta, perm, queue + key, leaf_acc, gs,
                (unsigned long long*)d_leaf_cycles};
       rc = launch_key(key, NPg, L);
       if (gs != st) {
@@ -1114,7 +1135,6 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
         SPERM_TRY(cudaEventRecord(join, gs));
         SPERM_TRY(cudaStreamWaitEvent(st, join, 0));
       }
-      off += h_hist[key];
       ++g;
     }
   }
