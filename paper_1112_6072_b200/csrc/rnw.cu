@@ -941,10 +941,8 @@ void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k) {
   const double T = std::ldexp(1.0, n - 1);
   double fma_leaf = 0, alu_leaf = 0, fma_prime = 0, alu_prime = 0;  // per term
   if (key == 0) {
-    int G = 1;  // group size is per leaf; model with the config-typical G of the bound (8 if NPg<=8)
-    (void)G;
-    // generic: NP adds, NP-NP/G products, (NP/G-1) smont per prime (6 units: WIDE 2, IMAD, HI 2,
-    // + IADD on alu), accumulate 2 alu per prime; G taken as 4 (weighted) - conservative
+    // generic: NP adds, NP-NP/G products, (NP/G-1) smont per prime (5 units: WIDE 2, IMAD, HI 2;
+    // + IADD on alu), accumulate 2 alu per prime; the group size is per leaf, modelled as G = 4
     const int NG = NPg / 4;
     alu_leaf = NPg;
     fma_leaf = NPg - NG;
@@ -964,10 +962,16 @@ void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k) {
     // ALU: smont/REDC subtractions, 2^B1 - 1 64-bit adds (2 each), accumulate
     const double NZH = B2 > 2 ? std::ldexp(1.0, B2 - 2) : 0.0, NX = std::ldexp(1.0, B1);
     const double nred = plan_ru(plan) ? NX : 1.0;
-    const double f_pr = (NGF - 1 + NZ + NZH) * 5.0 + nred * 3.0 + blk * 2.0;
-    const double a_pr = (NGF - 1 + NZ + NZH) * 1.0 + nred + 2.0 * (NX - 1) + 6.0;
-    fma_leaf = f_sh / blk;
-    alu_leaf = a_sh / blk;
+    double f_pr = (NGF - 1 + NZ + NZH) * 5.0 + nred * 3.0 + blk * 2.0;
+    const double add_pr = (NGF - 1 + NZ + NZH) * 1.0 + nred;  // 32-bit subtracts of smont / REDC
+    double a_pr = 2.0 * (NX - 1) + 6.0;                       // 64-bit adds, accumulate
+    // ptxas issues about half of the 32-bit adds as IMAD.IADD on the multiply pipe (SASS mix of
+    // the tree kernels, profiles/r01_v5_rnw_tree_ncu.txt): split them evenly
+    const double f_sh2 = f_sh + 0.5 * a_sh, a_sh2 = 0.5 * a_sh;
+    f_pr += 0.5 * add_pr;
+    a_pr += 0.5 * add_pr;
+    fma_leaf = f_sh2 / blk;
+    alu_leaf = a_sh2 / blk;
     fma_prime = f_pr / blk;
     alu_prime = a_pr / blk;
   }
