@@ -203,14 +203,27 @@ __device__ int build_child(const int32_t* __restrict__ a, int n, const Child& ch
   return (all_rows && cols_ok) ? 1 : 0;
 }
 
+// Copies the warp's node into shared memory with coalesced loads (stage_words > 0), so the
+// row-by-row passes below read shared memory instead of issuing one short global load per row.
+__device__ __forceinline__ const int32_t* stage_node(const int32_t* __restrict__ g, int n, int stage_words,
+                                                     int lane) {
+  if (!stage_words) return g;
+  extern __shared__ int32_t esm[];
+  int32_t* s = esm + (threadIdx.x >> 5) * stage_words;
+  const int nn = n * n;
+  for (int e = lane; e < nn; e += 32) s[e] = g[e];
+  __syncwarp();
+  return s;
+}
+
 __global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, int n, int64_t count,
     int* __restrict__ kid_count, int* __restrict__ early_count, int* __restrict__ kid_mask,
-    int* __restrict__ err) {
+    int* __restrict__ err, int stage_words) {
   const int lane = threadIdx.x & 31;
   const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= count) return;
-  const int32_t* a = mats + node * (int64_t)n * n;
+  const int32_t* a = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
   const int64_t cf = coef ? coef[node] : 1;
   Plan pl = plan_node(a, n, cf, lane);
   int kids = 0, mask = 0;
@@ -235,11 +248,12 @@ __global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
     int n, int64_t count, const int* __restrict__ kid_mask, const int64_t* __restrict__ kid_off,
     const int64_t* __restrict__ early_off,
     int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef, int32_t* __restrict__ out_job,
-    int32_t* __restrict__ early_mats, int64_t* __restrict__ early_coef, int32_t* __restrict__ early_job) {
+    int32_t* __restrict__ early_mats, int64_t* __restrict__ early_coef, int32_t* __restrict__ early_job,
+    int stage_words) {
   const int lane = threadIdx.x & 31;
   const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= count) return;
-  const int32_t* a = mats + node * (int64_t)n * n;
+  const int32_t* a = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
   const int64_t cf = coef ? coef[node] : 1;
   const int32_t jb = job ? job[node] : (int32_t)node;
   Plan pl = plan_node(a, n, cf, lane);
@@ -299,7 +313,14 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   SPERM_CUDA(cudaMallocAsync((void**)&off, sizeof(int64_t) * (2 * count + 2), st));
   int64_t* eoff = off + count + 1;
   SPERM_CUDA(cudaMemsetAsync(err, 0, sizeof(int) * 4, st));
-  const unsigned blocks = (unsigned)((count * 32 + kExpThreads - 1) / kExpThreads);
+  // shared-memory staging of each warp's node: up to 8 warps per CTA within 200 KB
+  const int stage_words = ((n * n + 3) / 4) * 4;
+  const int wpb = std::max(1, std::min(8, (int)((200 * 1024) / (stage_words * 4))));
+  const size_t esmem = (size_t)wpb * stage_words * 4;
+  SPERM_CUDA(cudaFuncSetAttribute(expand_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+  SPERM_CUDA(cudaFuncSetAttribute(expand_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+  const unsigned bthreads = 32u * wpb;
+  const unsigned blocks = (unsigned)((count * 32 + bthreads - 1) / bthreads);
   int rc = SPERM_OK;
   auto cleanup = [&]() {
     cudaFreeAsync(kc, st);
@@ -308,7 +329,8 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   {
     TimingScope ts("expand", st);
     count_launch();
-    expand_count_kernel<<<blocks, kExpThreads, 0, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err);
+    expand_count_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err,
+                                                          stage_words);
   }
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) { cleanup(); return cuda_check(le, "expand_count_kernel"); }
@@ -345,9 +367,9 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   {
     TimingScope ts("expand", st);
     count_launch();
-    expand_emit_kernel<<<blocks, kExpThreads, 0, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
+    expand_emit_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
                                                        d_out_mats, d_out_coef, d_out_job, d_early_mats,
-                                                       d_early_coef, d_early_job);
+                                                       d_early_coef, d_early_job, stage_words);
   }
   le = cudaGetLastError();
   cleanup();
