@@ -204,6 +204,158 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
   }
 }
 
+// CTA-distributed register variant for 32 < n <= 8*CS, n <= 32*RL: one 256-thread CTA per
+// trial.  Thread (w, l) holds rows l + 32a (a < RL) and columns w + 8s (s < CS) of B in
+// registers.  Column k lives in warp k % 8, so the pivot search is one warp's REDUX; that warp
+// writes the pivot and the multipliers of every active row to shared memory (double-buffered:
+// one __syncthreads per elimination step), the pivot row's entries reach the other warps by
+// shuffles, and every thread updates its own entries.  Same arithmetic, same order and the
+// same first-maximum pivot rule (by position) as the reference, so values are bit-identical.
+template <int RL, int CS>
+__global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+                                                           const int32_t* __restrict__ ids, int trials,
+                                                           uint64_t seed, double* __restrict__ xout) {
+  extern __shared__ double2 kfill[];  // [n*n] fill buffer, then lbuf[2][32*RL], piv[2]
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double2* lbuf = kfill + n * n;
+  double* pivd = reinterpret_cast<double*>(lbuf + 2 * 32 * RL);  // [2] d
+  int* pivi = reinterpret_cast<int*>(pivd + 2);                    // [2][2] (row p, position bp)
+  const double S32 = 0.8660254037844386;
+  const int64_t items = count * (int64_t)trials;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t job = item / trials;
+    const int trial = (int)(item % trials);
+    const int32_t* a = mats + job * (int64_t)n * n;
+    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
+    __syncthreads();  // previous trial done with the shared buffers
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - (e / n) * n;
+      double r = 0.0, s = 0.0;
+      if (a[e] != 0) {
+        const int ri = root_index(key, (uint64_t)i, (uint64_t)j);
+        r = ri == 0 ? 1.0 : -0.5;
+        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
+      }
+      kfill[e] = make_double2(r, s);
+    }
+    __syncthreads();
+    double re[RL][CS], im[RL][CS];
+    int pos[RL];
+    bool act[RL];
+#pragma unroll
+    for (int ra = 0; ra < RL; ++ra) {
+      const int row = l + 32 * ra;
+      pos[ra] = row;
+      act[ra] = row < n;
+#pragma unroll
+      for (int s = 0; s < CS; ++s) {
+        const int col = w + 8 * s;
+        double2 v = make_double2(0.0, 0.0);
+        if (row < n && col < n) v = kfill[row * n + col];
+        re[ra][s] = v.x;
+        im[ra][s] = v.y;
+      }
+    }
+    double x = 1.0;
+    bool done = false;
+#pragma unroll
+    for (int sk = 0; sk < CS; ++sk) {
+      for (int wk = 0; wk < 8; ++wk) {
+        const int k = 8 * sk + wk;
+        if (done || k >= n) break;
+        const int buf = k & 1;
+        if (w == wk) {
+          // pivot over the active rows: my rows, then the warp (hi/lo bit pattern, position)
+          double bm = -1.0;
+          int bpos = 0x7fffffff, ba = 0;
+#pragma unroll
+          for (int ra = 0; ra < RL; ++ra) {
+            if (act[ra]) {
+              const double m = __dadd_rn(__dmul_rn(re[ra][sk], re[ra][sk]), __dmul_rn(im[ra][sk], im[ra][sk]));
+              if (m > bm || (m == bm && pos[ra] < bpos)) { bm = m; bpos = pos[ra]; ba = ra; }
+            }
+          }
+          const bool any = bpos != 0x7fffffff;
+          const unsigned mh = any ? (unsigned)__double2hiint(bm) : 0u, ml = any ? (unsigned)__double2loint(bm) : 0u;
+          const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
+          const bool c1 = any && mh == bh;
+          const unsigned blo = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
+          const bool c2 = c1 && ml == blo;
+          const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)bpos : 0xffffffffu);
+          const int pl = __ffs(__ballot_sync(0xffffffffu, c2 && bpos == bp)) - 1;
+          const double d = __hiloint2double((int)bh, (int)blo);
+          const int pa = __shfl_sync(0xffffffffu, ba, pl);
+          double pr = 0.0, pi = 0.0;
+#pragma unroll
+          for (int ra = 0; ra < RL; ++ra)
+            if (ra == pa) { pr = re[ra][sk]; pi = im[ra][sk]; }
+          pr = __shfl_sync(0xffffffffu, pr, pl);
+          pi = __shfl_sync(0xffffffffu, pi, pl);
+          const int p = pl + 32 * pa;
+          // multipliers of the rows that stay active (position > k after the exchange)
+          if (d != 0.0) {
+#pragma unroll
+            for (int ra = 0; ra < RL; ++ra) {
+              const int row = l + 32 * ra;
+              int np = pos[ra];
+              if (row == p) np = k;
+              else if (act[ra] && np == k) np = bp;
+              if (act[ra] && np > k) {
+                const double xr = re[ra][sk], xi = im[ra][sk];
+                lbuf[buf * 32 * RL + row] =
+                    make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d),
+                                 __ddiv_rn(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d));
+              }
+            }
+          }
+          if (l == 0) {
+            pivd[buf] = d;
+            pivi[2 * buf] = p;
+            pivi[2 * buf + 1] = bp;
+          }
+        }
+        __syncthreads();
+        const double d = pivd[buf];
+        const int p = pivi[2 * buf], bp = pivi[2 * buf + 1];
+        if (d == 0.0) { x = 0.0; done = true; break; }
+        x = __dmul_rn(x, d);
+        if (k + 1 == n) { done = true; break; }
+#pragma unroll
+        for (int ra = 0; ra < RL; ++ra) {
+          const int row = l + 32 * ra;
+          if (row == p) pos[ra] = k;
+          else if (act[ra] && pos[ra] == k) pos[ra] = bp;
+          act[ra] = act[ra] && pos[ra] > k;
+        }
+        // the pivot row's entries of my columns, from lane p % 32 of this warp
+        const int pa = p >> 5, plane = p & 31;
+        double2 lm[RL];
+#pragma unroll
+        for (int ra = 0; ra < RL; ++ra)
+          lm[ra] = act[ra] ? lbuf[buf * 32 * RL + l + 32 * ra] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+          if (w + 8 * s <= k) continue;  // warp-uniform: finished columns
+          double ur = 0.0, ui = 0.0;
+#pragma unroll
+          for (int ra = 0; ra < RL; ++ra)
+            if (ra == pa) { ur = re[ra][s]; ui = im[ra][s]; }
+          ur = __shfl_sync(0xffffffffu, ur, plane);
+          ui = __shfl_sync(0xffffffffu, ui, plane);
+#pragma unroll
+          for (int ra = 0; ra < RL; ++ra) {
+            if (act[ra]) {
+              re[ra][s] = __dsub_rn(re[ra][s], __dsub_rn(__dmul_rn(lm[ra].x, ur), __dmul_rn(lm[ra].y, ui)));
+              im[ra][s] = __dsub_rn(im[ra][s], __dadd_rn(__dmul_rn(lm[ra].x, ui), __dmul_rn(lm[ra].y, ur)));
+            }
+          }
+        }
+      }
+    }
+    if (threadIdx.x == 0) xout[item] = x;
+  }
+}
+
 __global__ void kklll_mean_kernel(const double* __restrict__ xs, int64_t count, int trials,
                                   double* __restrict__ est) {
   const int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -241,6 +393,21 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     TimingScope ts("kklll", st);
     count_launch();
     kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+  } else if (n <= 96) {
+    // CTA-distributed registers: rows per lane RL = ceil(n/32), column slots per thread CS = ceil(n/8)
+    const int CSn = (n + 7) / 8;
+    auto kern = n <= 64 ? kklll_cta_kernel<2, 8> : CSn <= 9 ? kklll_cta_kernel<3, 9>
+                                             : CSn <= 10 ? kklll_cta_kernel<3, 10> : kklll_cta_kernel<3, 12>;
+    const int RLn = n <= 64 ? 2 : 3;
+    const size_t smem = sizeof(double2) * ((size_t)n * n + 2 * 32 * RLn) + 2 * sizeof(double) + 4 * sizeof(int);
+    SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+    grid = std::max<int64_t>(1, std::min(grid, items));
+    TimingScope ts("kklll", st);
+    count_launch();
+    kern<<<(unsigned)grid, 256, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else {
     const size_t per_warp = sizeof(double) * 2 * n * n;
     int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));

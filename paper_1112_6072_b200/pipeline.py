@@ -188,7 +188,7 @@ def reconstruct(res, k: int):
 
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
-              device="cuda", measure_jobs: bool = False) -> PHResult:
+              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 8 << 30) -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
 
     With a torch.distributed `group` of world size G, every rank replicates the
@@ -226,7 +226,7 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             idx = torch.tensor(sel[b0:b0 + batch_jobs], dtype=torch.int64, device=device)
             batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
                             s.job.index_select(0, idx))
-            for lv in iter_leaves(batch, leaf_order):
+            for lv in iter_leaves(batch, leaf_order, leaf_budget_bytes):
                 if lv.n > S.NMAX:
                     raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
                 cyc = torch.zeros(lv.count, dtype=torch.int64, device=device) if measure_jobs else None

@@ -178,6 +178,22 @@ def test_kklll_bit_exact_trials():
             assert abs(float(est[j]) - e) <= 1e-12 * abs(e)
 
 
+@pytest.mark.parametrize("n", [33, 47, 64, 65, 77, 96, 100])
+def test_kklll_bit_exact_large_orders(n):
+    """CTA-distributed kernel (32 < n <= 96) and the shared-memory kernel (n > 96):
+    every trial bit-identical to the oracle, including singular (zero) trials."""
+    rng = np.random.default_rng(n)
+    mats = (rng.random((2, n, n)) < 3.5 / n).astype(np.int64)
+    mats[:, np.arange(n), np.arange(n)] = 1
+    mats[1, :, 0] = 0  # a zero column: |det| = 0 in every trial
+    est, xs = P.sperm_estimate(dev(mats), trials=5, seed=3, keep_trials=True)
+    xs = xs.cpu().numpy()
+    for j in range(2):
+        ref = [kklll_trial(mats[j], 3, j, t) for t in range(5)]
+        assert np.array_equal(xs[j], np.array(ref)), (n, j)
+    assert (xs[1] == 0).all()
+
+
 def test_kklll_ids_and_default_trials():
     a = dodecahedron()
     est = P.sperm_estimate(dev(a[None]), trials=0, seed=3, ids=dev([5]))
@@ -221,6 +237,26 @@ def test_pipeline_fullerenes_config4():
             assert r.value == want, (n, iso)
             checked += 1
     assert checked >= 12
+
+
+def test_pipeline_streamed_leaves_tiny_budget():
+    """iter_leaves splits levels that would exceed the HBM budget into chunks (depth first):
+    a 256 KB budget forces many splits; per-job values and the total must not change."""
+    a = truncated_icosahedron()
+    r1 = pipeline.permanent(a, jobs_at_least=16, leaf_order=24)
+    r2 = pipeline.permanent(a, jobs_at_least=16, leaf_order=24, leaf_budget_bytes=256 << 10)
+    assert r1.value == r2.value == golden("C60_truncated_icosahedron")
+    assert r1.job_values == r2.job_values and r1.leaves == r2.leaves
+
+
+def test_pipeline_measure_jobs_and_signed_input():
+    """Per-job cycle counters are filled for every job; a signed matrix (no prime cap)."""
+    a = dodecahedron()
+    r = pipeline.permanent(a, jobs_at_least=12, leaf_order=10, measure_jobs=True)
+    assert r.value == 1392 and len(r.job_cycles) == r.num_jobs and (r.job_cycles > 0).all()
+    rng = np.random.default_rng(4)
+    b = a * rng.choice([-3, -1, 2, 5], size=a.shape)
+    assert pipeline.permanent(b, jobs_at_least=20, leaf_order=12).value == h_per(b)
 
 
 def test_pipeline_c60_leaf16():
