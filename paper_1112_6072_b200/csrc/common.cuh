@@ -38,6 +38,7 @@ struct TimingScope {
 };
 
 int sm_count();
+void keep_pool_memory();  // keep the default mempool's memory between calls (host.cu)
 void count_launch(int k = 1);  // own-kernel launch counter (sperm_launch_count)
 
 }  // namespace sperm

@@ -296,6 +296,7 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
                             int64_t cap_out, int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
                             int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  keep_pool_memory();
   if (!h_out_count || !h_early_count) return set_error(SPERM_ERR_ARG, "sperm_expand: NULL count outputs");
   *h_out_count = 0;
   *h_early_count = 0;

@@ -26,6 +26,23 @@ int cuda_check(cudaError_t e, const char* what) {
 static std::atomic<long long> g_launches{0};
 void count_launch(int k) { g_launches += k; }
 
+// The library's scratch buffers come from the device's default stream-ordered pool
+// (cudaMallocAsync).  With the default release threshold (0) the pool returns its memory to
+// the driver at every synchronization, so the next allocation has to map pages again; keep it.
+void keep_pool_memory() {
+  static std::atomic<unsigned> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) return;
+  const unsigned bit = 1u << dev;
+  if (done.load() & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  done.fetch_or(bit);
+}
+
 int sm_count() {
   static int cached = 0;
   if (!cached) {

@@ -374,6 +374,7 @@ using namespace sperm;
 extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d_ids, int trials,
                               uint64_t seed, double* d_est, double* d_trials_out, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  keep_pool_memory();
   if (n < 1 || n > kKNmax) return set_error(SPERM_ERR_ARG, "sperm_estimate: n out of range [1, 112]");
   if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_estimate: count < 0");
   if (trials <= 0) trials = n * n;

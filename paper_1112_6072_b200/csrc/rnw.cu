@@ -1016,6 +1016,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
                                int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
                                uint64_t* d_job_acc, uint64_t* d_leaf_cycles, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  keep_pool_memory();
   if (n < 0 || n > SPERM_NMAX) return set_error(SPERM_ERR_ARG, "sperm_permanent: n out of range [0, 48]");
   if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_permanent: count < 0");
   if (min_primes < 1 || min_primes > SPERM_KMAX)

@@ -128,7 +128,7 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
     return _cat([level] + early)
 
 
-def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30):
+def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30, stats=None):
     """The same H_per recursion as expand_to_leaves, streamed: a level whose children could
     exceed `budget_bytes` of HBM is split into chunks that are expanded to their leaves one
     after another (depth first over chunks), so the live node sets stay bounded however many
@@ -148,7 +148,13 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30):
                 sl = slice(c0, min(level.count, c0 + cap))
                 stack.append(NodeSet(level.n, level.mats[sl], level.coef[sl], level.job[sl]))
             continue
+        if stats is not None:
+            import time
+            t0 = time.perf_counter()
         (km, kc, kj), (em, ec, ej) = S.sperm_expand(level.mats, level.coef, level.job)
+        if stats is not None:
+            stats["expand_calls"] = stats.get("expand_calls", 0) + 1
+            stats["expand_host_s"] = stats.get("expand_host_s", 0.0) + time.perf_counter() - t0
         if em.shape[0]:
             yield NodeSet(level.n, em, ec, ej)
         stack.append(NodeSet(level.n - 1, km, kc, kj))
@@ -218,6 +224,16 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     pos = rank_positions(machine, order, rank)
     leaves = 0
     terms = 0.0
+    import time
+    stats = {"rnw_calls": 0, "rnw_host_s": 0.0, "leaf_sets": 0, "t_loop_s": 0.0}
+    t_loop = time.perf_counter()
+    # R-NW batches run on their own stream, so the expansion of the next chunk (on the current
+    # stream, with its host round trips) overlaps the integer-bound R-NW of the previous one.
+    main = torch.cuda.current_stream()
+    rnw_stream = torch.cuda.Stream()
+    acc.record_stream(rnw_stream)
+    if measure_jobs:
+        job_cycles.record_stream(rnw_stream)
     for s in jobsets:
         ids = s.job.cpu().numpy()
         sel = np.nonzero(pos[ids] >= 0)[0]
@@ -226,16 +242,27 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             idx = torch.tensor(sel[b0:b0 + batch_jobs], dtype=torch.int64, device=device)
             batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
                             s.job.index_select(0, idx))
-            for lv in iter_leaves(batch, leaf_order, leaf_budget_bytes):
+            for lv in iter_leaves(batch, leaf_order, leaf_budget_bytes, stats):
                 if lv.n > S.NMAX:
                     raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
-                cyc = torch.zeros(lv.count, dtype=torch.int64, device=device) if measure_jobs else None
-                S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
-                                  max_primes=k_total if nonneg else 0, job_acc=acc, leaf_cycles=cyc)
-                if measure_jobs:  # measured job cost T_i = SM cycles of its leaves
-                    job_cycles.index_add_(0, lv.job.long(), cyc)
+                stats["leaf_sets"] += 1
+                t_r = time.perf_counter()
+                rnw_stream.wait_stream(main)  # the leaves were written on the main stream
+                for t in (lv.mats, lv.coef, lv.job):
+                    t.record_stream(rnw_stream)  # keep them alive until the R-NW batch is done
+                with torch.cuda.stream(rnw_stream):
+                    cyc = torch.zeros(lv.count, dtype=torch.int64, device=device) if measure_jobs else None
+                    S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
+                                      max_primes=k_total if nonneg else 0, job_acc=acc, leaf_cycles=cyc,
+                                      stream=rnw_stream)
+                    if measure_jobs:  # measured job cost T_i = SM cycles of its leaves
+                        job_cycles.index_add_(0, lv.job.long(), cyc)
+                stats["rnw_calls"] += 1
+                stats["rnw_host_s"] += time.perf_counter() - t_r
                 leaves += lv.count
                 terms += S.sperm_rnw_terms(lv.n, lv.count)
+    main.wait_stream(rnw_stream)
+    stats["t_loop_s"] = time.perf_counter() - t_loop
     allreduce_accumulators(acc, group)
     res = S.sperm_reduce_mod(acc).cpu().numpy().view(np.uint32)
     job_values, value = reconstruct(res, k_total)
@@ -243,4 +270,4 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
                     job_order_n={s.n: s.count for s in jobsets}, leaves=leaves, terms=terms,
                     estimates=est, machine=machine,
                     job_cycles=job_cycles.cpu().numpy() if measure_jobs else None,
-                    job_sizes=job_sizes(jobsets, num_jobs))
+                    job_sizes=job_sizes(jobsets, num_jobs), stats=stats)

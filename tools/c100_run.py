@@ -24,6 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=159)
     ap.add_argument("--leaf", type=int, default=20)
+    ap.add_argument("--budget-gb", type=float, default=8.0, help="HBM budget of a streamed expansion level")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c100.json"))
     args = ap.parse_args()
     import numpy as np
@@ -43,7 +44,8 @@ def main():
     P.sperm_rnw_stats(reset=True)
     P.sperm_expand_stats(reset=True)
     t0 = time.perf_counter()
-    r = pipeline.permanent(a, jobs_at_least=args.jobs, leaf_order=args.leaf, measure_jobs=True)
+    r = pipeline.permanent(a, jobs_at_least=args.jobs, leaf_order=args.leaf, measure_jobs=True,
+                           leaf_budget_bytes=int(args.budget_gb * (1 << 30)))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     stages = {s: P.sperm_timing_get(s)[0] for s in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
@@ -57,7 +59,8 @@ def main():
            "leaves": r.leaves, "terms": terms, "stage_ms": stages,
            "terms_per_s_rnw": terms / (stages["rnw"] * 1e-3) if stages["rnw"] else None,
            "expand_GBps": xb / (stages["expand"] * 1e-3) / 1e9 if stages["expand"] else None,
-           "tau_T_estimate": float(kendalltau(T, r.estimates).statistic),
+           "tau_T_estimate": float(kendalltau(T, r.estimates).statistic), "host": r.stats,
+           "launches": P.sperm_launch_count(),
            "paper_T1_s_PentiumIII": 118413.21, "paper_T32_s_32xPentiumIII": 3796.85}
     print(json.dumps(out), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
