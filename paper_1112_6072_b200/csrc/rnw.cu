@@ -36,6 +36,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -98,6 +99,14 @@ __device__ __forceinline__ int meta_k(int2 m) { return m.x & 0xff; }
 __device__ __forceinline__ int meta_plan(int2 m) { return (m.x >> 8) & 0xff; }
 __device__ __forceinline__ int meta_G(int2 m) { return (m.x >> 24) & 0xff; }
 
+// log2(r!)/r for r = 1..SPERM_NMAX (Bregman-Minc), computed once per process on first use
+__device__ double d_breg[SPERM_NMAX + 1];
+__device__ __forceinline__ double breg_term(int r) { return d_breg[r]; }
+__global__ void breg_init_kernel() {
+  const int r = threadIdx.x;
+  if (r <= SPERM_NMAX) d_breg[r] = r > 0 ? lgamma((double)r + 1.0) / ((double)r * 0.6931471805599453) : 0.0;
+}
+
 // ============================================================================ prep
 // One warp per leaf.  Row / column abs sums -> number of primes k, generic group size G;
 // then the tree plan: 32 lanes run the greedy disjoint-support column pick from 32
@@ -110,7 +119,20 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   const int wib = threadIdx.x >> 5;
   const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (leaf >= count) return;
-  const int32_t* a = mats + leaf * (int64_t)n * n;
+  // stage the leaf in shared memory with coalesced loads; the per-lane row/column scans
+  // below then read shared memory (one warp per leaf, 8 warps per CTA)
+  extern __shared__ int32_t prep_sm[];
+  const int ns = n + 1;  // padded row stride: the row scans a[i*ns + j] hit distinct banks
+  int32_t* sa = prep_sm + wib * (n * ns);
+  {
+    const int32_t* g = mats + leaf * (int64_t)n * n;
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n;
+      sa[i * ns + (e - i * n)] = g[e];
+    }
+    __syncwarp();
+  }
+  const int32_t* a = sa;
   __shared__ int64_t sR[8][SPERM_NMAX];
   __shared__ unsigned long long sSupp[8][SPERM_NMAX];
   __shared__ int sCnt[8][SPERM_NMAX];
@@ -124,10 +146,10 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     unsigned long long sm = 0;
     int nz = 0;
     for (int j = 0; j < n; ++j) {
-      const int32_t u = a[i * n + j];
+      const int32_t u = a[i * ns + j];
       r += llabs((long long)u);
       if (u != 0 && u != 1) binary = false;
-      const int32_t v = a[j * n + i];
+      const int32_t v = a[j * ns + i];
       c += llabs((long long)v);
       if (v != 0) { sm |= 1ull << j; ++nz; }
     }
@@ -138,11 +160,12 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     if (r >= (1ll << 30)) range_bad = true;
     if (r > 0) {
       lr += log2((double)r);
-      br += lgamma((double)r + 1.0) / ((double)r * 0.6931471805599453);
+      // Bregman term log2(r!)/r; only used when the leaf is 0/1, where r = count <= n <= 48
+      if (r <= SPERM_NMAX) br += breg_term((int)r);
     }
     if (c > 0) {
       lc += log2((double)c);
-      bc += lgamma((double)c + 1.0) / ((double)c * 0.6931471805599453);
+      if (c <= SPERM_NMAX) bc += breg_term((int)c);
     }
   }
   for (int o = 16; o; o >>= 1) {
@@ -226,10 +249,13 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   if (pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0) {
     const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
     if (np >= B && n - 6 >= B) {
+      // saturating product of non-negative bounds (no 64-bit division): saturate at 2^40 when the
+      // operands' bit lengths could reach 2^62; every threshold tested below is < 2^31
       auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
         if (x == 0 || y == 0) return 0;
-        if (x > ((int64_t)1 << 40) / y) return (int64_t)1 << 40;
-        return x * y;
+        if ((64 - __clzll(x)) + (64 - __clzll(y)) > 62) return (int64_t)1 << 40;
+        const int64_t p = x * y;
+        return p > ((int64_t)1 << 40) ? ((int64_t)1 << 40) : p;
       };
       const int ZL = B2 < 2 ? B2 : 2;  // exact Z_lo columns; the rest (<= 2) form Z_hi
       int64_t X = 1, Zlo = 1, Zhi = 1;
@@ -1024,6 +1050,18 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   if (max_primes != 0 && (max_primes < min_primes || max_primes > SPERM_KMAX))
     return set_error(SPERM_ERR_ARG, "sperm_permanent: max_primes must be 0 or in [min_primes, 8]");
   if (count == 0) return SPERM_OK;
+  {  // the Bregman table of the prep kernel, once per device
+    static std::atomic<unsigned> breg_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned bit = 1u << (dev & 31);
+    if (!(breg_done.load() & bit)) {
+      count_launch();
+      breg_init_kernel<<<1, 64, 0, st>>>();
+      SPERM_LAUNCH_CHECK("breg_init_kernel");
+      breg_done.fetch_or(bit);
+    }
+  }
   if (n > 0 && !d_mats) return set_error(SPERM_ERR_ARG, "sperm_permanent: d_mats is NULL");
   if (d_job_acc && d_job && num_jobs <= 0) return set_error(SPERM_ERR_ARG, "sperm_permanent: num_jobs");
   const int NPg = n <= 8 ? 8 : ((n + 7) / 8) * 8;
@@ -1066,7 +1104,9 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     TimingScope ts("rnw_prep", st);
     const int64_t threads = count * 32;
     count_launch();
-    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
+    const size_t prep_smem = (size_t)8 * n * (n + 1) * sizeof(int32_t);  // padded rows, 8 warps
+    SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
+    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
     count_launch();
