@@ -840,7 +840,12 @@ StreamPool& stream_pool() {
 // leaf holds at least one 32-lane chunk.
 int choose_m(int n, int64_t nleaves, int mmin) {
   const int tb = n - 1;
-  const double target_items = (double)sm_count() * 16.0 * 8.0;
+  static const double per_warp = [] {  // A-B knob: SPERM_RNW_ITEMS_PER_WARP (default 2, measured
+    const char* e = getenv("SPERM_RNW_ITEMS_PER_WARP");  // best of 1/2/4/8 on configs[1])
+    const double v = e ? atof(e) : 0.0;
+    return v > 0.0 ? v : 2.0;
+  }();
+  const double target_items = (double)sm_count() * 16.0 * per_warp;
   const double per_lane = std::ldexp((double)nleaves, tb) / (32.0 * target_items);
   int m = per_lane >= 1.0 ? (int)std::floor(std::log2(per_lane)) : 0;
   m = std::min(m, kMaxLaneBits);
