@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ph", action="store_true", help="skip the whole-path per(C60) measurement")
     ap.add_argument("--ph-leaf", type=int, default=32, help="leaf order L of the per(C60) run")
+    ap.add_argument("--no-c100", action="store_true", help="skip the per(C100) run (the paper's case study)")
     return ap.parse_args()
 
 
@@ -213,12 +214,75 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_ph:
         out["ph"] = bench_ph(P, torch, leaf_order=args.ph_leaf)
+    if rank == 0 and world == 1 and not args.no_ph:
+        try:
+            out["expand_roofline"] = bench_expand(P, torch)
+        except Exception as e:
+            out["expand_roofline"] = {"error": repr(e)[:300]}
+    if rank == 0 and world == 1 and not args.no_c100:
+        try:
+            out["ph_c100"] = bench_c100(P, torch)
+        except Exception as e:  # reported, never fatal for the main line
+            out["ph_c100"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(h_np)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_expand(P, torch, jobs_at_least: int = 200000, reps: int = 3):
+    """HBM roofline of one Eq. (2) expansion level (sperm_expand: count + scan + emit kernels):
+    C100 pre-expanded to >= 2e5 nodes, that level expanded `reps` times (library event timers)."""
+    from paper_1112_6072_b200 import pipeline
+    from workloads import paper_graph
+    s = pipeline.pre_expand(pipeline.root_nodeset(paper_graph("C100")), jobs_at_least=jobs_at_least)[0]
+    P.sperm_expand(s.mats, s.coef, s.job)  # warm-up
+    torch.cuda.synchronize()
+    P.sperm_timing_enable(True)
+    P.sperm_timing_reset()
+    P.sperm_expand_stats(reset=True)
+    for _ in range(reps):
+        P.sperm_expand(s.mats, s.coef, s.job)
+    torch.cuda.synchronize()
+    ms, launches = P.sperm_timing_get("expand")
+    nbytes, nodes = P.sperm_expand_stats(reset=True)
+    P.sperm_timing_enable(False)
+    pk, pk_kind = peaks()
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+            "frac": gbs / pk["hbm_gbs"] if pk.get("hbm_gbs") else None, "traffic": None,
+            "kernel": "expand_count_kernel + expand_emit_kernel", "level": {"n": s.n, "nodes": s.count},
+            "ms_per_level": ms / reps, "algorithmic_bytes_per_level": nbytes / reps,
+            "peak_note": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy)"}
+
+
+def bench_c100(P, torch, leaf_order: int = 16, jobs_at_least: int = 159):
+    """per(C100) — the paper's own case study (§4.1): the appendix graph by the whole
+    path, checked against Table T12's printed Total (tests/golden/paper_pins.txt).
+    The paper: 118413.21 s on one Pentium III (Table 5), 3796.85 s on 32 (Table 6)."""
+    from paper_1112_6072_b200 import pipeline
+    from workloads import paper_graph
+    pin = None
+    for ln in open(os.path.join(ROOT, "tests", "golden", "paper_pins.txt")):
+        if ln.startswith("per_C100 "):
+            pin = int(ln.split()[1])
+    P.sperm_timing_enable(True)
+    P.sperm_timing_reset()
+    P.sperm_rnw_stats(reset=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = pipeline.permanent(paper_graph("C100"), jobs_at_least=jobs_at_least, leaf_order=leaf_order)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw")}
+    terms = P.sperm_rnw_stats(reset=True)[0]
+    P.sperm_timing_enable(False)
+    return {"workload": f"per(C100), PAPER.md appendix graph; J>={jobs_at_least}, leaves of order <= {leaf_order}",
+            "per": str(r.value), "paper_table_T12_total": str(pin), "matches_paper": r.value == pin,
+            "wall_s": wall, "jobs": r.num_jobs, "leaves": r.leaves, "terms": terms,
+            "stage_ms_overlapping": stages, "paper_T1_s": 118413.21, "paper_T32_s": 3796.85}
 
 
 def bench_ph(P, torch, leaf_order: int = 32, jobs_at_least: int = 992):

@@ -58,6 +58,12 @@ uint32_t sperm_prime(int i);
  * (limbs >= k+1 suffices).  Garner's algorithm. */
 int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int* h_sign);
 
+/* sperm_crt over `count` rows (host, synchronous): row r has residues
+ * h_residues[r*stride .. r*stride + h_k[r]) (h_k NULL: every row uses k_all primes) and
+ * writes h_mag[r*limbs .. (r+1)*limbs) and h_sign[r]. */
+int sperm_crt_batch(const uint32_t* h_residues, int64_t count, int stride, const int32_t* h_k, int k_all,
+                    uint32_t* h_mag, int limbs, int* h_sign);
+
 /* Number of CRT primes that reconstruct per(A) of one HOST matrix h_mat [n][n] (host,
  * synchronous): |per(A)| <= min(prod_i sum_j |a_ij|, prod_j sum_i |a_ij|), and for a 0/1
  * matrix the Bregman-Minc bound prod_i (r_i!)^(1/r_i) (rows and columns).  SPERM_ERR_PRIMES

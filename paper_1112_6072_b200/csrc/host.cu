@@ -187,6 +187,18 @@ int sperm_timing_get(const char* name, double* h_ms, int64_t* h_launches) {
 // ------------------------------------------------------------------ CRT
 // Garner's algorithm: mixed-radix digits v_i with x = v_0 + p_0 (v_1 + p_1 (v_2 + ...)),
 // then x is expanded into base-2^32 limbs; the symmetric representative is taken.
+int sperm_crt_batch(const uint32_t* h_residues, int64_t count, int stride, const int32_t* h_k, int k_all,
+                    uint32_t* h_mag, int limbs, int* h_sign) {
+  if (count < 0 || (count > 0 && (!h_residues || !h_mag || !h_sign)) || stride < 1)
+    return set_error(SPERM_ERR_ARG, "sperm_crt_batch: bad arguments");
+  for (int64_t r = 0; r < count; ++r) {
+    const int k = h_k ? h_k[r] : k_all;
+    const int rc = sperm_crt(h_residues + r * stride, k, h_mag + r * limbs, limbs, h_sign + r);
+    if (rc != SPERM_OK) return rc;
+  }
+  return SPERM_OK;
+}
+
 int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int* h_sign) {
   if (!h_residues || !h_mag || !h_sign || k < 1 || k > SPERM_KMAX || limbs < k + 1)
     return set_error(SPERM_ERR_ARG, "sperm_crt: bad arguments");

@@ -40,6 +40,7 @@ _SIGS = {
     "sperm_last_error": (ctypes.c_char_p, []),
     "sperm_prime": (ctypes.c_uint32, [_I]),
     "sperm_crt": (_I, [_P, _I, _P, _I, _P]),
+    "sperm_crt_batch": (_I, [_P, _I64, _I, _P, _I, _P, _I, _P]),
     "sperm_bound_primes": (_I, [_P, _I, _P]),
     "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P]),
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
@@ -190,9 +191,22 @@ def residues_to_ints(res, k) -> List[int]:
         res = res.cpu().numpy()
     if isinstance(k, torch.Tensor):
         k = k.cpu().numpy()
-    res = np.asarray(res).view(np.uint32)
-    k = np.broadcast_to(np.asarray(k), (res.shape[0],))
-    return [sperm_crt(res[i], int(k[i])) for i in range(res.shape[0])]
+    res = np.ascontiguousarray(np.asarray(res).view(np.uint32))
+    count = res.shape[0]
+    if count == 0:
+        return []
+    ks = np.ascontiguousarray(np.broadcast_to(np.asarray(k), (count,)).astype(np.int32))
+    limbs = KMAX + 2
+    mag = np.zeros((count, limbs), dtype=np.uint32)
+    sign = np.zeros(count, dtype=np.int32)
+    _check(lib().sperm_crt_batch(res.ctypes.data, count, res.shape[1], ks.ctypes.data, 0, mag.ctypes.data,
+                                 limbs, sign.ctypes.data))
+    # little-endian uint32 limbs -> Python ints (marshalling)
+    out = []
+    for r in range(count):
+        v = int.from_bytes(mag[r].tobytes(), "little")
+        out.append(int(sign[r]) * v)
+    return out
 
 
 # --------------------------------------------------------------------- expansion
