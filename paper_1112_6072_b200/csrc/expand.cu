@@ -14,6 +14,7 @@
 //   row pivot r, cofactor at p:     delete row r, column p;   coef *= a_rp
 //   column pivot c (= row pivot of A^T, reading R2): the same with rows and columns exchanged.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include <cub/device/device_scan.cuh>
@@ -44,7 +45,8 @@ struct Plan {
 __device__ __forceinline__ int32_t ld(const int32_t* a, int n, int i, int j) { return a[i * n + j]; }
 
 // Pivot selection and the Eq. (2) children of one node (warp-uniform result).
-__device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, int lane) {
+__device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, int lane, int* rowcnt_out = nullptr,
+                          int* colcnt_out = nullptr) {
   int colcnt[kMaxChunks];
 #pragma unroll
   for (int c = 0; c < kMaxChunks; ++c) colcnt[c] = 0;
@@ -62,6 +64,15 @@ __device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, in
       }
     }
     best_row_key = min(best_row_key, (rc << 8) | i);
+    if (rowcnt_out && lane == 0) rowcnt_out[i] = rc;
+  }
+  if (colcnt_out) {
+#pragma unroll
+    for (int c = 0; c < kMaxChunks; ++c) {
+      const int j = c * 32 + lane;
+      if (c < nch && j < n) colcnt_out[j] = colcnt[c];
+    }
+    __syncwarp();
   }
   int best_col_key = 0x7fffffff;
 #pragma unroll
@@ -203,6 +214,52 @@ __device__ int build_child(const int32_t* __restrict__ a, int n, const Child& ch
   return (all_rows && cols_ok) ? 1 : 0;
 }
 
+// Survival test of a child (reading R4: no zero row or column) from the parent's line counts
+// and the few lines the child changes — O(n) per child instead of rebuilding it.  Row i of a
+// column-merge child is nonzero iff it keeps a nonzero outside the two merged columns or its
+// merged entry is nonzero; an unmerged column is nonzero iff it has a nonzero outside the
+// deleted row; the merged column iff some merged entry is nonzero (and symmetrically for a
+// row merge, which is a column pivot).  Also flags int32 overflow of merged entries.
+__device__ int survives(const int32_t* __restrict__ a, int n, const Child& ch, const int* __restrict__ rowcnt,
+                        const int* __restrict__ colcnt, int lane, bool* ovf) {
+  bool ok = true, over = false, merged_nz = false;
+  if (ch.merge == 0) {
+    const int r = ch.del_row, p = ch.del_col;
+    for (int i = lane; i < n; i += 32) {
+      if (i != r && rowcnt[i] - (ld(a, n, i, p) != 0) == 0) ok = false;
+      if (i != p && colcnt[i] - (ld(a, n, r, i) != 0) == 0) ok = false;
+    }
+    merged_nz = true;
+  } else if (ch.merge == 1) {  // row pivot r: column keep := al*col(del_col) + be*col(keep)
+    const int r = ch.del_row, ka = ch.keep, kb = ch.del_col;
+    for (int i = lane; i < n; i += 32) {
+      if (i != r) {
+        const int32_t va = ld(a, n, i, ka), vb = ld(a, n, i, kb);
+        const long long mv = (long long)ch.al * vb + (long long)ch.be * va;
+        if (mv > INT32_MAX || mv < INT32_MIN) over = true;
+        if (mv != 0) merged_nz = true;
+        else if (rowcnt[i] - (va != 0) - (vb != 0) == 0) ok = false;
+      }
+      if (i != ka && i != kb && colcnt[i] - (ld(a, n, r, i) != 0) == 0) ok = false;
+    }
+  } else {  // column pivot c: row keep := al*row(del_row) + be*row(keep)
+    const int c = ch.del_col, ka = ch.keep, kb = ch.del_row;
+    for (int j = lane; j < n; j += 32) {
+      if (j != c) {
+        const int32_t va = ld(a, n, ka, j), vb = ld(a, n, kb, j);
+        const long long mv = (long long)ch.al * vb + (long long)ch.be * va;
+        if (mv > INT32_MAX || mv < INT32_MIN) over = true;
+        if (mv != 0) merged_nz = true;
+        else if (colcnt[j] - (va != 0) - (vb != 0) == 0) ok = false;
+      }
+      if (j != ka && j != kb && rowcnt[j] - (ld(a, n, j, c) != 0) == 0) ok = false;
+    }
+  }
+  ok = __all_sync(0xffffffffu, ok) && __any_sync(0xffffffffu, merged_nz);
+  if (__any_sync(0xffffffffu, over)) *ovf = true;
+  return ok ? 1 : 0;
+}
+
 // Copies the warp's node into shared memory with coalesced loads (stage_words > 0), so the
 // row-by-row passes below read shared memory instead of issuing one short global load per row.
 __device__ __forceinline__ const int32_t* stage_node(const int32_t* __restrict__ g, int n, int stage_words,
@@ -219,18 +276,21 @@ __device__ __forceinline__ const int32_t* stage_node(const int32_t* __restrict__
 __global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, int n, int64_t count,
     int* __restrict__ kid_count, int* __restrict__ early_count, int* __restrict__ kid_mask,
-    int* __restrict__ err, int stage_words) {
+    int* __restrict__ err, int stage_words, Plan* __restrict__ plans) {
   const int lane = threadIdx.x & 31;
   const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= count) return;
   const int32_t* a = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
   const int64_t cf = coef ? coef[node] : 1;
-  Plan pl = plan_node(a, n, cf, lane);
+  __shared__ int s_cnt[kExpThreads / 32][2 * SPERM_EXPAND_NMAX];  // row and column counts per warp
+  int* rowcnt = s_cnt[threadIdx.x >> 5];
+  int* colcnt = rowcnt + SPERM_EXPAND_NMAX;
+  Plan pl = plan_node(a, n, cf, lane, rowcnt, colcnt);
   int kids = 0, mask = 0;
   bool ovf = false;
   for (int c = 0; c < pl.nkids; ++c) {
     if (!pl.kid[c].valid) ovf = true;
-    if (build_child<false>(a, n, pl.kid[c], nullptr, lane, &ovf)) {
+    if (survives(a, n, pl.kid[c], rowcnt, colcnt, lane, &ovf)) {
       ++kids;
       mask |= 1 << c;
     }
@@ -238,6 +298,7 @@ __global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
   if (lane == 0) {
     kid_count[node] = kids;
     kid_mask[node] = mask;
+    plans[node] = pl;  // the emit pass reuses the pivot and children (no second scan)
     early_count[node] = pl.early;
     if (ovf) atomicOr(err, 1);
   }
@@ -249,14 +310,14 @@ __global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
     const int64_t* __restrict__ early_off,
     int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef, int32_t* __restrict__ out_job,
     int32_t* __restrict__ early_mats, int64_t* __restrict__ early_coef, int32_t* __restrict__ early_job,
-    int stage_words) {
+    int stage_words, const Plan* __restrict__ plans) {
   const int lane = threadIdx.x & 31;
   const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= count) return;
   const int32_t* a = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
   const int64_t cf = coef ? coef[node] : 1;
   const int32_t jb = job ? job[node] : (int32_t)node;
-  Plan pl = plan_node(a, n, cf, lane);
+  const Plan pl = plans[node];
   if (pl.early) {
     const int64_t o = early_off[node];
     int32_t* dst = early_mats + o * (int64_t)n * n;
@@ -313,6 +374,8 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   int64_t* off = nullptr;
   SPERM_CUDA(cudaMallocAsync((void**)&off, sizeof(int64_t) * (2 * count + 2), st));
   int64_t* eoff = off + count + 1;
+  Plan* plans = nullptr;  // per-node pivot and children, count pass -> emit pass
+  SPERM_CUDA(cudaMallocAsync((void**)&plans, sizeof(Plan) * count, st));
   SPERM_CUDA(cudaMemsetAsync(err, 0, sizeof(int) * 4, st));
   // shared-memory staging of each warp's node: up to 8 warps per CTA within 200 KB
   const int stage_words = ((n * n + 3) / 4) * 4;
@@ -326,12 +389,18 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   auto cleanup = [&]() {
     cudaFreeAsync(kc, st);
     cudaFreeAsync(off, st);
+    cudaFreeAsync(plans, st);
   };
   {
     TimingScope ts("expand", st);
     count_launch();
-    expand_count_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err,
-                                                          stage_words);
+    static const bool count_stage = [] {  // A-B knob SPERM_EXPAND_COUNT_STAGE=0/1 (default staged)
+      const char* e = getenv("SPERM_EXPAND_COUNT_STAGE");
+      return !(e && e[0] == '0');
+    }();
+    const unsigned cblocks = count_stage ? blocks : (unsigned)((count * 32 + kExpThreads - 1) / kExpThreads);
+    expand_count_kernel<<<cblocks, count_stage ? bthreads : kExpThreads, count_stage ? esmem : 0, st>>>(
+        d_in_mats, d_in_coef, n, count, kc, ec, km, err, count_stage ? stage_words : 0, plans);
   }
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) { cleanup(); return cuda_check(le, "expand_count_kernel"); }
@@ -368,9 +437,16 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   {
     TimingScope ts("expand", st);
     count_launch();
-    expand_emit_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
-                                                       d_out_mats, d_out_coef, d_out_job, d_early_mats,
-                                                       d_early_coef, d_early_job, stage_words);
+    // the emit pass reads each kept row once per child; staging it in shared memory (A-B knob
+    // SPERM_EXPAND_EMIT_STAGE=0/1) trades occupancy for L2 re-reads
+    static const bool emit_stage = [] {  // measured: unstaged 5.0 ms vs staged 6.1 ms per C100 level
+      const char* e = getenv("SPERM_EXPAND_EMIT_STAGE");
+      return e && e[0] == '1';
+    }();
+    const unsigned eblocks = emit_stage ? blocks : (unsigned)((count * 32 + kExpThreads - 1) / kExpThreads);
+    expand_emit_kernel<<<eblocks, emit_stage ? bthreads : kExpThreads, emit_stage ? esmem : 0, st>>>(
+        d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff, d_out_mats, d_out_coef, d_out_job, d_early_mats,
+        d_early_coef, d_early_job, emit_stage ? stage_words : 0, plans);
   }
   le = cudaGetLastError();
   cleanup();
