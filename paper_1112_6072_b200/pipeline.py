@@ -230,7 +230,9 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     # R-NW batches run on their own stream, so the expansion of the next chunk (on the current
     # stream, with its host round trips) overlaps the integer-bound R-NW of the previous one.
     main = torch.cuda.current_stream()
-    rnw_stream = torch.cuda.Stream()
+    import os
+    # SPERM_PIPELINE_OVERLAP=0: everything on one stream (clean per-stage device timings)
+    rnw_stream = main if os.environ.get("SPERM_PIPELINE_OVERLAP", "1") == "0" else torch.cuda.Stream()
     acc.record_stream(rnw_stream)
     if measure_jobs:
         job_cycles.record_stream(rnw_stream)
