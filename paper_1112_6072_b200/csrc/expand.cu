@@ -2,12 +2,12 @@
 // every node is split by Eq. (2) on its pivot line (Algorithm
 // H_per Step 1) into at most two children of order n-1.
 //
-// One warp per node; lane l holds columns l, l+32, ... of the row being processed, so
-// every global access of a row is coalesced.  Pass 1 (count) builds each child in
-// registers without storing it, to learn whether it survives (no zero line, reading
-// R4); an exclusive scan of the per-node child counts gives every child its output
-// slot in natural order (parents in order, A1 before A2 — stable, reading R6); pass 2
-// (emit) rebuilds and stores.  Both passes run the same device function.
+// One warp per node.  Pass 1 (count) stages the node in shared memory, picks the pivot
+// (lane l holds columns l, l+32, ... of the row being scanned) and tests from the line
+// counts whether each child survives (no zero line, reading R4); an exclusive scan of the
+// per-node child counts gives every child its output slot in natural order (parents in
+// order, A1 before A2 — stable, reading R6); pass 2 (emit) writes the surviving children
+// output-element parallel (write_child).
 //
 // A child is described by the lines it deletes and the merge it performs:
 //   row pivot r, merge of p_a,p_b:  delete row r, column p_b; column p_a := al*col(p_b) + be*col(p_a)
@@ -25,7 +25,6 @@ namespace sperm {
 namespace {
 
 constexpr int kExpThreads = 256;
-constexpr int kMaxChunks = SPERM_EXPAND_NMAX / 32;  // columns per lane
 
 struct Child {
   int del_row, del_col;
@@ -42,45 +41,40 @@ struct Plan {
   Child kid[2];
 };
 
-__device__ __forceinline__ int32_t ld(const int32_t* a, int n, int i, int j) { return a[i * n + j]; }
+// A staged node: shared-memory copy with row stride ns = n | 1 (odd), so that a warp reading
+// one column (lane = row) and a warp reading one row (lane = column) both hit 32 distinct banks.
+struct NodeView {
+  const int32_t* a;
+  int n, ns;
+  __device__ __forceinline__ int32_t at(int i, int j) const { return a[i * ns + j]; }
+};
 
-// Pivot selection and the Eq. (2) children of one node (warp-uniform result).
-__device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, int lane, int* rowcnt_out = nullptr,
-                          int* colcnt_out = nullptr) {
-  int colcnt[kMaxChunks];
-#pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) colcnt[c] = 0;
-  const int nch = (n + 31) >> 5;
+__host__ __device__ __forceinline__ int stage_stride(int n) { return n | 1; }
+
+// Pivot selection and the Eq. (2) children of one node (warp-uniform result).  Line counts by
+// lane-per-line scans (lane l counts row l and column l; lanes loop for n > 32), written to
+// rowcnt/colcnt for the survival test.
+__device__ Plan plan_node(const NodeView& A, int64_t coef, int lane, int* rowcnt, int* colcnt) {
+  const int n = A.n;
   int best_row_key = 0x7fffffff;  // (count << 8) | index, min = fewest nonzeros, lowest index
-  for (int i = 0; i < n; ++i) {
-    int rc = 0;
-#pragma unroll
-    for (int c = 0; c < kMaxChunks; ++c) {
-      if (c < nch) {
-        const int j = c * 32 + lane;
-        const bool nz = j < n && ld(a, n, i, j) != 0;
-        colcnt[c] += nz;
-        rc += __popc(__ballot_sync(0xffffffffu, nz));
-      }
-    }
-    best_row_key = min(best_row_key, (rc << 8) | i);
-    if (rowcnt_out && lane == 0) rowcnt_out[i] = rc;
-  }
-  if (colcnt_out) {
-#pragma unroll
-    for (int c = 0; c < kMaxChunks; ++c) {
-      const int j = c * 32 + lane;
-      if (c < nch && j < n) colcnt_out[j] = colcnt[c];
-    }
-    __syncwarp();
-  }
   int best_col_key = 0x7fffffff;
-#pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) {
-    const int j = c * 32 + lane;
-    if (c < nch && j < n) best_col_key = min(best_col_key, (colcnt[c] << 8) | j);
+  for (int l = lane; l < n; l += 32) {
+    int rc = 0, cc = 0;
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+      rc += A.at(l, j) != 0;
+      cc += A.at(j, l) != 0;
+    }
+    rowcnt[l] = rc;
+    colcnt[l] = cc;
+    best_row_key = min(best_row_key, (rc << 8) | l);
+    best_col_key = min(best_col_key, (cc << 8) | l);
   }
-  for (int o = 16; o; o >>= 1) best_col_key = min(best_col_key, __shfl_xor_sync(0xffffffffu, best_col_key, o));
+  for (int o = 16; o; o >>= 1) {
+    best_row_key = min(best_row_key, __shfl_xor_sync(0xffffffffu, best_row_key, o));
+    best_col_key = min(best_col_key, __shfl_xor_sync(0xffffffffu, best_col_key, o));
+  }
+  __syncwarp();
   Plan pl;
   pl.nkids = 0;
   pl.early = 0;
@@ -97,17 +91,17 @@ __device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, in
   int pos[4];
   int32_t val[4];
   int cnt = 0;
-  for (int c = 0; c < nch; ++c) {
-    const int t = c * 32 + lane;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int t = c0 + lane;
     int32_t v = 0;
-    if (t < n) v = colpiv ? ld(a, n, t, idx) : ld(a, n, idx, t);
+    if (t < n) v = colpiv ? A.at(t, idx) : A.at(idx, t);
     unsigned b = __ballot_sync(0xffffffffu, v != 0);
     while (b) {
       const int l = __ffs(b) - 1;
       b &= b - 1;
       const int32_t vv = __shfl_sync(0xffffffffu, v, l);
       if (cnt < 4) {
-        pos[cnt] = c * 32 + l;
+        pos[cnt] = c0 + l;
         val[cnt] = vv;
       }
       ++cnt;
@@ -154,105 +148,46 @@ __device__ Plan plan_node(const int32_t* __restrict__ a, int n, int64_t coef, in
   return pl;
 }
 
-// Builds child `ch` of node `a` row by row; stores it to `out` if WRITE.  Returns
-// 1 if the child has no zero row or column (it survives), 0 otherwise; sets *ovf on
-// an int32 overflow of a merged entry.
-template <bool WRITE>
-__device__ int build_child(const int32_t* __restrict__ a, int n, const Child& ch, int32_t* __restrict__ out,
-                           int lane, bool* ovf) {
-  const int nch = (n + 31) >> 5;
-  const int m = n - 1;
-  bool colnz[kMaxChunks];
-#pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) colnz[c] = false;
-  bool all_rows = true;
-  bool over = false;
-  for (int i = 0; i < n; ++i) {
-    if (i == ch.del_row) continue;
-    const int ii = i - (i > ch.del_row);
-    bool rownz = false;
-#pragma unroll
-    for (int c = 0; c < kMaxChunks; ++c) {
-      if (c < nch) {
-        const int j = c * 32 + lane;
-        int32_t v = j < n ? ld(a, n, i, j) : 0;
-        if (ch.merge == 2 && i == ch.keep) {
-          const int32_t vr = j < n ? ld(a, n, ch.del_row, j) : 0;
-          const long long mv = (long long)ch.al * vr + (long long)ch.be * v;
-          if (mv > INT32_MAX || mv < INT32_MIN) over = true;
-          v = (int32_t)mv;
-        }
-        // column merge: the kept column takes al*a[i][del_col] + be*a[i][keep]
-        if (ch.merge == 1 && j == ch.keep) {
-          const int32_t vd = ld(a, n, i, ch.del_col);
-          const long long mv = (long long)ch.al * vd + (long long)ch.be * v;
-          if (mv > INT32_MAX || mv < INT32_MIN) over = true;
-          v = (int32_t)mv;
-        }
-        const bool keepcol = j < n && j != ch.del_col;
-        if (keepcol && v != 0) {
-          rownz = true;
-          colnz[c] = true;
-        }
-        if (WRITE && keepcol) {
-          const int jj = j - (j > ch.del_col);
-          out[ii * m + jj] = v;
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, rownz)) all_rows = false;
-  }
-  // every kept column must have a nonzero
-  bool cols_ok = true;
-#pragma unroll
-  for (int c = 0; c < kMaxChunks; ++c) {
-    const int j = c * 32 + lane;
-    if (c < nch && j < n && j != ch.del_col && !colnz[c]) cols_ok = false;
-  }
-  cols_ok = __all_sync(0xffffffffu, cols_ok);
-  if (__any_sync(0xffffffffu, over)) *ovf = true;
-  return (all_rows && cols_ok) ? 1 : 0;
-}
-
 // Survival test of a child (reading R4: no zero row or column) from the parent's line counts
 // and the few lines the child changes — O(n) per child instead of rebuilding it.  Row i of a
 // column-merge child is nonzero iff it keeps a nonzero outside the two merged columns or its
 // merged entry is nonzero; an unmerged column is nonzero iff it has a nonzero outside the
 // deleted row; the merged column iff some merged entry is nonzero (and symmetrically for a
 // row merge, which is a column pivot).  Also flags int32 overflow of merged entries.
-__device__ int survives(const int32_t* __restrict__ a, int n, const Child& ch, const int* __restrict__ rowcnt,
+__device__ int survives(const NodeView& A, const Child& ch, const int* __restrict__ rowcnt,
                         const int* __restrict__ colcnt, int lane, bool* ovf) {
+  const int n = A.n;
   bool ok = true, over = false, merged_nz = false;
   if (ch.merge == 0) {
     const int r = ch.del_row, p = ch.del_col;
     for (int i = lane; i < n; i += 32) {
-      if (i != r && rowcnt[i] - (ld(a, n, i, p) != 0) == 0) ok = false;
-      if (i != p && colcnt[i] - (ld(a, n, r, i) != 0) == 0) ok = false;
+      if (i != r && rowcnt[i] - (A.at(i, p) != 0) == 0) ok = false;
+      if (i != p && colcnt[i] - (A.at(r, i) != 0) == 0) ok = false;
     }
     merged_nz = true;
   } else if (ch.merge == 1) {  // row pivot r: column keep := al*col(del_col) + be*col(keep)
     const int r = ch.del_row, ka = ch.keep, kb = ch.del_col;
     for (int i = lane; i < n; i += 32) {
       if (i != r) {
-        const int32_t va = ld(a, n, i, ka), vb = ld(a, n, i, kb);
+        const int32_t va = A.at(i, ka), vb = A.at(i, kb);
         const long long mv = (long long)ch.al * vb + (long long)ch.be * va;
         if (mv > INT32_MAX || mv < INT32_MIN) over = true;
         if (mv != 0) merged_nz = true;
         else if (rowcnt[i] - (va != 0) - (vb != 0) == 0) ok = false;
       }
-      if (i != ka && i != kb && colcnt[i] - (ld(a, n, r, i) != 0) == 0) ok = false;
+      if (i != ka && i != kb && colcnt[i] - (A.at(r, i) != 0) == 0) ok = false;
     }
   } else {  // column pivot c: row keep := al*row(del_row) + be*row(keep)
     const int c = ch.del_col, ka = ch.keep, kb = ch.del_row;
     for (int j = lane; j < n; j += 32) {
       if (j != c) {
-        const int32_t va = ld(a, n, ka, j), vb = ld(a, n, kb, j);
+        const int32_t va = A.at(ka, j), vb = A.at(kb, j);
         const long long mv = (long long)ch.al * vb + (long long)ch.be * va;
         if (mv > INT32_MAX || mv < INT32_MIN) over = true;
         if (mv != 0) merged_nz = true;
         else if (colcnt[j] - (va != 0) - (vb != 0) == 0) ok = false;
       }
-      if (j != ka && j != kb && rowcnt[j] - (ld(a, n, j, c) != 0) == 0) ok = false;
+      if (j != ka && j != kb && rowcnt[j] - (A.at(j, c) != 0) == 0) ok = false;
     }
   }
   ok = __all_sync(0xffffffffu, ok) && __any_sync(0xffffffffu, merged_nz);
@@ -260,17 +195,77 @@ __device__ int survives(const int32_t* __restrict__ a, int n, const Child& ch, c
   return ok ? 1 : 0;
 }
 
-// Copies the warp's node into shared memory with coalesced loads (stage_words > 0), so the
-// row-by-row passes below read shared memory instead of issuing one short global load per row.
-__device__ __forceinline__ const int32_t* stage_node(const int32_t* __restrict__ g, int n, int stage_words,
-                                                     int lane) {
-  if (!stage_words) return g;
+// Words each lane moves per batch: all of a batch's loads are issued before its stores, so a
+// node's whole transfer is in flight at once (a node of order <= 22 is one batch) instead of
+// one dependent load round trip per row — the expansion levels are latency-bound otherwise.
+constexpr int kStageU = 16;
+
+// Copies the warp's node (dense, row-major in global memory) into its shared-memory slot with
+// row stride stage_stride(n); `stage_words` = the slot size in words.
+__device__ __forceinline__ NodeView stage_node(const int32_t* __restrict__ g, int n, int stage_words, int lane) {
   extern __shared__ int32_t esm[];
   int32_t* s = esm + (threadIdx.x >> 5) * stage_words;
-  const int nn = n * n;
-  for (int e = lane; e < nn; e += 32) s[e] = g[e];
+  const int nn = n * n, ns = stage_stride(n);
+  const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)n) + 1u;  // e / n for e * n < 2^32
+  for (int base = 0; base < nn; base += 32 * kStageU) {
+    int32_t r[kStageU];
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int e = base + u * 32 + lane;
+      r[u] = e < nn ? g[e] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int e = base + u * 32 + lane;
+      const int i = (int)__umulhi((uint32_t)e, magic);
+      if (e < nn) s[i * ns + (e - i * n)] = r[u];
+    }
+  }
   __syncwarp();
-  return s;
+  NodeView v;
+  v.a = s;
+  v.n = n;
+  v.ns = ns;
+  return v;
+}
+
+// Writes the n x n block of a staged node, or child `ch` of it (order m = n - 1), densely to
+// `out`, output-element parallel: lane l produces elements l, l+32, ... so every store is
+// coalesced and a lane's loads are independent.  Child element (ii, jj) is parent element
+// (ii + [ii >= del_row], jj + [jj >= del_col]), merged as in Eq. (2) (al * deleted line +
+// be * kept line).  The count pass has already rejected any level with an overflowing merged
+// entry, so the merge is computed modulo 2^32 (exact whenever the result fits, as it then does).
+template <bool CHILD>
+__device__ __forceinline__ void write_dense(const NodeView& A, const Child& ch, int32_t* __restrict__ out, int lane) {
+  const int m = CHILD ? A.n - 1 : A.n, mm = m * m;
+  const int dr = CHILD ? ch.del_row : 0x7fff, dc = CHILD ? ch.del_col : 0x7fff;
+  // floor(e / m) = umulhi(e, ceil(2^32 / m)) exactly for e * m < 2^32 (e < 2^14 here)
+  const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)m) + 1u;
+  for (int base = 0; base < mm; base += 32 * kStageU) {
+    int32_t r[kStageU];
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int e = base + u * 32 + lane;
+      int32_t v = 0;
+      if (e < mm) {
+        const int ii = (int)__umulhi((uint32_t)e, magic), jj = e - ii * m;
+        const int i = ii + (ii >= dr), j = jj + (jj >= dc);
+        v = A.at(i, j);
+        if (CHILD) {
+          if (ch.merge == 1 && j == ch.keep)
+            v = (int32_t)((uint32_t)ch.al * (uint32_t)A.at(i, ch.del_col) + (uint32_t)ch.be * (uint32_t)v);
+          else if (ch.merge == 2 && i == ch.keep)
+            v = (int32_t)((uint32_t)ch.al * (uint32_t)A.at(ch.del_row, j) + (uint32_t)ch.be * (uint32_t)v);
+        }
+      }
+      r[u] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int e = base + u * 32 + lane;
+      if (e < mm) out[e] = r[u];
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
@@ -280,17 +275,17 @@ __global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= count) return;
-  const int32_t* a = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
+  const NodeView A = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
   const int64_t cf = coef ? coef[node] : 1;
   __shared__ int s_cnt[kExpThreads / 32][2 * SPERM_EXPAND_NMAX];  // row and column counts per warp
   int* rowcnt = s_cnt[threadIdx.x >> 5];
   int* colcnt = rowcnt + SPERM_EXPAND_NMAX;
-  Plan pl = plan_node(a, n, cf, lane, rowcnt, colcnt);
+  Plan pl = plan_node(A, cf, lane, rowcnt, colcnt);
   int kids = 0, mask = 0;
   bool ovf = false;
   for (int c = 0; c < pl.nkids; ++c) {
     if (!pl.kid[c].valid) ovf = true;
-    if (survives(a, n, pl.kid[c], rowcnt, colcnt, lane, &ovf)) {
+    if (survives(A, pl.kid[c], rowcnt, colcnt, lane, &ovf)) {
       ++kids;
       mask |= 1 << c;
     }
@@ -314,14 +309,15 @@ __global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= count) return;
-  const int32_t* a = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
+  const int mask = kid_mask[node];
+  const Plan pl = plans[node];
+  if (!mask && !pl.early) return;  // no surviving child: nothing to read
+  const NodeView A = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
   const int64_t cf = coef ? coef[node] : 1;
   const int32_t jb = job ? job[node] : (int32_t)node;
-  const Plan pl = plans[node];
   if (pl.early) {
     const int64_t o = early_off[node];
-    int32_t* dst = early_mats + o * (int64_t)n * n;
-    for (int e = lane; e < n * n; e += 32) dst[e] = a[e];
+    write_dense<false>(A, pl.kid[0], early_mats + o * (int64_t)n * n, lane);
     if (lane == 0) {
       early_coef[o] = cf;
       early_job[o] = jb;
@@ -330,11 +326,9 @@ __global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
   }
   int64_t o = kid_off[node];
   const int64_t m2 = (int64_t)(n - 1) * (n - 1);
-  bool ovf = false;
-  const int mask = kid_mask[node];
   for (int c = 0; c < pl.nkids; ++c) {
     if ((mask >> c) & 1) {  // survivors found by the count pass
-      build_child<true>(a, n, pl.kid[c], out_mats + o * m2, lane, &ovf);
+      write_dense<true>(A, pl.kid[c], out_mats + o * m2, lane);
       if (lane == 0) {
         out_coef[o] = pl.kid[c].coef;
         out_job[o] = jb;
@@ -377,8 +371,8 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   Plan* plans = nullptr;  // per-node pivot and children, count pass -> emit pass
   SPERM_CUDA(cudaMallocAsync((void**)&plans, sizeof(Plan) * count, st));
   SPERM_CUDA(cudaMemsetAsync(err, 0, sizeof(int) * 4, st));
-  // shared-memory staging of each warp's node: up to 8 warps per CTA within 200 KB
-  const int stage_words = ((n * n + 3) / 4) * 4;
+  // shared-memory staging of each warp's node (row stride n | 1): up to 8 warps per CTA within 200 KB
+  const int stage_words = ((n * stage_stride(n) + 3) / 4) * 4;
   const int wpb = std::max(1, std::min(8, (int)((200 * 1024) / (stage_words * 4))));
   const size_t esmem = (size_t)wpb * stage_words * 4;
   SPERM_CUDA(cudaFuncSetAttribute(expand_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
@@ -394,13 +388,8 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   {
     TimingScope ts("expand", st);
     count_launch();
-    static const bool count_stage = [] {  // A-B knob SPERM_EXPAND_COUNT_STAGE=0/1 (default staged)
-      const char* e = getenv("SPERM_EXPAND_COUNT_STAGE");
-      return !(e && e[0] == '0');
-    }();
-    const unsigned cblocks = count_stage ? blocks : (unsigned)((count * 32 + kExpThreads - 1) / kExpThreads);
-    expand_count_kernel<<<cblocks, count_stage ? bthreads : kExpThreads, count_stage ? esmem : 0, st>>>(
-        d_in_mats, d_in_coef, n, count, kc, ec, km, err, count_stage ? stage_words : 0, plans);
+    expand_count_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err,
+                                                         stage_words, plans);
   }
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) { cleanup(); return cuda_check(le, "expand_count_kernel"); }
@@ -437,16 +426,11 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   {
     TimingScope ts("expand", st);
     count_launch();
-    // the emit pass reads each kept row once per child; staging it in shared memory (A-B knob
-    // SPERM_EXPAND_EMIT_STAGE=0/1) trades occupancy for L2 re-reads
-    static const bool emit_stage = [] {  // measured: unstaged 5.0 ms vs staged 6.1 ms per C100 level
-      const char* e = getenv("SPERM_EXPAND_EMIT_STAGE");
-      return e && e[0] == '1';
-    }();
-    const unsigned eblocks = emit_stage ? blocks : (unsigned)((count * 32 + kExpThreads - 1) / kExpThreads);
-    expand_emit_kernel<<<eblocks, emit_stage ? bthreads : kExpThreads, emit_stage ? esmem : 0, st>>>(
-        d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff, d_out_mats, d_out_coef, d_out_job, d_early_mats,
-        d_early_coef, d_early_job, emit_stage ? stage_words : 0, plans);
+    // the emit pass stages the parent too (read once, then once per child from shared memory;
+    // measured on the config-5 fullerene: 1.46 s staged vs 1.73 s reading global memory)
+    expand_emit_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
+                                                        d_out_mats, d_out_coef, d_out_job, d_early_mats, d_early_coef,
+                                                        d_early_job, stage_words, plans);
   }
   le = cudaGetLastError();
   cleanup();

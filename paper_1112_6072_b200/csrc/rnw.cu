@@ -125,10 +125,25 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   const int ns = n + 1;  // padded row stride: the row scans a[i*ns + j] hit distinct banks
   int32_t* sa = prep_sm + wib * (n * ns);
   {
+    // every load of a batch is issued before its stores (one batch covers n <= 22), so the
+    // leaf arrives in one memory round trip instead of n*n/32 dependent ones
+    constexpr int U = 16;
     const int32_t* g = mats + leaf * (int64_t)n * n;
-    for (int e = lane; e < n * n; e += 32) {
-      const int i = e / n;
-      sa[i * ns + (e - i * n)] = g[e];
+    const int nn = n * n;
+    const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)n) + 1u;  // e / n for e < 2^16
+    for (int base = 0; base < nn; base += 32 * U) {
+      int32_t r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * 32 + lane;
+        r[u] = e < nn ? g[e] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * 32 + lane;
+        const int i = (int)__umulhi((uint32_t)e, magic);
+        if (e < nn) sa[i * ns + (e - i * n)] = r[u];
+      }
     }
     __syncwarp();
   }
@@ -184,16 +199,20 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   }
   __syncwarp();
 
-  // ---- tree plan: greedy pick of up to 6 low columns with disjoint supports of <= 3 rows
-  int picks[kMaxLow] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  // ---- tree plan: greedy pick of up to kMaxLow low columns with disjoint supports of <= 3
+  // rows, lane l starting from column l mod n; picks packed one byte each (no local memory)
+  unsigned long long packed = 0;
   int np = 0;
   if (allow_tree && n >= 8 && !range_bad) {
     unsigned long long used = 0;
+    const int l0 = lane % n;
     for (int lvl = 1; lvl <= KS; ++lvl)
       for (int t = 0; t < n; ++t) {
-        const int j = (t + lane) % n;
+        int j = t + l0;
+        j -= j >= n ? n : 0;
         if (cnt[j] == lvl && !(supp[j] & used) && np < kMaxLow && np < n - 2) {
-          picks[np++] = j;
+          packed |= (unsigned long long)j << (8 * np);
+          ++np;
           used |= supp[j];
         }
       }
@@ -203,10 +222,25 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   for (int o = 16; o; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
   const int best = 31 - (key & 0xff);
   np = key >> 8;
-  for (int c = 0; c < kMaxLow; ++c) picks[c] = __shfl_sync(0xffffffffu, c < np ? picks[c] : -1, best);
+  packed = __shfl_sync(0xffffffffu, packed, best);
+  // lane c < np: support of low column c and the product of its slot rows' bounds
+  auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
+    // saturating product of non-negative bounds (no 64-bit division): saturate at 2^40 when the
+    // operands' bit lengths could reach 2^62; every threshold tested below is < 2^31
+    if (x == 0 || y == 0) return 0;
+    if ((64 - __clzll(x)) + (64 - __clzll(y)) > 62) return (int64_t)1 << 40;
+    const int64_t p = x * y;
+    return p > ((int64_t)1 << 40) ? ((int64_t)1 << 40) : p;
+  };
+  unsigned long long my_supp = 0;
+  int64_t my_q = 1;
+  if (lane < np) {
+    my_supp = supp[(packed >> (8 * lane)) & 0xff];
+    for (unsigned long long b = my_supp; b; b &= b - 1) my_q = sat_mul(my_q, R[__ffsll((long long)b) - 1]);
+  }
 
-  // ---- number of primes (lane 0) and the generic group size G (lane 31)
-  int k = min_primes, G = 1;
+  // ---- number of primes (lane 0)
+  int k = min_primes;
   if (lane == 0) {
     if (range_bad) atomicOr(err, 1);
     double lb = zero ? -1.0 : fmin(lr, lc);
@@ -222,52 +256,29 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       k = kcap;
     }
   }
-  if (lane == 31) {
-    // generic: largest group size G in {8,4,2,1} with every group product of row bounds < 2^30
-    for (int g = 8; g >= 2; g >>= 1) {
-      bool ok = true;
-      for (int s = 0; s < NPg && ok; s += g) {
-        int64_t prod = 1;
-        for (int r = s; r < s + g; ++r) {
-          const int64_t b = r < n ? R[r] : 1;
-          if (b == 0) { prod = 0; break; }
-          if (prod > ((1ll << 30) - 1) / b) { ok = false; break; }
-          prod *= b;
-        }
-        if (prod >= (1ll << 30)) ok = false;
-      }
-      if (ok) { G = g; break; }
-    }
-  }
   k = __shfl_sync(0xffffffffu, k, 0);
-  G = __shfl_sync(0xffffffffu, G, 31);
   // ---- tree plans: lane l tests plan l+1 (exact-arithmetic bounds); the first feasible wins
   const int pl = lane + 1;
   bool feasible = false;
   int fi = 0, pmexp = 0;
   unsigned long long slot_rows = 0;
-  if (pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0) {
+  {
+    const bool test = pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0;
     const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
-    if (np >= B && n - 6 >= B) {
-      // saturating product of non-negative bounds (no 64-bit division): saturate at 2^40 when the
-      // operands' bit lengths could reach 2^62; every threshold tested below is < 2^31
-      auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
-        if (x == 0 || y == 0) return 0;
-        if ((64 - __clzll(x)) + (64 - __clzll(y)) > 62) return (int64_t)1 << 40;
-        const int64_t p = x * y;
-        return p > ((int64_t)1 << 40) ? ((int64_t)1 << 40) : p;
-      };
-      const int ZL = B2 < 2 ? B2 : 2;  // exact Z_lo columns; the rest (<= 2) form Z_hi
-      int64_t X = 1, Zlo = 1, Zhi = 1;
-      for (int c = 0; c < B; ++c) {
-        int64_t q = 1;
-        for (int i = 0; i < n; ++i)
-          if ((supp[picks[c]] >> i) & 1ull) q = sat_mul(q, R[i]);
-        slot_rows |= supp[picks[c]];
+    const int ZL = B2 < 2 ? B2 : 2;  // exact Z_lo columns; the rest (<= 2) form Z_hi
+    int64_t X = 1, Zlo = 1, Zhi = 1;
+#pragma unroll
+    for (int c = 0; c < kMaxLow; ++c) {  // warp-uniform shuffles, per-lane plan bounds
+      const int64_t q = __shfl_sync(0xffffffffu, my_q, c);
+      const unsigned long long sc = __shfl_sync(0xffffffffu, my_supp, c);
+      if (c < B) {
+        slot_rows |= sc;
         if (c < B1) X = sat_mul(X, q);
         else if (c < B1 + ZL) Zlo = sat_mul(Zlo, q);
         else Zhi = sat_mul(Zhi, q);
       }
+    }
+    if (test && np >= B && n - 6 >= B) {
       // |X| * 2^B < p_min keeps a block's sum of 2^B products X_u*Y_v below p*2^31 (one REDC);
       // with one REDC per X_u (plan_ru) only the 2^B2 products of one accumulator count
       const int xbits = 31 - (plan_ru(pl) ? B2 : B);
@@ -292,38 +303,65 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     }
   }
   const unsigned fmask = __ballot_sync(0xffffffffu, feasible);
-  const int win = fmask ? __ffs(fmask) - 1 : -1;  // lowest plan index = preferred
-  if (win >= 0 && lane == win) {
-    const int B = plan_b1(pl) + plan_b2(pl), NF = nfix_of(fi);
-    // permutation record: rows [slot rows of low column c (ascending, -1 padded to KS)...,
-    // fixed rows ascending, -1 to NS + NF]; columns [low columns, high columns ascending, nw]
+  if (fmask) {
+    const int win = __ffs(fmask) - 1;  // lowest plan index = preferred
+    const int wpl = win + 1, B = plan_b1(wpl) + plan_b2(wpl);
+    const int wfi = __shfl_sync(0xffffffffu, fi, win);
+    const int NF = nfix_of(wfi);
+    slot_rows = __shfl_sync(0xffffffffu, slot_rows, win);
+    // permutation record, written by all lanes in parallel: rows [slot rows of low column c
+    // (ascending, -1 padded to KS)..., fixed rows ascending, -1 to NS + NF]; columns [low
+    // columns, high columns ascending, nw]
     int8_t* pr = perm + leaf * kPermW;
-    int r = 0;
-    for (int c = 0; c < B; ++c) {
-      int s = 0;
-      for (int i = 0; i < n; ++i)
-        if ((supp[picks[c]] >> i) & 1ull) { pr[r++] = (int8_t)i; ++s; }
-      for (; s < KS; ++s) pr[r++] = -1;
-    }
-    int f = 0;
-    for (int i = 0; i < n; ++i)
-      if (!((slot_rows >> i) & 1ull)) { pr[r++] = (int8_t)i; ++f; }
-    for (; f < NF; ++f) pr[r++] = -1;
-    // nw column: the non-low column with most nonzeros (highest index on ties)
-    unsigned long long low = 0;
-    for (int c = 0; c < B; ++c) low |= 1ull << picks[c];
-    int nw = -1;
-    for (int j = 0; j < n; ++j)
-      if (!((low >> j) & 1ull) && (nw < 0 || cnt[j] >= cnt[nw])) nw = j;
     int8_t* pc = pr + kPermRows;
-    int cc = 0;
-    for (int c = 0; c < B; ++c) pc[cc++] = (int8_t)picks[c];
-    for (int j = 0; j < n; ++j)
-      if (!((low >> j) & 1ull) && j != nw) pc[cc++] = (int8_t)j;
-    pc[cc++] = (int8_t)nw;
-    meta[leaf] = make_int2(k | (pl << 8) | (fi << 16) | (G << 24), pmexp);
+    const unsigned long long nmask = n == 64 ? ~0ull : ((1ull << n) - 1);
+    const unsigned long long fixed = ~slot_rows & nmask;
+    unsigned long long low = 0;
+    for (int c = 0; c < B; ++c) low |= 1ull << ((packed >> (8 * c)) & 0xff);
+    // nw column: the non-low column with most nonzeros (highest index on ties)
+    int nwkey = -1;
+    for (int j = lane; j < n; j += 32)
+      if (!((low >> j) & 1ull)) nwkey = max(nwkey, (cnt[j] << 8) | j);
+    for (int o = 16; o; o >>= 1) nwkey = max(nwkey, __shfl_xor_sync(0xffffffffu, nwkey, o));
+    const int nw = nwkey & 0xff;
+    const unsigned long long high = nmask & ~low & ~(1ull << nw);
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long below = (1ull << i) - 1;
+      if ((fixed >> i) & 1ull) {
+        pr[B * KS + __popcll(fixed & below)] = (int8_t)i;
+      } else {
+        for (int c = 0; c < B; ++c) {
+          const unsigned long long sc = supp[(packed >> (8 * c)) & 0xff];
+          if ((sc >> i) & 1ull) pr[c * KS + __popcll(sc & below)] = (int8_t)i;
+        }
+      }
+      if ((high >> i) & 1ull) pc[B + __popcll(high & below)] = (int8_t)i;
+    }
+    if (lane < B) {
+      const int j = (packed >> (8 * lane)) & 0xff;
+      pc[lane] = (int8_t)j;
+      for (int s = __popcll(supp[j]); s < KS; ++s) pr[lane * KS + s] = -1;
+    }
+    for (int f = n - __popcll(slot_rows) + lane; f < NF; f += 32) pr[B * KS + f] = -1;
+    if (lane == 0) pc[n - 1] = (int8_t)nw;
+    if (lane == win) meta[leaf] = make_int2(k | (wpl << 8) | (wfi << 16), pmexp);
+  } else if (lane == 0) {
+    // generic plan: largest group size G in {8,4,2,1} with every group product of row bounds
+    // < 2^30 (row bounds are < 2^30, so a product of two fits int64 before the test)
+    int G = 1;
+    for (int gs = 8; gs >= 2 && !range_bad; gs >>= 1) {
+      bool ok = true;
+      for (int s = 0; s < NPg && ok; s += gs) {
+        int64_t prod = 1;
+        for (int r = s; r < s + gs && ok; ++r) {
+          prod *= r < n ? R[r] : 1;
+          if (prod >= (1ll << 30)) ok = false;
+        }
+      }
+      if (ok) { G = gs; break; }
+    }
+    meta[leaf] = make_int2(k | (G << 24), NPg / G - 1);
   }
-  if (win < 0 && lane == 0) meta[leaf] = make_int2(k | (G << 24), NPg / G - 1);  // generic plan
 }
 
 // ============================================================================ generic kernel
@@ -728,42 +766,73 @@ __device__ __forceinline__ uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
   return r;
 }
 
-__global__ void rnw_finalize_kernel(int n, int64_t count, const int2* __restrict__ meta,
-                                    const unsigned long long* __restrict__ leaf_acc,
-                                    const int64_t* __restrict__ coef, const int32_t* __restrict__ job,
-                                    uint32_t* __restrict__ leaf_res, int32_t* __restrict__ leaf_k,
-                                    unsigned long long* __restrict__ job_acc, int64_t num_jobs) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= count * SPERM_KMAX) return;
-  const int64_t leaf = idx / SPERM_KMAX;
-  const int q = (int)(idx % SPERM_KMAX);
-  const int2 mt = meta[leaf];
-  const int k = meta_k(mt);
-  if (q == 0 && leaf_k) leaf_k[leaf] = k;
-  if (q >= k) {
-    if (leaf_res) leaf_res[idx] = 0u;
-    return;
+// Largest Montgomery exponent a plan can record in meta.y (generic: NP/G - 1 <= 47; tree:
+// NFIX/GF + 2 <= 22), so a finalize block tabulates the per-leaf scale factors once.
+constexpr int kMaxMexp = 48;
+constexpr int kFinThreads = 256;  // 32 leaves x 8 primes per block iteration
+
+// Leaf residues per = (-1)^(n-1) 2^(1-n) R^mexp S mod p_q (R = 2^32: the kernels' Montgomery
+// factors), times the leaf coefficient; accumulated into the job rows and the total row.  A
+// grid-stride kernel: each block builds the factor table f[q][mexp] once, then handles 32
+// leaves per iteration and adds each (job, q) run of equal jobs with one atomic.
+__global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
+    int n, int64_t count, const int2* __restrict__ meta, const unsigned long long* __restrict__ leaf_acc,
+    const int64_t* __restrict__ coef, const int32_t* __restrict__ job, uint32_t* __restrict__ leaf_res,
+    int32_t* __restrict__ leaf_k, unsigned long long* __restrict__ job_acc, int64_t num_jobs) {
+  __shared__ uint32_t s_f[SPERM_KMAX][kMaxMexp];
+  __shared__ unsigned long long s_val[kFinThreads];
+  __shared__ int32_t s_job[kFinThreads / SPERM_KMAX];
+  for (int t = threadIdx.x; t < SPERM_KMAX * kMaxMexp; t += blockDim.x) {
+    const int q = t / kMaxMexp, y = t % kMaxMexp;
+    const uint64_t pq = (uint64_t)c_p[q];
+    uint64_t f = 1;
+    if (n > 0) {
+      f = powmod((pq + 1) / 2, (uint64_t)(n - 1), pq);
+      f = f * powmod(((uint64_t)1 << 32) % pq, (uint64_t)y, pq) % pq;
+      if ((n - 1) & 1) f = (pq - f) % pq;
+    }
+    s_f[q][y] = (uint32_t)f;
   }
+  __syncthreads();
+  const int q = threadIdx.x % SPERM_KMAX, li = threadIdx.x / SPERM_KMAX;
   const uint64_t pq = (uint64_t)c_p[q];
-  uint64_t val;
-  if (n == 0) {
-    val = 1;
-  } else {
-    // per = (-1)^(n-1) 2^(1-n) R^mexp S  (R = 2^32: Montgomery factors of the kernel)
-    const uint64_t S = (uint64_t)(leaf_acc[leaf * SPERM_KMAX + q] % pq);
-    uint64_t f = powmod((pq + 1) / 2, (uint64_t)(n - 1), pq);
-    f = f * powmod(((uint64_t)1 << 32) % pq, (uint64_t)mt.y, pq) % pq;
-    if ((n - 1) & 1) f = (pq - f) % pq;
-    val = S * f % pq;
-  }
-  const int64_t cf = coef ? coef[leaf] : 1;
-  int64_t cm = cf % (int64_t)pq;
-  if (cm < 0) cm += (int64_t)pq;
-  val = val * (uint64_t)cm % pq;
-  if (leaf_res) leaf_res[idx] = (uint32_t)val;
-  if (job_acc) {
-    atomicAdd(job_acc + (job ? (int64_t)job[leaf] : 0) * SPERM_KMAX + q, (unsigned long long)val);
-    if (job) atomicAdd(job_acc + num_jobs * SPERM_KMAX + q, (unsigned long long)val);  // total row
+  for (int64_t base = (int64_t)blockIdx.x * kFinThreads; base < count * SPERM_KMAX;
+       base += (int64_t)gridDim.x * kFinThreads) {
+    const int64_t idx = base + threadIdx.x;
+    const int64_t leaf = idx / SPERM_KMAX;
+    uint64_t val = 0;
+    int32_t jb = -1;
+    if (leaf < count) {
+      const int2 mt = meta[leaf];
+      const int k = meta_k(mt);
+      if (q == 0 && leaf_k) leaf_k[leaf] = k;
+      jb = job ? job[leaf] : 0;
+      if (q < k) {
+        val = n == 0 ? 1 : (leaf_acc[leaf * SPERM_KMAX + q] % pq) * s_f[q][mt.y] % pq;
+        const int64_t cf = coef ? coef[leaf] : 1;
+        int64_t cm = cf % (int64_t)pq;
+        if (cm < 0) cm += (int64_t)pq;
+        val = val * (uint64_t)cm % pq;
+      }
+      if (leaf_res) leaf_res[idx] = (uint32_t)val;
+    }
+    if (job_acc) {
+      s_val[threadIdx.x] = val;
+      if (q == 0) s_job[li] = jb;
+      __syncthreads();
+      // thread (li, q) heads a run of leaves with equal jobs: sums the run, one atomic per run
+      if (jb >= 0 && (li == 0 || s_job[li - 1] != jb)) {
+        unsigned long long sum = 0;
+        for (int r = li; r < kFinThreads / SPERM_KMAX && s_job[r] == jb; ++r) sum += s_val[r * SPERM_KMAX + q];
+        if (sum) atomicAdd(job_acc + (int64_t)jb * SPERM_KMAX + q, sum);
+      }
+      if (job && li == 0) {  // the total row: one atomic per prime per block iteration
+        unsigned long long sum = 0;
+        for (int r = 0; r < kFinThreads / SPERM_KMAX; ++r) sum += s_val[r * SPERM_KMAX + q];
+        if (sum) atomicAdd(job_acc + num_jobs * SPERM_KMAX + q, sum);
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -779,15 +848,30 @@ __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order
                                 uint8_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist,
                                 int* __restrict__ hist_k) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  const int32_t leaf = order ? order[i] : (int32_t)i;
-  const int2 mt = meta[leaf];
-  const int plan = meta_plan(mt);
-  const int key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
-  keys[i] = (uint8_t)key;
-  ids[i] = leaf;
-  atomicAdd(hist + key, 1);
-  atomicAdd(hist_k + key, meta_k(mt));
+  int key = 0;
+  int2 mt = make_int2(0, 0);
+  if (i < count) {
+    const int32_t leaf = order ? order[i] : (int32_t)i;
+    mt = meta[leaf];
+    const int plan = meta_plan(mt);
+    key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
+    keys[i] = (uint8_t)key;
+    ids[i] = leaf;
+  }
+  // block histogram in shared memory, then one global atomic per nonzero bin
+  __shared__ int s_h[kNumKeys], s_hk[kNumKeys];
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) s_h[t] = s_hk[t] = 0;
+  __syncthreads();
+  if (i < count) {
+    atomicAdd(&s_h[key], 1);
+    atomicAdd(&s_hk[key], meta_k(mt));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x)
+    if (s_h[t]) {
+      atomicAdd(hist + t, s_h[t]);
+      atomicAdd(hist_k + t, s_hk[t]);
+    }
 }
 
 // ============================================================================ launch helpers
@@ -1193,7 +1277,8 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     TimingScope ts("rnw_finalize", st);
     const int64_t tot = count * SPERM_KMAX;
     count_launch();
-    rnw_finalize_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+    const int64_t fblocks = std::min<int64_t>((tot + kFinThreads - 1) / kFinThreads, (int64_t)sm_count() * 8);
+    rnw_finalize_kernel<<<(unsigned)fblocks, kFinThreads, 0, st>>>(
         n, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k, (unsigned long long*)d_job_acc, num_jobs);
   }
   cudaError_t le = cudaGetLastError();
