@@ -128,11 +128,25 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
     return _cat([level] + early)
 
 
-def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30, stats=None):
+def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None):
     """The same H_per recursion as expand_to_leaves, streamed: a level whose children could
     exceed `budget_bytes` of HBM is split into chunks that are expanded to their leaves one
     after another (depth first over chunks), so the live node sets stay bounded however many
     leaves a job has.  Yields NodeSets of leaves (order <= L) and of s >= 5 nodes."""
+    # A level is expanded whole (breadth first: the largest, best-utilised launches) while its own
+    # expansion fits the budget.  A level that does not is split into chunks sized so that a
+    # chunk's whole subtree down to order L is projected to fit (growth per level = children /
+    # parents seen so far at that order, else the largest at any order, else 2; 25% margin), so a
+    # chunk normally reaches its leaves without nested splits, which would each keep their parent
+    # level alive: the live memory stays ~ the chunked level + one chunk's two current levels.
+    # Only the first chunk is cut at a time; the rest is re-split with the growth seen by then.
+    seen: Dict[int, List[int]] = {}  # order -> [parents expanded, children produced]
+
+    def g_at(m: int) -> float:
+        if m in seen:
+            return seen[m][1] / seen[m][0]
+        return max(c / p for p, c in seen.values()) if seen else 2.0
+
     stack = [jobs]
     while stack:
         level = stack.pop()
@@ -141,12 +155,23 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30, stats=None):
         if level.n <= L or level.n < 2:
             yield level
             continue
-        per_node = 2 * 4 * (level.n - 1) ** 2 + 4 * level.n ** 2
-        cap = max(1, budget_bytes // per_node)
+        # bytes per node of one level of order m: its parents (4 m^2 each) and sperm_expand's
+        # output slots (2 children of order m-1 and 1 early node of order m per parent)
+        per_level = lambda m: 8 * m * m + 8 * (m - 1) ** 2  # noqa: E731
+        cap = max(1, budget_bytes // per_level(level.n))
         if level.count > cap:
-            for c0 in reversed(range(0, level.count, cap)):
-                sl = slice(c0, min(level.count, c0 + cap))
-                stack.append(NodeSet(level.n, level.mats[sl], level.coef[sl], level.job[sl]))
+            peak, mult = 0.0, 1.0
+            for m in range(level.n, L, -1):
+                peak = max(peak, mult * per_level(m))
+                mult *= g_at(m)
+                if mult * 8 * L * L > budget_bytes:  # one node's subtree alone exceeds the budget
+                    break
+            cap = max(1, min(cap, int(budget_bytes // (1.25 * peak))))
+        if level.count > cap:
+            # the first chunk now; the rest is re-split when popped, with the growth its
+            # predecessor's subtree has shown by then
+            stack.append(NodeSet(level.n, level.mats[cap:], level.coef[cap:], level.job[cap:]))
+            stack.append(NodeSet(level.n, level.mats[:cap], level.coef[:cap], level.job[:cap]))
             continue
         if stats is not None:
             import time
@@ -155,6 +180,9 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 8 << 30, stats=None):
         if stats is not None:
             stats["expand_calls"] = stats.get("expand_calls", 0) + 1
             stats["expand_host_s"] = stats.get("expand_host_s", 0.0) + time.perf_counter() - t0
+        pc = seen.setdefault(level.n, [0, 0])
+        pc[0] += level.count
+        pc[1] += km.shape[0]
         if em.shape[0]:
             yield NodeSet(level.n, em, ec, ej)
         stack.append(NodeSet(level.n - 1, km, kc, kj))
@@ -194,7 +222,7 @@ def reconstruct(res, k: int):
 
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
-              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 8 << 30) -> PHResult:
+              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30) -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
 
     With a torch.distributed `group` of world size G, every rank replicates the
@@ -227,12 +255,14 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     import time
     stats = {"rnw_calls": 0, "rnw_host_s": 0.0, "leaf_sets": 0, "t_loop_s": 0.0}
     t_loop = time.perf_counter()
-    # R-NW batches run on their own stream, so the expansion of the next chunk (on the current
-    # stream, with its host round trips) overlaps the integer-bound R-NW of the previous one.
+    # Every stage runs on the caller's stream.  SPERM_PIPELINE_OVERLAP=1 puts the R-NW batches on
+    # a stream of their own instead, so that the next chunk's expansion could overlap them; the
+    # persistent R-NW grids fill every SM, though, and per(C100) at L = 15 measured 45.9 s with
+    # the second stream against 33.1 s without (the expansion kernels queue behind the R-NW CTAs
+    # while the host waits on their count read-back).
     main = torch.cuda.current_stream()
     import os
-    # SPERM_PIPELINE_OVERLAP=0: everything on one stream (clean per-stage device timings)
-    rnw_stream = main if os.environ.get("SPERM_PIPELINE_OVERLAP", "1") == "0" else torch.cuda.Stream()
+    rnw_stream = torch.cuda.Stream() if os.environ.get("SPERM_PIPELINE_OVERLAP", "0") == "1" else main
     acc.record_stream(rnw_stream)
     if measure_jobs:
         job_cycles.record_stream(rnw_stream)

@@ -24,7 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=159)
     ap.add_argument("--leaf", type=int, default=20)
-    ap.add_argument("--budget-gb", type=float, default=8.0, help="HBM budget of a streamed expansion level")
+    ap.add_argument("--budget-gb", type=float, default=16.0, help="HBM budget of a streamed expansion level")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c100.json"))
     args = ap.parse_args()
     import numpy as np

@@ -1,6 +1,6 @@
 """Whole-path run of one workload with per-stage device timings (the library's CUDA-event
-timers) and the expansion's algorithmic GB/s.  SPERM_PIPELINE_OVERLAP=0 puts every stage on
-one stream so the stage timings add up to the device time.
+timers) and the expansion's algorithmic GB/s.  The pipeline runs every stage on one stream
+(unless SPERM_PIPELINE_OVERLAP=1), so the stage timings add up to the device time.
 
     python tools/stage_run.py --workload fullerene96 --jobs 1000 --leaf 20
     python tools/stage_run.py --workload c100 --jobs 159 --leaf 16
@@ -52,7 +52,7 @@ def main():
                       "leaves": r.leaves, "stage_ms": st,
                       "expand_GBps": round(xb / (st["expand"] * 1e-3) / 1e9, 1) if st["expand"] else None,
                       "terms_per_s_rnw": terms / (st["rnw"] * 1e-3) if st["rnw"] else None,
-                      "overlap": os.environ.get("SPERM_PIPELINE_OVERLAP", "1")}), flush=True)
+                      "overlap": os.environ.get("SPERM_PIPELINE_OVERLAP", "0")}), flush=True)
 
 
 if __name__ == "__main__":
