@@ -6,8 +6,8 @@
 //           trial_key(seed, id, trial), i, j)  (counter-based SplitMix64; K1)
 //   Step 2: X = |det B|^2 by LU with partial pivoting (first maximal |b_ik|^2), every real
 //           operation a single IEEE round-to-nearest fp64 op in a fixed order with no
-//           contraction (__dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn; K2), so the
-//           value equals the reference evaluation bit for bit.
+//           contraction (__dmul_rn/__dadd_rn/__dsub_rn; quotients correctly rounded, see
+//           div_by; K2), so the value equals the reference evaluation bit for bit.
 // The estimate is the trial-order sum of X divided by N (K3).
 #include <algorithm>
 
@@ -30,6 +30,24 @@ __device__ __forceinline__ uint64_t trial_key(uint64_t seed, uint64_t job, uint6
 __device__ __forceinline__ int root_index(uint64_t key, uint64_t i, uint64_t j) {
   const uint64_t h = mix64(key ^ ((i << 32) | j));
   return (int)(((h >> 32) * 3ull) >> 32);
+}
+
+// RN(a / d) for the step's pivot magnitude d > 0, given y = RN(1/d) (one __drcp_rn per
+// elimination step instead of a full division per multiplier): q0 = RN(a y) is within one ulp
+// of a/d, r = a - q0 d is exact (FMA), and RN(q0 + r y) is the correctly rounded quotient
+// (Markstein's theorem), i.e. the same double as the reference's a / d.  The theorem needs no
+// over/underflow in the intermediates: d_ok (warp-uniform) and the |a| range select the plain
+// IEEE division otherwise.  A zero numerator returns a * y, which keeps the sign of a / d.
+__device__ __forceinline__ bool div_range_ok(double v) {
+  const double av = fabs(v);
+  return av >= 0x1p-900 && av <= 0x1p900;
+}
+__device__ __forceinline__ double div_by(double a, double d, double y, bool d_ok) {
+  if (!d_ok || (a != 0.0 && !div_range_ok(a))) return __ddiv_rn(a, d);
+  const double q0 = __dmul_rn(a, y);
+  if (a == 0.0) return q0;
+  const double r = __fma_rn(-q0, d, a);
+  return __fma_rn(r, y, q0);
 }
 
 __global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
@@ -87,10 +105,12 @@ __global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int6
       x = __dmul_rn(x, d);
       if (k + 1 == n) break;
       const double pr = re[k * n + k], pi = im[k * n + k];
+      const double y = __drcp_rn(d);
+      const bool d_ok = div_range_ok(d);
       for (int i = k + 1 + lane; i < n; i += 32) {
         const double xr = re[i * n + k], xi = im[i * n + k];
-        re[i * n + k] = __ddiv_rn(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d);
-        im[i * n + k] = __ddiv_rn(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d);
+        re[i * n + k] = div_by(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d, y, d_ok);
+        im[i * n + k] = div_by(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d, y, d_ok);
       }
       __syncwarp();
       const int w = n - k - 1;
@@ -188,8 +208,10 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
       if (active) {
         const double2 pk = prow[k];
         const double xr = re[k], xi = im[k];
-        const double lr = __ddiv_rn(__dadd_rn(__dmul_rn(xr, pk.x), __dmul_rn(xi, pk.y)), d);
-        const double li = __ddiv_rn(__dsub_rn(__dmul_rn(xi, pk.x), __dmul_rn(xr, pk.y)), d);
+        const double y = __drcp_rn(d);
+        const bool d_ok = div_range_ok(d);
+        const double lr = div_by(__dadd_rn(__dmul_rn(xr, pk.x), __dmul_rn(xi, pk.y)), d, y, d_ok);
+        const double li = div_by(__dsub_rn(__dmul_rn(xi, pk.x), __dmul_rn(xr, pk.y)), d, y, d_ok);
 #pragma unroll
         for (int j = 1; j < NC; ++j) {  // j > k (static trip count keeps re/im in registers)
           if (j <= k) continue;
@@ -207,10 +229,87 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
 // CTA-distributed register variant for 32 < n <= 8*CS, n <= 32*RL: one 256-thread CTA per
 // trial.  Thread (w, l) holds rows l + 32a (a < RL) and columns w + 8s (s < CS) of B in
 // registers.  Column k lives in warp k % 8, so the pivot search is one warp's REDUX; that warp
-// writes the pivot and the multipliers of every active row to shared memory (double-buffered:
-// one __syncthreads per elimination step), the pivot row's entries reach the other warps by
-// shuffles, and every thread updates its own entries.  Same arithmetic, same order and the
-// same first-maximum pivot rule (by position) as the reference, so values are bit-identical.
+// writes the pivot and the multipliers of every active row to shared memory (double-buffered),
+// the pivot row's entries reach the other warps by shuffles, and every thread updates its own
+// entries.  Look-ahead: during elimination step k the warp that owns column k+1 updates that
+// column first and then already chooses pivot k+1 and writes its multipliers, while the other
+// warps are still applying step k — one __syncthreads per step and the pivot search off the
+// critical path.  Same arithmetic on every entry, in the same order, and the same
+// first-maximum pivot rule (by position) as the reference, so values are bit-identical.
+template <int RL>
+__device__ __forceinline__ void kk_pivot(int k, int buf, const double (&cr)[RL], const double (&ci)[RL],
+                                         const int (&pos)[RL], const bool (&act)[RL], int l, double2* lbuf,
+                                         double* pivd, int* pivi) {
+  // pivot over the active rows: my rows, then the warp (hi/lo bit pattern, position)
+  double bm = -1.0;
+  int bpos = 0x7fffffff, ba = 0;
+#pragma unroll
+  for (int ra = 0; ra < RL; ++ra) {
+    if (act[ra]) {
+      const double m = __dadd_rn(__dmul_rn(cr[ra], cr[ra]), __dmul_rn(ci[ra], ci[ra]));
+      if (m > bm || (m == bm && pos[ra] < bpos)) { bm = m; bpos = pos[ra]; ba = ra; }
+    }
+  }
+  const bool any = bpos != 0x7fffffff;
+  const unsigned mh = any ? (unsigned)__double2hiint(bm) : 0u, ml = any ? (unsigned)__double2loint(bm) : 0u;
+  const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
+  const bool c1 = any && mh == bh;
+  const unsigned blo = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
+  const bool c2 = c1 && ml == blo;
+  const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)bpos : 0xffffffffu);
+  const int pl = __ffs(__ballot_sync(0xffffffffu, c2 && bpos == bp)) - 1;
+  const double d = __hiloint2double((int)bh, (int)blo);
+  const int pa = __shfl_sync(0xffffffffu, ba, pl);
+  double pr = 0.0, pi = 0.0;
+#pragma unroll
+  for (int ra = 0; ra < RL; ++ra)
+    if (ra == pa) { pr = cr[ra]; pi = ci[ra]; }
+  pr = __shfl_sync(0xffffffffu, pr, pl);
+  pi = __shfl_sync(0xffffffffu, pi, pl);
+  const int p = pl + 32 * pa;
+  // multipliers of the rows that stay active (position > k after the exchange)
+  if (d != 0.0) {
+    const double y = __drcp_rn(d);
+    const bool d_ok = div_range_ok(d);
+#pragma unroll
+    for (int ra = 0; ra < RL; ++ra) {
+      const int row = l + 32 * ra;
+      int np = pos[ra];
+      if (row == p) np = k;
+      else if (act[ra] && np == k) np = bp;
+      if (act[ra] && np > k) {
+        const double xr = cr[ra], xi = ci[ra];
+        lbuf[buf * 32 * RL + row] = make_double2(div_by(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d, y, d_ok),
+                                                 div_by(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d, y, d_ok));
+      }
+    }
+  }
+  if (l == 0) {
+    pivd[buf] = d;
+    pivi[2 * buf] = p;
+    pivi[2 * buf + 1] = bp;
+  }
+}
+
+// b_ij -= l_i * u_j on one column (my RL rows): u = the pivot row's entry, from lane `plane`
+template <int RL>
+__device__ __forceinline__ void kk_update(double (&cr)[RL], double (&ci)[RL], const double2 (&lm)[RL],
+                                          const bool (&act)[RL], int pa, int plane) {
+  double ur = 0.0, ui = 0.0;
+#pragma unroll
+  for (int ra = 0; ra < RL; ++ra)
+    if (ra == pa) { ur = cr[ra]; ui = ci[ra]; }
+  ur = __shfl_sync(0xffffffffu, ur, plane);
+  ui = __shfl_sync(0xffffffffu, ui, plane);
+#pragma unroll
+  for (int ra = 0; ra < RL; ++ra) {
+    if (act[ra]) {
+      cr[ra] = __dsub_rn(cr[ra], __dsub_rn(__dmul_rn(lm[ra].x, ur), __dmul_rn(lm[ra].y, ui)));
+      ci[ra] = __dsub_rn(ci[ra], __dadd_rn(__dmul_rn(lm[ra].x, ui), __dmul_rn(lm[ra].y, ur)));
+    }
+  }
+}
+
 template <int RL, int CS>
 __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
                                                            const int32_t* __restrict__ ids, int trials,
@@ -239,7 +338,7 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
       kfill[e] = make_double2(r, s);
     }
     __syncthreads();
-    double re[RL][CS], im[RL][CS];
+    double re[CS][RL], im[CS][RL];  // [column slot][row slot]
     int pos[RL];
     bool act[RL];
 #pragma unroll
@@ -252,10 +351,12 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
         const int col = w + 8 * s;
         double2 v = make_double2(0.0, 0.0);
         if (row < n && col < n) v = kfill[row * n + col];
-        re[ra][s] = v.x;
-        im[ra][s] = v.y;
+        re[s][ra] = v.x;
+        im[s][ra] = v.y;
       }
     }
+    if (w == 0) kk_pivot<RL>(0, 0, re[0], im[0], pos, act, l, lbuf, pivd, pivi);  // pivot of step 0
+    __syncthreads();
     double x = 1.0;
     bool done = false;
 #pragma unroll
@@ -264,57 +365,6 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
         const int k = 8 * sk + wk;
         if (done || k >= n) break;
         const int buf = k & 1;
-        if (w == wk) {
-          // pivot over the active rows: my rows, then the warp (hi/lo bit pattern, position)
-          double bm = -1.0;
-          int bpos = 0x7fffffff, ba = 0;
-#pragma unroll
-          for (int ra = 0; ra < RL; ++ra) {
-            if (act[ra]) {
-              const double m = __dadd_rn(__dmul_rn(re[ra][sk], re[ra][sk]), __dmul_rn(im[ra][sk], im[ra][sk]));
-              if (m > bm || (m == bm && pos[ra] < bpos)) { bm = m; bpos = pos[ra]; ba = ra; }
-            }
-          }
-          const bool any = bpos != 0x7fffffff;
-          const unsigned mh = any ? (unsigned)__double2hiint(bm) : 0u, ml = any ? (unsigned)__double2loint(bm) : 0u;
-          const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
-          const bool c1 = any && mh == bh;
-          const unsigned blo = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
-          const bool c2 = c1 && ml == blo;
-          const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)bpos : 0xffffffffu);
-          const int pl = __ffs(__ballot_sync(0xffffffffu, c2 && bpos == bp)) - 1;
-          const double d = __hiloint2double((int)bh, (int)blo);
-          const int pa = __shfl_sync(0xffffffffu, ba, pl);
-          double pr = 0.0, pi = 0.0;
-#pragma unroll
-          for (int ra = 0; ra < RL; ++ra)
-            if (ra == pa) { pr = re[ra][sk]; pi = im[ra][sk]; }
-          pr = __shfl_sync(0xffffffffu, pr, pl);
-          pi = __shfl_sync(0xffffffffu, pi, pl);
-          const int p = pl + 32 * pa;
-          // multipliers of the rows that stay active (position > k after the exchange)
-          if (d != 0.0) {
-#pragma unroll
-            for (int ra = 0; ra < RL; ++ra) {
-              const int row = l + 32 * ra;
-              int np = pos[ra];
-              if (row == p) np = k;
-              else if (act[ra] && np == k) np = bp;
-              if (act[ra] && np > k) {
-                const double xr = re[ra][sk], xi = im[ra][sk];
-                lbuf[buf * 32 * RL + row] =
-                    make_double2(__ddiv_rn(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d),
-                                 __ddiv_rn(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d));
-              }
-            }
-          }
-          if (l == 0) {
-            pivd[buf] = d;
-            pivi[2 * buf] = p;
-            pivi[2 * buf + 1] = bp;
-          }
-        }
-        __syncthreads();
         const double d = pivd[buf];
         const int p = pivi[2 * buf], bp = pivi[2 * buf + 1];
         if (d == 0.0) { x = 0.0; done = true; break; }
@@ -327,29 +377,29 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
           else if (act[ra] && pos[ra] == k) pos[ra] = bp;
           act[ra] = act[ra] && pos[ra] > k;
         }
-        // the pivot row's entries of my columns, from lane p % 32 of this warp
         const int pa = p >> 5, plane = p & 31;
         double2 lm[RL];
 #pragma unroll
         for (int ra = 0; ra < RL; ++ra)
           lm[ra] = act[ra] ? lbuf[buf * 32 * RL + l + 32 * ra] : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int s = 0; s < CS; ++s) {
-          if (w + 8 * s <= k) continue;  // warp-uniform: finished columns
-          double ur = 0.0, ui = 0.0;
-#pragma unroll
-          for (int ra = 0; ra < RL; ++ra)
-            if (ra == pa) { ur = re[ra][s]; ui = im[ra][s]; }
-          ur = __shfl_sync(0xffffffffu, ur, plane);
-          ui = __shfl_sync(0xffffffffu, ui, plane);
-#pragma unroll
-          for (int ra = 0; ra < RL; ++ra) {
-            if (act[ra]) {
-              re[ra][s] = __dsub_rn(re[ra][s], __dsub_rn(__dmul_rn(lm[ra].x, ur), __dmul_rn(lm[ra].y, ui)));
-              im[ra][s] = __dsub_rn(im[ra][s], __dadd_rn(__dmul_rn(lm[ra].x, ui), __dmul_rn(lm[ra].y, ur)));
-            }
+        // look-ahead: column k+1 first in its warp, then pivot k+1 (warp-uniform branches)
+        const int w1 = (wk + 1) & 7;
+        if (w == w1) {
+          if (wk < 7) {
+            kk_update<RL>(re[sk], im[sk], lm, act, pa, plane);
+            kk_pivot<RL>(k + 1, buf ^ 1, re[sk], im[sk], pos, act, l, lbuf, pivd, pivi);
+          } else if (sk + 1 < CS) {
+            kk_update<RL>(re[sk + 1], im[sk + 1], lm, act, pa, plane);
+            kk_pivot<RL>(k + 1, buf ^ 1, re[sk + 1], im[sk + 1], pos, act, l, lbuf, pivd, pivi);
           }
         }
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+          if (w + 8 * s <= k) continue;                          // finished columns
+          if (w == w1 && s == (wk < 7 ? sk : sk + 1)) continue;  // column k+1: done above
+          kk_update<RL>(re[s], im[s], lm, act, pa, plane);
+        }
+        __syncthreads();
       }
     }
     if (threadIdx.x == 0) xout[item] = x;

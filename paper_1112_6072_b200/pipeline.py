@@ -205,6 +205,20 @@ def rank_positions(machine, order, rank: int) -> np.ndarray:
     return pos
 
 
+def estimate_owner(job_ids, world: int):
+    """Rank that computes the KKLLL estimate of each job: job id mod world."""
+    return job_ids % world
+
+
+def gather_estimates(est_part, group=None):
+    """Every rank's estimates from per-rank partial vectors (0.0 at the jobs other ranks own):
+    one SUM all-reduce, exact since x + 0.0 = x for the nonnegative estimates."""
+    import torch.distributed as dist
+    if group is not None and dist.get_world_size(group) > 1:
+        dist.all_reduce(est_part, op=dist.ReduceOp.SUM, group=group)
+    return est_part
+
+
 def allreduce_accumulators(acc, group=None):
     """Algorithm PH Step 4 across GPUs: one SUM all-reduce of the
     [jobs + 1][8] residue accumulators (NCCL on GPUs).  Each rank added residues < 2^31
@@ -238,14 +252,23 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     root = root_nodeset(a, device)
     jobsets = pre_expand(root, jobs_at_least, job_order)
     num_jobs = sum(s.count for s in jobsets)
-    # improved Step 3: KKLLL weights of every job (replicated, deterministic)
-    est = np.zeros(num_jobs)
+    # improved Step 3: KKLLL weights.  Each rank estimates the jobs it owns (job id mod world);
+    # one all-reduce gives every rank every estimate, bit-identical to a replicated run (a job's
+    # trials depend only on (seed, job id, trial)).
+    est_dev = torch.zeros(num_jobs, dtype=torch.float64, device=device)
     for s in jobsets:
+        ids = s.job
+        mats = s.mats
+        if world > 1:
+            idx = torch.nonzero(estimate_owner(ids, world) == rank).flatten()
+            ids, mats = ids.index_select(0, idx), mats.index_select(0, idx)
+        if ids.shape[0] == 0:
+            continue
         if s.n <= 112:
-            e = S.sperm_estimate(s.mats, trials=trials, seed=seed, ids=s.job).cpu().numpy()
+            est_dev[ids.long()] = S.sperm_estimate(mats, trials=trials, seed=seed, ids=ids)
         else:
-            e = np.full(s.count, np.inf)
-        est[s.job.cpu().numpy()] = e
+            est_dev[ids.long()] = float("inf")
+    est = gather_estimates(est_dev, group).cpu().numpy()
     machine, order, _ = S.sperm_schedule(est, world, policy, seed=seed)
     acc = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
     job_cycles = torch.zeros(num_jobs, dtype=torch.int64, device=device) if measure_jobs else None

@@ -1,7 +1,8 @@
 """Multi-rank host logic of the hot path on CPU (-m "not gpu"): world_size 2 over gloo.
 
-Each rank replicates the LPT schedule (host C++, sperm_schedule), takes the jobs dealt to
-it (pipeline.rank_positions), adds its jobs' residues to the [jobs + 1][8] accumulators,
+Each rank estimates the jobs it owns (pipeline.estimate_owner) and one all-reduce gives all
+ranks every estimate (pipeline.gather_estimates); each rank replicates the LPT schedule (host
+C++, sperm_schedule), takes the jobs dealt to it (pipeline.rank_positions), adds its jobs' residues to the [jobs + 1][8] accumulators,
 and one all-reduce (pipeline.allreduce_accumulators — NCCL on GPUs, gloo here) forms
 Algorithm PH Step 4; host CRT (pipeline.reconstruct) must give the exact total and every
 job value.  The per-job values come from the oracle (test infrastructure) in place of the
@@ -39,8 +40,16 @@ def _worker(rank, world, port, policy, q):
         jobs = pre_expand(a, jobs_at_least=30)
         J = len(jobs)
         vals = [node_permanent(j) for j in jobs]
-        est = [kklll_estimate((np.array(to_dense(m, k)) != 0).astype(int), 16, 7, i)
-               for i, (c, m, k) in enumerate(jobs)]
+        est_all = [kklll_estimate((np.array(to_dense(m, k)) != 0).astype(int), 16, 7, i)
+                   for i, (c, m, k) in enumerate(jobs)]
+        # sharded estimation: this rank fills only the jobs it owns, one all-reduce combines
+        owner = pipeline.estimate_owner(torch.arange(J), world)
+        part = torch.zeros(J, dtype=torch.float64)
+        for i in range(J):
+            if int(owner[i]) == rank:
+                part[i] = est_all[i]
+        est = pipeline.gather_estimates(part, dist.group.WORLD).numpy()
+        est_ok = est.tolist() == est_all  # bit-identical to the replicated estimates
         machine, order, _ = P.sperm_schedule(est, world, policy, seed=5)
         pos = pipeline.rank_positions(machine, order, rank)
         k = P.sperm_bound_primes(a)
@@ -61,7 +70,7 @@ def _worker(rank, world, port, policy, q):
         sched = torch.tensor(np.asarray(machine, dtype=np.int64))
         gathered = [torch.zeros_like(sched) for _ in range(world)]
         dist.all_gather(gathered, sched)
-        q.put((rank, total, job_values == vals, bool((owned == 1).all()),
+        q.put((rank, total, job_values == vals and est_ok, bool((owned == 1).all()),
                all(torch.equal(g, gathered[0]) for g in gathered)))
     finally:
         dist.destroy_process_group()
