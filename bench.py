@@ -261,7 +261,7 @@ def bench_expand(P, torch, jobs_at_least: int = 200000, reps: int = 3):
             "peak_note": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy)"}
 
 
-def bench_c100(P, torch, leaf_order: int = 16, jobs_at_least: int = 159):
+def bench_c100(P, torch, leaf_order: int = 15, jobs_at_least: int = 159):
     """per(C100) — the paper's own case study (§4.1): the appendix graph by the whole
     path, checked against Table T12's printed Total (tests/golden/paper_pins.txt).
     The paper: 118413.21 s on one Pentium III (Table 5), 3796.85 s on 32 (Table 6)."""
@@ -279,13 +279,13 @@ def bench_c100(P, torch, leaf_order: int = 16, jobs_at_least: int = 159):
     r = pipeline.permanent(paper_graph("C100"), jobs_at_least=jobs_at_least, leaf_order=leaf_order)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw")}
+    stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
     terms = P.sperm_rnw_stats(reset=True)[0]
     P.sperm_timing_enable(False)
     return {"workload": f"per(C100), PAPER.md appendix graph; J>={jobs_at_least}, leaves of order <= {leaf_order}",
             "per": str(r.value), "paper_table_T12_total": str(pin), "matches_paper": r.value == pin,
             "wall_s": wall, "jobs": r.num_jobs, "leaves": r.leaves, "terms": terms,
-            "stage_ms_overlapping": stages, "paper_T1_s": 118413.21, "paper_T32_s": 3796.85}
+            "stage_ms": stages, "stage_note": "device time per stage (library CUDA-event timers, one stream)", "paper_T1_s": 118413.21, "paper_T32_s": 3796.85}
 
 
 def bench_ph(P, torch, leaf_order: int = 32, jobs_at_least: int = 992):
