@@ -19,18 +19,17 @@
 //    flipped column densely (4 rows per 128-bit broadcast load); the n-fold product is formed
 //    as NP/G exact int32 group products chained by signed Montgomery products mod each prime.
 //
-//  * tree (plans 1-5): rows and columns are renumbered (per(A) is invariant) so that the B
+//  * tree (plans 1-12): rows and columns are renumbered (per(A) is invariant) so that the B
 //    lowest Gray bits belong to columns with pairwise disjoint supports of <= 3 rows ("slot"
 //    rows).  The 2^B terms of an aligned block share every row sum except the slot rows of
-//    their low columns, and a slot row of low column c takes one of two values (bit c clear
-//    or set).  Each term's product is therefore
-//        prod_i w_i = X_u * Y_v,  X_u = prod_{c<B1} Q_c^{u_c} (exact int32),
-//                                 Y_v = P_F * prod_{c>=B1} Q_c^{v_c}  (mod p),
-//    with Q_c^0/Q_c^1 the products of column c's slot rows and P_F the product of the other
-//    ("fixed") rows.  The kernel forms X_u * Y_v for every one of the 2^B terms with one
-//    32x32->64 multiply-add (IMAD.WIDE) per term and prime, and reduces once per 2^B1 terms.
-//    The signs (-1)^{|u|+|v|} are folded into X and Y by negating Q_c^1.  Only the per-block
-//    row-sum update (a high Gray bit flip) touches all rows.
+//    their low columns, and a slot row of low column c depends on bit c alone (clear or set).
+//    With the sign (-1)^{|g(t)|} = (-1)^{|g_high|} (-1)^{|u|}, the block's sum factorises:
+//        sum_u (-1)^{|u|} prod_i w_i = (-1)^{|g_high|} P_F prod_{c<B} (Q_c^0 - Q_c^1),
+//    with Q_c^0 / Q_c^1 the products of column c's slot rows (bit clear / set) and P_F the
+//    product of the other ("fixed") rows — distributivity, since each slot row belongs to one
+//    low column.  A block of 2^B Gray-code terms therefore costs one row-sum update (the high
+//    Gray bit flip, touching all rows), B exact slot products and ~B/2 + NFIX/GF Montgomery
+//    products per prime, instead of 2^B n-fold products.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -51,29 +50,23 @@ constexpr int KS = 3;             // slot rows per low column (tree plans)
 constexpr int kNumNFix = 7;
 constexpr int kPermRows = 64;     // per-leaf permutation record: 64 row bytes + 64 column bytes
 constexpr int kPermW = 128;
-constexpr int kNumKeys = 80;      // plan * 8 + nfix index
+constexpr int kPermGend = kPermW - 1;  // byte 127 (column bytes >= 48 are unused): E-group ends
+constexpr int kNumKeys = 104;     // plan * 8 + nfix index
 
 __host__ __device__ constexpr int nfix_of(int i) {
   return i == 0 ? 4 : i == 1 ? 8 : i == 2 ? 12 : i == 3 ? 16 : i == 4 ? 24 : i == 5 ? 32 : 40;
 }
-// tree plans: (B1, B2, GF) — B1 low bits in the exact X tree, B2 in the modular Y tree,
-// GF fixed rows per exact group.  Plan 0 = generic kernel.
-// Plans in order of preference (larger blocks first); the first whose bounds hold is used.
-//   plan:  1  2  3  4  5  6  7  8  9
-//   B1:    4  4  4  3  2  3  2  2  1
-//   B2:    4  3  2  4  4  2  2  1  1
-//   RU:    0  0  0  0  1  0  0  0  0   (1 = one REDC per X_u accumulator instead of per block)
-// B2 > 2 splits the Y tree: Z_lo (2 columns, exact) and Z_hi (B2-2 columns, exact), joined by
-// Montgomery products W_h = P_F Z_hi,h, y = W_h Z_lo,v.
-__host__ __device__ constexpr int plan_b1(int p) {
-  return p == 1 || p == 2 || p == 3 ? 4 : p == 4 || p == 6 ? 3 : p == 5 || p == 7 || p == 8 ? 2 : p == 9 ? 1 : 0;
+// tree plans: (B, GF) — B low columns summed in closed form per block, GF fixed rows per exact
+// group.  Plan 0 = generic kernel.  Plans in order of preference (more low columns = fewer
+// blocks first); the first whose bounds hold is used.
+//   plan:  1  2  3  4  5  6  7  8 |  9 10 11 12
+//   B:     8  7  6  5  4  3  2  1 |  8  6  4  2
+//   GF:    4  4  4  4  4  4  4  4 |  2  2  2  2
+__host__ __device__ constexpr int plan_b(int p) {
+  return p >= 1 && p <= 8 ? 9 - p : p == 9 ? 8 : p == 10 ? 6 : p == 11 ? 4 : p == 12 ? 2 : 0;
 }
-__host__ __device__ constexpr int plan_b2(int p) {
-  return p == 1 || p == 4 || p == 5 ? 4 : p == 2 ? 3 : p == 3 || p == 6 || p == 7 ? 2 : p == 8 || p == 9 ? 1 : 0;
-}
-__host__ __device__ constexpr int plan_gf(int p) { return p >= 1 && p <= 7 ? 4 : 2; }
-__host__ __device__ constexpr int plan_ru(int p) { return p == 5 ? 1 : 0; }
-constexpr int kNumPlans = 10;
+__host__ __device__ constexpr int plan_gf(int p) { return p <= 8 ? 4 : 2; }
+constexpr int kNumPlans = 13;
 constexpr int kMaxLow = 8;  // low columns picked per leaf
 
 // the CRT primes (kPrimes, common.cuh) and p^-1 mod 2^32
@@ -88,12 +81,6 @@ __device__ __forceinline__ int32_t smont(int32_t a, int32_t b, int32_t p, int32_
   const int32_t m = (int32_t)t * pinv;
   return (int32_t)(t >> 32) - __mulhi(m, p);
 }
-// Signed Montgomery reduction T*2^-32 mod p for |T| < p*2^31; result in (-p, p).
-__device__ __forceinline__ int32_t redc(int64_t t, int32_t p, int32_t pinv) {
-  const int32_t m = (int32_t)t * pinv;
-  return (int32_t)(t >> 32) - __mulhi(m, p);
-}
-
 // per-leaf metadata: x = k | plan << 8 | nfix_idx << 16 | G << 24, y = Montgomery exponent
 __device__ __forceinline__ int meta_k(int2 m) { return m.x & 0xff; }
 __device__ __forceinline__ int meta_plan(int2 m) { return (m.x >> 8) & 0xff; }
@@ -261,28 +248,35 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   const int pl = lane + 1;
   bool feasible = false;
   int fi = 0, pmexp = 0;
+  unsigned gend = 0;  // bit c: an exact group of E_c ends at low column c
   unsigned long long slot_rows = 0;
   {
     const bool test = pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0;
-    const int B1 = plan_b1(pl), B2 = plan_b2(pl), B = B1 + B2, GF = plan_gf(pl);
-    const int ZL = B2 < 2 ? B2 : 2;  // exact Z_lo columns; the rest (<= 2) form Z_hi
-    int64_t X = 1, Zlo = 1, Zhi = 1;
+    const int B = plan_b(pl), GF = plan_gf(pl);
+    // every slot product |Q_c| <= q_c < 2^30 keeps E_c = Q_c^0 - Q_c^1 in int32; consecutive
+    // E_c are multiplied exactly while the product of their bounds 2 q_c stays < 2^31 (a group
+    // ends at bit c of gend), each group then costs one Montgomery product per prime
+    bool qok = true;
+    int64_t gp = 1;
 #pragma unroll
     for (int c = 0; c < kMaxLow; ++c) {  // warp-uniform shuffles, per-lane plan bounds
       const int64_t q = __shfl_sync(0xffffffffu, my_q, c);
       const unsigned long long sc = __shfl_sync(0xffffffffu, my_supp, c);
       if (c < B) {
         slot_rows |= sc;
-        if (c < B1) X = sat_mul(X, q);
-        else if (c < B1 + ZL) Zlo = sat_mul(Zlo, q);
-        else Zhi = sat_mul(Zhi, q);
+        if (q >= ((int64_t)1 << 30)) qok = false;
+        const int64_t e = 2 * q;
+        if (c > 0 && sat_mul(gp, e) >= ((int64_t)1 << 31)) {
+          gend |= 1u << (c - 1);
+          gp = e;
+        } else {
+          gp = c == 0 ? e : sat_mul(gp, e);
+        }
       }
     }
+    gend |= 1u << (B > 0 ? B - 1 : 0);
     if (test && np >= B && n - 6 >= B) {
-      // |X| * 2^B < p_min keeps a block's sum of 2^B products X_u*Y_v below p*2^31 (one REDC);
-      // with one REDC per X_u (plan_ru) only the 2^B2 products of one accumulator count
-      const int xbits = 31 - (plan_ru(pl) ? B2 : B);
-      bool ok = X < ((int64_t)1 << xbits) && Zlo < ((int64_t)1 << 30) && Zhi < ((int64_t)1 << 30);
+      bool ok = qok;
       const int nf = n - __popcll(slot_rows);
       while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
       if (fi == kNumNFix) ok = false;
@@ -298,14 +292,14 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       }
       if (g >= ((int64_t)1 << 30)) ok = false;
       feasible = ok;
-      // Montgomery factors: NGF-1 (P_F chain) + [B2 > 2] (W_h) + 1 (y) + 1 (REDC)
-      if (ok) pmexp = nfix_of(fi) / GF + 1 + (B2 > 2 ? 1 : 0);
+      // Montgomery factors per block value: NGF-1 (P_F chain) + one per exact E group
+      if (ok) pmexp = nfix_of(fi) / GF - 1 + __popc(gend);
     }
   }
   const unsigned fmask = __ballot_sync(0xffffffffu, feasible);
   if (fmask) {
     const int win = __ffs(fmask) - 1;  // lowest plan index = preferred
-    const int wpl = win + 1, B = plan_b1(wpl) + plan_b2(wpl);
+    const int wpl = win + 1, B = plan_b(wpl);
     const int wfi = __shfl_sync(0xffffffffu, fi, win);
     const int NF = nfix_of(wfi);
     slot_rows = __shfl_sync(0xffffffffu, slot_rows, win);
@@ -344,7 +338,10 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     }
     for (int f = n - __popcll(slot_rows) + lane; f < NF; f += 32) pr[B * KS + f] = -1;
     if (lane == 0) pc[n - 1] = (int8_t)nw;
-    if (lane == win) meta[leaf] = make_int2(k | (wpl << 8) | (wfi << 16), pmexp);
+    if (lane == win) {
+      pr[kPermGend] = (int8_t)gend;
+      meta[leaf] = make_int2(k | (wpl << 8) | (wfi << 16), pmexp);
+    }
   } else if (lane == 0) {
     // generic plan: largest group size G in {8,4,2,1} with every group product of row bounds
     // < 2^30 (row bounds are < 2^30, so a product of two fits int64 before the test)
@@ -538,9 +535,9 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_generic_kernel(
 
 // ============================================================================ tree kernel
 // shared memory per warp (words): colpos[nh][S4] | colneg[nh][S4] (bank-shifted) | w0[S4] |
-// delta[NS] | sacc int64[KMAX][32]
+// delta[NS]
 struct TreeSmem {
-  int S4, nh, pos, neg, w0, delta, sacc, words;
+  int S4, nh, pos, neg, w0, delta, words;
 };
 __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
   TreeSmem t;
@@ -550,8 +547,7 @@ __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
   t.neg = ((t.nh * t.S4 + 31) / 32) * 32 + 16;
   t.w0 = ((t.neg + t.nh * t.S4 + 3) / 4) * 4;
   t.delta = t.w0 + t.S4;
-  t.sacc = ((t.delta + NS + 1) / 2) * 2;
-  t.words = ((t.sacc + 2 * SPERM_KMAX * 32 + 3) / 4) * 4;
+  t.words = ((t.delta + NS + 3) / 4) * 4;
   return t;
 }
 
@@ -560,23 +556,19 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
     uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
-  constexpr int B1 = plan_b1(PLAN), B2 = plan_b2(PLAN), B = B1 + B2, GF = plan_gf(PLAN);
+  constexpr int B = plan_b(PLAN), GF = plan_gf(PLAN);
   constexpr int NS = B * KS;       // slot rows
   constexpr int NRT = NS + NFIX;   // row sums held in registers
   constexpr int S4 = (NRT + 3) / 4 * 4;
   constexpr int NGF = NFIX / GF;   // exact fixed-row groups
-  constexpr int NX = 1 << B1, NZ = 1 << B2;
-  constexpr int ZL = B2 < 2 ? B2 : 2, ZH = B2 - ZL;  // split Y tree (see the plan table)
-  constexpr int NZL = 1 << ZL, NZH = 1 << ZH;
-  constexpr bool RU = plan_ru(PLAN) != 0;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   const TreeSmem L = tree_smem(NRT, NS, n, B);
   int32_t* sm = reinterpret_cast<int32_t*>(smem4) + (threadIdx.x >> 5) * L.words;
-  long long* sacc = reinterpret_cast<long long*>(sm + L.sacc);
   int64_t cur_leaf = -1;
   int64_t prev_leaf = -1;
   long long t_item = 0;
+  unsigned gend = 0;
   while (true) {
     unsigned long long item = 0;
     if (lane == 0) item = atomicAdd(queue, 1ull);
@@ -618,10 +610,10 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
         const int row = pr[s];
         sm[L.delta + s] = row >= 0 ? 2 * a[row * n + pc[s / KS]] : 0;
       }
+      gend = (unsigned)(uint8_t)pr[kPermGend];
       __syncwarp();
       cur_leaf = leaf;
     }
-    for (int q = 0; q < k; ++q) sacc[q * 32 + lane] = 0;
     const uint64_t t0 = ((chunk << 5) + (uint64_t)lane) << m;
     // base row sums (low bits clear) of the lane's first block
     int32_t W[S4];
@@ -638,6 +630,9 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
     int32_t D[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) D[s] = sm[L.delta + s];
+    int64_t acc[SPERM_KMAX];
+#pragma unroll
+    for (int q = 0; q < SPERM_KMAX; ++q) acc[q] = 0;
     const uint64_t O0 = t0 >> B;
     const uint32_t nblk = 1u << (m - B);
     for (uint32_t ob = 0; ob < nblk; ++ob) {
@@ -651,8 +646,8 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
           W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
         }
       }
-      // slot products: Q0 (bit clear), Q1 = -(bit set)  (sign (-1)^{|u|+|v|} folded in)
-      int32_t Q0[B], Q1[B];
+      // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1), exact per group
+      int32_t E[B];
 #pragma unroll
       for (int c = 0; c < B; ++c) {
         int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
@@ -661,39 +656,8 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
           x0 *= W[c * KS + s];
           x1 *= W[c * KS + s] + D[c * KS + s];
         }
-        Q0[c] = x0;
-        Q1[c] = -x1;
-      }
-      // exact product trees: X over low columns [0, B1), Z_lo over [B1, B1+ZL), Z_hi over the rest
-      int32_t X[NX], Z[NZL], ZH_[NZH];
-      X[0] = Q0[0];
-      X[1] = Q1[0];
-#pragma unroll
-      for (int c = 1; c < B1; ++c)
-#pragma unroll
-        for (int s = 0; s < (1 << c); ++s) {
-          X[s + (1 << c)] = X[s] * Q1[c];
-          X[s] = X[s] * Q0[c];
-        }
-      Z[0] = Q0[B1];
-      Z[1] = Q1[B1];
-#pragma unroll
-      for (int c = 1; c < ZL; ++c)
-#pragma unroll
-        for (int s = 0; s < (1 << c); ++s) {
-          Z[s + (1 << c)] = Z[s] * Q1[B1 + c];
-          Z[s] = Z[s] * Q0[B1 + c];
-        }
-      if (ZH > 0) {
-        ZH_[0] = Q0[B1 + ZL];
-        ZH_[1] = Q1[B1 + ZL];
-#pragma unroll
-        for (int c = 1; c < ZH; ++c)
-#pragma unroll
-          for (int s = 0; s < (1 << c); ++s) {
-            ZH_[s + (1 << c)] = ZH_[s] * Q1[B1 + ZL + c];
-            ZH_[s] = ZH_[s] * Q0[B1 + ZL + c];
-          }
+        E[c] = x0 - x1;
+        if (c > 0 && !((gend >> (c - 1)) & 1u)) E[c] *= E[c - 1];  // joins the previous group
       }
       int32_t FG[NGF];
 #pragma unroll
@@ -704,51 +668,30 @@ __global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
         FG[g] = x;
       }
       const bool neg = (O0 + ob) & 1ull;  // (-1)^{|high Gray bits|}
-      for (int q = 0; q < k; ++q) {
-        const int32_t p = c_p[q], pinv = c_pinv[q];
-        int32_t pf = FG[0];
 #pragma unroll
-        for (int g = 1; g < NGF; ++g) pf = smont(pf, FG[g], p, pinv);
-        int32_t wh[NZH];
-        if (ZH > 0) {
+      for (int q = 0; q < SPERM_KMAX; ++q) {
+        if (q < k) {
+          const int32_t p = c_p[q], pinv = c_pinv[q];
+          int32_t v = FG[0];
 #pragma unroll
-          for (int h = 0; h < NZH; ++h) wh[h] = smont(pf, ZH_[h], p, pinv);
+          for (int g = 1; g < NGF; ++g) v = smont(v, FG[g], p, pinv);
+#pragma unroll
+          for (int c = 0; c < B; ++c)
+            if ((gend >> c) & 1u) v = smont(v, E[c], p, pinv);  // warp-uniform: per-leaf mask
+          acc[q] += neg ? -(int64_t)v : (int64_t)v;
         }
-        // one 32x32->64 multiply-add per term (X_u * Y_v, v = h 2^ZL + l); NX independent
-        // accumulator chains.  The prep bound on |X| keeps every REDC input below p * 2^31.
-        int64_t acc[NX];
-#pragma unroll
-        for (int v = 0; v < NZ; ++v) {
-          const int32_t y = smont(ZH > 0 ? wh[v >> ZL] : pf, Z[v & (NZL - 1)], p, pinv);
-#pragma unroll
-          for (int u = 0; u < NX; ++u) {
-            if (v == 0) acc[u] = (int64_t)X[u] * y;
-            else acc[u] += (int64_t)X[u] * y;
-          }
-        }
-        int64_t blk;
-        if (RU) {  // one REDC per accumulator
-          blk = 0;
-#pragma unroll
-          for (int u = 0; u < NX; ++u) blk += redc(acc[u], p, pinv);
-        } else {
-#pragma unroll
-          for (int s = NX / 2; s >= 1; s >>= 1)
-#pragma unroll
-            for (int u = 0; u < s; ++u) acc[u] += acc[u + s];
-          blk = redc(acc[0], p, pinv);
-        }
-        sacc[q * 32 + lane] += neg ? -blk : blk;
       }
     }
-    __syncwarp();
-    for (int q = 0; q < k; ++q) {
-      int64_t v = sacc[q * 32 + lane];
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) {
-        int64_t r = v % c_p[q];
-        if (r < 0) r += c_p[q];
-        atomicAdd(leaf_acc + leaf * SPERM_KMAX + q, (unsigned long long)r);
+#pragma unroll
+    for (int q = 0; q < SPERM_KMAX; ++q) {
+      if (q < k) {
+        int64_t v = acc[q];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+          int64_t r = v % c_p[q];
+          if (r < 0) r += c_p[q];
+          atomicAdd(leaf_acc + leaf * SPERM_KMAX + q, (unsigned long long)r);
+        }
       }
     }
   }
@@ -843,10 +786,11 @@ __global__ void reduce_mod_kernel(const unsigned long long* __restrict__ acc, in
   out[idx] = (uint32_t)(acc[idx] % (unsigned long long)c_p[idx % SPERM_KMAX]);
 }
 
-// evaluation-order leaf ids, their plan keys, and the per-key histogram
+// evaluation-order leaf ids, their plan keys, and per key: leaves, sum of k (primes) and sum
+// of k * mexp (Montgomery products per block value, summed over primes: the op model's input)
 __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order, const int2* __restrict__ meta,
                                 uint8_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist,
-                                int* __restrict__ hist_k) {
+                                int* __restrict__ hist_k, unsigned long long* __restrict__ hist_kx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int key = 0;
   int2 mt = make_int2(0, 0);
@@ -860,17 +804,23 @@ __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order
   }
   // block histogram in shared memory, then one global atomic per nonzero bin
   __shared__ int s_h[kNumKeys], s_hk[kNumKeys];
-  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) s_h[t] = s_hk[t] = 0;
+  __shared__ unsigned long long s_hx[kNumKeys];
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
+    s_h[t] = s_hk[t] = 0;
+    s_hx[t] = 0ull;
+  }
   __syncthreads();
   if (i < count) {
     atomicAdd(&s_h[key], 1);
     atomicAdd(&s_hk[key], meta_k(mt));
+    atomicAdd(&s_hx[key], (unsigned long long)(meta_k(mt) * mt.y));
   }
   __syncthreads();
   for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x)
     if (s_h[t]) {
       atomicAdd(hist + t, s_h[t]);
       atomicAdd(hist_k + t, s_hk[t]);
+      atomicAdd(hist_kx + t, s_hx[t]);
     }
 }
 
@@ -977,7 +927,7 @@ int launch_generic(const Launch& L) {
 
 template <int NFIX, int PLAN>
 int launch_tree(const Launch& L) {
-  constexpr int B = plan_b1(PLAN) + plan_b2(PLAN);
+  constexpr int B = plan_b(PLAN);
   constexpr int NS = B * KS, NRT = NS + NFIX;
   const int tb = L.n - 1;
   const int m = choose_m(L.n, L.nleaves, std::min(B + 2, L.n - 6));
@@ -1028,12 +978,15 @@ int launch_key(int key, int NPg, const Launch& L) {
     case 7: return launch_tree_nfix<7>(fi, L);
     case 8: return launch_tree_nfix<8>(fi, L);
     case 9: return launch_tree_nfix<9>(fi, L);
+    case 10: return launch_tree_nfix<10>(fi, L);
+    case 11: return launch_tree_nfix<11>(fi, L);
+    case 12: return launch_tree_nfix<12>(fi, L);
     default: return set_error(SPERM_ERR_ARG, "sperm_permanent: bad plan key");
   }
 }
 
 // First tree plan the prep pass may choose (0 = generic kernel only).  Testing / A-B
-// measurements only: SPERM_RNW_PLAN_MIN=<p> restricts the plans to p..9.
+// measurements only: SPERM_RNW_PLAN_MIN=<p> restricts the plans to p..12.
 int first_plan() {
   const char* e = getenv("SPERM_RNW_PLAN_MIN");
   if (!e || !e[0]) return 1;
@@ -1052,48 +1005,36 @@ struct RnwStats {
 std::mutex g_stats_mu;
 RnwStats g_stats;
 
-void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k) {
+void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k, double sum_kx) {
+  // sum_kx = sum over the key's leaves of k * mexp: Montgomery products per term (generic) or
+  // per block value (tree), summed over the primes
   const double T = std::ldexp(1.0, n - 1);
-  double fma_leaf = 0, alu_leaf = 0, fma_prime = 0, alu_prime = 0;  // per term
+  double fma_terms = 0, alu_terms = 0;  // totals over the key's leaves, per term-count unit
   if (key == 0) {
-    // generic: NP adds, NP-NP/G products, (NP/G-1) smont per prime (5 units: WIDE 2, IMAD, HI 2;
-    // + IADD on alu), accumulate 2 alu per prime; the group size is per leaf, modelled as G = 4
+    // generic, per term: NP adds, NP - NP/G products (G per leaf, modelled as 4) and per prime
+    // (NP/G - 1) smont (5 units: WIDE 2, IMAD, HI 2; + one IADD on the alu) and a 2-op accumulate
     const int NG = NPg / 4;
-    alu_leaf = NPg;
-    fma_leaf = NPg - NG;
-    fma_prime = (NG - 1) * 5.0;
-    alu_prime = (NG - 1) * 1.0 + 2.0;
+    fma_terms = T * ((NPg - NG) * (double)leaves + 5.0 * sum_kx);
+    alu_terms = T * (NPg * (double)leaves + sum_kx + 2.0 * sum_k);
   } else {
     const int plan = key / 8, fi = key % 8;
-    const int B1 = plan_b1(plan), B2 = plan_b2(plan), B = B1 + B2, GF = plan_gf(plan);
+    const int B = plan_b(plan), GF = plan_gf(plan);
     const int NS = B * KS, NFIX = nfix_of(fi), S4 = (NS + NFIX + 3) / 4 * 4, NGF = NFIX / GF;
-    const double blk = std::ldexp(1.0, B), NZ = std::ldexp(1.0, B2);
-    // shared per block: W update (S4 adds), Q products and slot adds, X/Z trees, fixed groups
-    const double f_sh = B * 2.0 * (KS - 1) + (std::ldexp(1.0, B1 + 1) - 4) + (std::ldexp(1.0, B2 + 1) - 4) +
-                        NGF * (GF - 1.0);
-    const double a_sh = S4 + B * (double)KS + 8;
-    // per prime per block: (NGF-1 + NZ + NZH) smont (NZH = 2^(B2-2) W_h products when B2 > 2),
-    // 2^B IMAD.WIDE (2 each), one REDC (or one per X_u, plan_ru) of 3 units;
-    // ALU: smont/REDC subtractions, 2^B1 - 1 64-bit adds (2 each), accumulate
-    const double NZH = B2 > 2 ? std::ldexp(1.0, B2 - 2) : 0.0, NX = std::ldexp(1.0, B1);
-    const double nred = plan_ru(plan) ? NX : 1.0;
-    double f_pr = (NGF - 1 + NZ + NZH) * 5.0 + nred * 3.0 + blk * 2.0;
-    const double add_pr = (NGF - 1 + NZ + NZH) * 1.0 + nred;  // 32-bit subtracts of smont / REDC
-    double a_pr = 2.0 * (NX - 1) + 6.0;                       // 64-bit adds, accumulate
+    const double blocks = std::ldexp(T, -B);  // per leaf
+    // per block, prime-independent: W update (S4 adds), slot products 2 (KS - 1) muls + KS adds
+    // + 1 subtract per low column, <= B - 1 group joins, NGF (GF - 1) fixed-row products, ~8 ops
+    // of loop / Gray bookkeeping; per prime: the block's smont chain (sum_kx) + 4-op accumulate
+    const double f_sh = B * 2.0 * (KS - 1) + (B - 1) + NGF * (GF - 1.0);
+    const double a_sh = S4 + B * (KS + 1.0) + 8;
     // ptxas issues about half of the 32-bit adds as IMAD.IADD on the multiply pipe (SASS mix of
-    // the tree kernels, profiles/r01_v5_rnw_tree_ncu.txt): split them evenly
-    const double f_sh2 = f_sh + 0.5 * a_sh, a_sh2 = 0.5 * a_sh;
-    f_pr += 0.5 * add_pr;
-    a_pr += 0.5 * add_pr;
-    fma_leaf = f_sh2 / blk;
-    alu_leaf = a_sh2 / blk;
-    fma_prime = f_pr / blk;
-    alu_prime = a_pr / blk;
+    // the tree kernels): split them evenly
+    fma_terms = blocks * ((f_sh + 0.5 * a_sh) * (double)leaves + 5.5 * sum_kx + 2.0 * sum_k);
+    alu_terms = blocks * (0.5 * a_sh * (double)leaves + 0.5 * sum_kx + 2.0 * sum_k);
   }
   std::lock_guard<std::mutex> lk(g_stats_mu);
   g_stats.terms += T * leaves;
-  g_stats.fma += T * (fma_leaf * leaves + fma_prime * sum_k);
-  g_stats.alu += T * (alu_leaf * leaves + alu_prime * sum_k);
+  g_stats.fma += fma_terms;
+  g_stats.alu += alu_terms;
 }
 
 }  // namespace
@@ -1161,7 +1102,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   int8_t* perm = nullptr;
   uint8_t* keys = nullptr;
   int32_t* ids = nullptr;
-  int* small = nullptr;  // [0..1] queue (u64), [2] err, [4..) hist, then hist_k
+  int* small = nullptr;  // [2] err, [4..) hist, hist_k, then u64 queue[keys], hist_kx[keys]
   void* sort_tmp = nullptr;
   auto cleanup = [&]() {
     cudaFreeAsync(meta, st);
@@ -1182,11 +1123,13 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   SPERM_TRY(cudaMallocAsync((void**)&perm, (size_t)kPermW * count, st));
   SPERM_TRY(cudaMallocAsync((void**)&keys, 2 * (size_t)count, st));
   SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
-  SPERM_TRY(cudaMallocAsync((void**)&small, sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * kNumKeys, st));
+  const size_t small_bytes = sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * 2 * kNumKeys;
+  SPERM_TRY(cudaMallocAsync((void**)&small, small_bytes, st));
   SPERM_TRY(cudaMemsetAsync(leaf_acc, 0, sizeof(unsigned long long) * count * SPERM_KMAX, st));
-  SPERM_TRY(cudaMemsetAsync(small, 0, sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * kNumKeys, st));
+  SPERM_TRY(cudaMemsetAsync(small, 0, small_bytes, st));
   // per-group work counters after the histograms (8-byte aligned: 4 + 2*48 ints = 400 bytes)
   unsigned long long* queue = reinterpret_cast<unsigned long long*>(small + 4 + 2 * kNumKeys);
+  unsigned long long* hist_kx = queue + kNumKeys;
   int* err = small + 2;
   int* hist = small + 4;
   {
@@ -1199,11 +1142,13 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
     count_launch();
-    rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist, hist + kNumKeys);
+    rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist, hist + kNumKeys, hist_kx);
     SPERM_TRY(cudaGetLastError());
   }
   int hsmall[4 + 2 * kNumKeys];
+  unsigned long long h_kx[kNumKeys];
   SPERM_TRY(cudaMemcpyAsync(hsmall, small, sizeof(hsmall), cudaMemcpyDeviceToHost, st));
+  SPERM_TRY(cudaMemcpyAsync(h_kx, hist_kx, sizeof(h_kx), cudaMemcpyDeviceToHost, st));
   SPERM_TRY(cudaStreamSynchronize(st));
   if (hsmall[2] & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
   if (hsmall[2] & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
@@ -1218,7 +1163,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   }
   if (n > 0) {
     for (int key = 0; key < kNumKeys; ++key)
-      if (h_hist[key]) record_stats(key, NPg, n, h_hist[key], hsmall[4 + kNumKeys + key]);
+      if (h_hist[key]) record_stats(key, NPg, n, h_hist[key], hsmall[4 + kNumKeys + key], (double)h_kx[key]);
   }
   int nonzero_keys = 0;
   for (int q = 0; q < kNumKeys; ++q) nonzero_keys += h_hist[q] > 0;

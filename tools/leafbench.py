@@ -46,8 +46,10 @@ def main():
     P.sperm_timing_reset()
     P.sperm_rnw_stats(reset=True)
     t0 = time.perf_counter()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off captures only this call
     P.sperm_permanent(m, coef=c, min_primes=3, max_primes=3)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     wall = time.perf_counter() - t0
     st = {s: P.sperm_timing_get(s)[0] for s in ("rnw_prep", "rnw", "rnw_finalize")}
     terms = P.sperm_rnw_stats(reset=True)[0]
