@@ -67,6 +67,12 @@ __host__ __device__ constexpr int plan_b(int p) {
 }
 __host__ __device__ constexpr int plan_gf(int p) { return p <= 8 ? 4 : 2; }
 constexpr int kNumPlans = 13;
+// resident 256-thread CTAs per SM a tree kernel is compiled for: 3 (<= 85 registers, 24 warps to
+// hide the fixed-latency multiply chains of short blocks) where ptxas fits it without spilling
+// (-Xptxas -v over all plans and NFIX), else 2
+__host__ __device__ constexpr int tree_min_blocks(int B, int nfix) {
+  return (B <= 5 && 3 * B + nfix <= 24) || (B <= 3 && nfix <= 24) || (B <= 2 && nfix <= 32) ? 3 : 2;
+}
 constexpr int kMaxLow = 8;  // low columns picked per leaf
 
 // the CRT primes (kPrimes, common.cuh) and p^-1 mod 2^32
@@ -552,7 +558,7 @@ __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
 }
 
 template <int NFIX, int PLAN>
-__global__ void __launch_bounds__(kRnwThreads, 2) rnw_tree_kernel(
+__global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFIX)) rnw_tree_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
     uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
