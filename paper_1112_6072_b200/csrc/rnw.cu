@@ -144,6 +144,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   __shared__ int64_t sR[8][SPERM_NMAX];
   __shared__ unsigned long long sSupp[8][SPERM_NMAX];
   __shared__ int sCnt[8][SPERM_NMAX];
+  __shared__ int sBl[8][SPERM_NMAX];  // bit length of each row bound: R_i < 2^bl_i
   int64_t* R = sR[wib];
   unsigned long long* supp = sSupp[wib];
   int* cnt = sCnt[wib];
@@ -162,6 +163,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (v != 0) { sm |= 1ull << j; ++nz; }
     }
     R[i] = r;
+    sBl[wib][i] = r ? 64 - __clzll(r) : 0;
     supp[i] = sm;  // support of column i (rows j with a_ji != 0)
     cnt[i] = nz;
     if (r == 0 || c == 0) zero = true;
@@ -199,16 +201,26 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   if (allow_tree && n >= 8 && !range_bad) {
     unsigned long long used = 0;
     const int l0 = lane % n;
-    for (int lvl = 1; lvl <= KS; ++lvl)
-      for (int t = 0; t < n; ++t) {
-        int j = t + l0;
+    const unsigned long long nmask = (1ull << n) - 1;  // n <= 48
+    for (int lvl = 1; lvl <= KS; ++lvl) {
+      // columns with exactly lvl nonzeros, visited in the lane's rotated order l0, l0+1, ...
+      unsigned long long m = 0;
+      for (int c0 = 0; c0 < n; c0 += 32) {
+        const int j = c0 + lane;
+        m |= (unsigned long long)__ballot_sync(0xffffffffu, j < n && cnt[j] == lvl) << c0;
+      }
+      unsigned long long rot = l0 ? ((m >> l0) | (m << (n - l0))) & nmask : m;
+      while (rot) {
+        int j = __ffsll((long long)rot) - 1 + l0;
+        rot &= rot - 1;
         j -= j >= n ? n : 0;
-        if (cnt[j] == lvl && !(supp[j] & used) && np < kMaxLow && np < n - 2) {
+        if (!(supp[j] & used) && np < kMaxLow && np < n - 2) {
           packed |= (unsigned long long)j << (8 * np);
           ++np;
           used |= supp[j];
         }
       }
+    }
   }
   // best lane: most picks, lowest lane on ties
   int key = (np << 8) | (31 - lane);
@@ -286,17 +298,19 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       const int nf = n - __popcll(slot_rows);
       while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
       if (fi == kNumNFix) ok = false;
-      int pos = 0;
-      int64_t g = 1;
-      for (int i = 0; i < n && ok; ++i) {
+      // every exact group of GF consecutive fixed rows: prod R_i < 2^(sum bl_i) <= 2^30
+      // (bit-length sums: a conservative, division- and multiply-free test)
+      const int* bl = sBl[wib];
+      int pos = 0, bits = 0;
+      for (int i = 0; i < n; ++i) {
         if ((slot_rows >> i) & 1ull) continue;
-        g = sat_mul(g, R[i]);
-        if (++pos % GF == 0) {
-          if (g >= ((int64_t)1 << 30)) ok = false;
-          g = 1;
+        bits += bl[i];
+        if ((++pos & (GF - 1)) == 0) {
+          if (bits > 30) ok = false;
+          bits = 0;
         }
       }
-      if (g >= ((int64_t)1 << 30)) ok = false;
+      if (bits > 30) ok = false;
       feasible = ok;
       // Montgomery factors per block value: NGF-1 (P_F chain) + one per exact E group
       if (ok) pmexp = nfix_of(fi) / GF - 1 + __popc(gend);
