@@ -159,9 +159,10 @@ int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d_out, void*
  *  d_early_*           [cap_early] unsplit nodes of order n (device; may be
  *                      NULL when cap_early == 0).
  *  h_out_count, h_early_count  host outputs: numbers written (or needed).
- * Synchronous w.r.t. the host (the counts are read back).  Returns
- * SPERM_ERR_CAPACITY if a capacity is too small (counts still report the
- * needed sizes), SPERM_ERR_RANGE if a merged entry or coefficient overflows. */
+ * count < 2^30 per call.  Synchronous w.r.t. the host (the counts are read
+ * back).  Returns SPERM_ERR_CAPACITY if a capacity is too small (counts still
+ * report the needed sizes), SPERM_ERR_RANGE if a merged entry or coefficient
+ * overflows; after either error the output buffers' contents are unspecified. */
 int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job,
                  int n, int64_t count,
                  int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job, int64_t cap_out,

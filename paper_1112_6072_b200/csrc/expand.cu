@@ -2,12 +2,11 @@
 // every node is split by Eq. (2) on its pivot line (Algorithm
 // H_per Step 1) into at most two children of order n-1.
 //
-// One warp per node.  Pass 1 (count) stages the node in shared memory, picks the pivot
-// (lane l holds columns l, l+32, ... of the row being scanned) and tests from the line
-// counts whether each child survives (no zero line, reading R4); an exclusive scan of the
-// per-node child counts gives every child its output slot in natural order (parents in
-// order, A1 before A2 — stable, reading R6); pass 2 (emit) writes the surviving children
-// output-element parallel (write_child).
+// One warp per node, one pass (expand_level_kernel): the node is staged in shared memory, the
+// pivot picked (lane-per-line counts) and each child tested for survival from the line counts
+// (no zero line, reading R4); a decoupled look-back over tiles of consecutive nodes gives every
+// surviving child its output slot in natural order (parents in order, A1 before A2 — stable,
+// reading R6), and the children are written output-element parallel (write_dense).
 //
 // A child is described by the lines it deletes and the merge it performs:
 //   row pivot r, merge of p_a,p_b:  delete row r, column p_b; column p_a := al*col(p_b) + be*col(p_a)
@@ -17,7 +16,6 @@
 #include <cstdlib>
 #include <mutex>
 
-#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -268,72 +266,145 @@ __device__ __forceinline__ void write_dense(const NodeView& A, const Child& ch, 
   }
 }
 
-__global__ void __launch_bounds__(kExpThreads) expand_count_kernel(
-    const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, int n, int64_t count,
-    int* __restrict__ kid_count, int* __restrict__ early_count, int* __restrict__ kid_mask,
-    int* __restrict__ err, int stage_words, Plan* __restrict__ plans) {
-  const int lane = threadIdx.x & 31;
-  const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (node >= count) return;
-  const NodeView A = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
-  const int64_t cf = coef ? coef[node] : 1;
-  __shared__ int s_cnt[kExpThreads / 32][2 * SPERM_EXPAND_NMAX];  // row and column counts per warp
-  int* rowcnt = s_cnt[threadIdx.x >> 5];
-  int* colcnt = rowcnt + SPERM_EXPAND_NMAX;
-  Plan pl = plan_node(A, cf, lane, rowcnt, colcnt);
-  int kids = 0, mask = 0;
-  bool ovf = false;
-  for (int c = 0; c < pl.nkids; ++c) {
-    if (!pl.kid[c].valid) ovf = true;
-    if (survives(A, pl.kid[c], rowcnt, colcnt, lane, &ovf)) {
-      ++kids;
-      mask |= 1 << c;
-    }
-  }
-  if (lane == 0) {
-    kid_count[node] = kids;
-    kid_mask[node] = mask;
-    plans[node] = pl;  // the emit pass reuses the pivot and children (no second scan)
-    early_count[node] = pl.early;
-    if (ovf) atomicOr(err, 1);
-  }
+// Tile status of the single-pass scan (decoupled look-back): flag (2 bits: 0 empty,
+// 1 aggregate, 2 inclusive prefix) | surviving children (31 bits) | early nodes (31 bits).
+constexpr unsigned long long kStFlagAgg = 1ull << 62, kStFlagPre = 2ull << 62;
+constexpr unsigned long long kSt31 = (1ull << 31) - 1;
+__device__ __forceinline__ unsigned long long st_pack(unsigned long long flag, long long kids, long long early) {
+  return flag | ((unsigned long long)kids << 31) | (unsigned long long)early;
 }
 
-__global__ void __launch_bounds__(kExpThreads) expand_emit_kernel(
+// One expansion level in a single pass.  A CTA takes the next tile of `wpb` consecutive
+// nodes (ticket order = node order), one warp per node: stage it, pick the pivot, test which
+// children survive; the tile's child / early counts get their output offsets from the
+// preceding tiles by a decoupled look-back, and every warp then writes its children (and
+// early node) in natural order.  The node is read from HBM once.  err bits: 1 overflow of a
+// merged entry or coefficient, 2 output capacity exceeded or output buffer missing.
+__global__ void __launch_bounds__(kExpThreads) expand_level_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, const int32_t* __restrict__ job,
-    int n, int64_t count, const int* __restrict__ kid_mask, const int64_t* __restrict__ kid_off,
-    const int64_t* __restrict__ early_off,
-    int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef, int32_t* __restrict__ out_job,
+    int n, int64_t count, int stage_words,
+    int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef, int32_t* __restrict__ out_job, int64_t cap_out,
     int32_t* __restrict__ early_mats, int64_t* __restrict__ early_coef, int32_t* __restrict__ early_job,
-    int stage_words, const Plan* __restrict__ plans) {
-  const int lane = threadIdx.x & 31;
-  const int64_t node = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (node >= count) return;
-  const int mask = kid_mask[node];
-  const Plan pl = plans[node];
-  if (!mask && !pl.early) return;  // no surviving child: nothing to read
-  const NodeView A = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
-  const int64_t cf = coef ? coef[node] : 1;
+    int64_t cap_early, unsigned long long* __restrict__ tile_status, unsigned* __restrict__ ticket,
+    long long* __restrict__ totals, int* __restrict__ err) {
+  __shared__ int s_tile;
+  __shared__ int s_kids[kExpThreads / 32], s_early[kExpThreads / 32];
+  __shared__ long long s_base[2];
+  __shared__ int s_cnt[kExpThreads / 32][2 * SPERM_EXPAND_NMAX];  // row and column counts per warp
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t node = tile * wpb + w;
+  const bool live = node < count;
+  NodeView A;
+  Plan pl;
+  pl.nkids = 0;
+  pl.early = 0;
+  int kids = 0, mask = 0;
+  int64_t cf = 1;
+  if (live) {
+    A = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
+    cf = coef ? coef[node] : 1;
+    int* rowcnt = s_cnt[w];
+    int* colcnt = rowcnt + SPERM_EXPAND_NMAX;
+    pl = plan_node(A, cf, lane, rowcnt, colcnt);
+    bool ovf = false;
+    for (int c = 0; c < pl.nkids; ++c) {
+      if (!pl.kid[c].valid) ovf = true;
+      if (survives(A, pl.kid[c], rowcnt, colcnt, lane, &ovf)) {
+        ++kids;
+        mask |= 1 << c;
+      }
+    }
+    if (ovf && lane == 0) atomicOr(err, 1);
+  }
+  if (lane == 0) {
+    s_kids[w] = kids;
+    s_early[w] = pl.early;
+  }
+  __syncthreads();
+  if (w == 0) {
+    // warp 0: tile aggregate, publish it, then look back over the preceding tiles 32 at a time
+    // (lane l reads tile j - l): aggregates are summed until the nearest inclusive prefix
+    long long ak = 0, ae = 0;
+    for (int i = 0; i < wpb; ++i) {
+      ak += s_kids[i];
+      ae += s_early[i];
+    }
+    long long ek = 0, ee = 0;  // exclusive prefix of this tile
+    if (tile == 0) {
+      if (lane == 0) atomicExch(tile_status, st_pack(kStFlagPre, ak, ae));
+    } else {
+      if (lane == 0) atomicExch(tile_status + tile, st_pack(kStFlagAgg, ak, ae));
+      int64_t j = tile - 1;  // newest tile of the current window
+      while (true) {
+        const int64_t t = j - lane;
+        unsigned long long v = 2ull << 62;  // before tile 0: an empty inclusive prefix
+        if (t >= 0) v = *(volatile unsigned long long*)(tile_status + t);
+        // wait until every tile of the window up to the nearest prefix has published
+        unsigned pre = __ballot_sync(0xffffffffu, (v & (3ull << 62)) == kStFlagPre);
+        const unsigned upto = pre ? (pre & (0u - pre)) * 2u - 1u : 0xffffffffu;  // lanes <= first prefix
+        if (__ballot_sync(0xffffffffu, (v & (3ull << 62)) == 0ull) & upto) continue;  // re-read the window
+        long long k_ = 0, e_ = 0;
+        if ((upto >> lane) & 1u && t >= 0) {
+          k_ = (long long)((v >> 31) & kSt31);
+          e_ = (long long)(v & kSt31);
+        }
+        for (int o = 16; o; o >>= 1) {
+          k_ += __shfl_xor_sync(0xffffffffu, k_, o);
+          e_ += __shfl_xor_sync(0xffffffffu, e_, o);
+        }
+        ek += k_;
+        ee += e_;
+        if (pre) break;
+        j -= 32;
+      }
+      if (lane == 0) atomicExch(tile_status + tile, st_pack(kStFlagPre, ek + ak, ee + ae));
+    }
+    if (lane == 0) {
+      s_base[0] = ek;
+      s_base[1] = ee;
+      if ((tile + 1) * wpb >= count) {  // the last tile: level totals
+        totals[0] = ek + ak;
+        totals[1] = ee + ae;
+      }
+    }
+  }
+  __syncthreads();
+  if (!live) return;
+  long long ok_ = s_base[0], oe = s_base[1];
+  for (int i = 0; i < w; ++i) {
+    ok_ += s_kids[i];
+    oe += s_early[i];
+  }
   const int32_t jb = job ? job[node] : (int32_t)node;
   if (pl.early) {
-    const int64_t o = early_off[node];
-    write_dense<false>(A, pl.kid[0], early_mats + o * (int64_t)n * n, lane);
+    if (oe >= cap_early || !early_mats || !early_coef || !early_job) {
+      if (lane == 0) atomicOr(err, 2);
+      return;
+    }
+    write_dense<false>(A, pl.kid[0], early_mats + oe * (int64_t)n * n, lane);
     if (lane == 0) {
-      early_coef[o] = cf;
-      early_job[o] = jb;
+      early_coef[oe] = cf;
+      early_job[oe] = jb;
     }
     return;
   }
-  int64_t o = kid_off[node];
+  if (!kids) return;
+  if (ok_ + kids > cap_out || !out_mats || !out_coef || !out_job) {
+    if (lane == 0) atomicOr(err, 2);
+    return;
+  }
   const int64_t m2 = (int64_t)(n - 1) * (n - 1);
   for (int c = 0; c < pl.nkids; ++c) {
-    if ((mask >> c) & 1) {  // survivors found by the count pass
-      write_dense<true>(A, pl.kid[c], out_mats + o * m2, lane);
+    if ((mask >> c) & 1) {
+      write_dense<true>(A, pl.kid[c], out_mats + ok_ * m2, lane);
       if (lane == 0) {
-        out_coef[o] = pl.kid[c].coef;
-        out_job[o] = jb;
+        out_coef[ok_] = pl.kid[c].coef;
+        out_job[ok_] = jb;
       }
-      ++o;
+      ++ok_;
     }
   }
 }
@@ -357,84 +428,47 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   *h_early_count = 0;
   if (n < 2 || n > SPERM_EXPAND_NMAX) return set_error(SPERM_ERR_ARG, "sperm_expand: n out of range [2, 128]");
   if (count < 0) return set_error(SPERM_ERR_ARG, "sperm_expand: count < 0");
+  if (count >= (int64_t)1 << 30) return set_error(SPERM_ERR_ARG, "sperm_expand: count >= 2^30 (split the level)");
   if (count == 0) return SPERM_OK;
   if (!d_in_mats) return set_error(SPERM_ERR_ARG, "sperm_expand: d_in_mats is NULL");
-  // scratch: kid_count[count] int, early_count[count] int, offsets 2*count int64, err int, totals
-  int* kc = nullptr;
-  SPERM_CUDA(cudaMallocAsync((void**)&kc, sizeof(int) * (3 * count + 4), st));
-  int* ec = kc + count;
-  int* km = kc + 2 * count;
-  int* err = kc + 3 * count;
-  int64_t* off = nullptr;
-  SPERM_CUDA(cudaMallocAsync((void**)&off, sizeof(int64_t) * (2 * count + 2), st));
-  int64_t* eoff = off + count + 1;
-  Plan* plans = nullptr;  // per-node pivot and children, count pass -> emit pass
-  SPERM_CUDA(cudaMallocAsync((void**)&plans, sizeof(Plan) * count, st));
-  SPERM_CUDA(cudaMemsetAsync(err, 0, sizeof(int) * 4, st));
   // shared-memory staging of each warp's node (row stride n | 1): up to 8 warps per CTA within 200 KB
   const int stage_words = ((n * stage_stride(n) + 3) / 4) * 4;
   const int wpb = std::max(1, std::min(8, (int)((200 * 1024) / (stage_words * 4))));
   const size_t esmem = (size_t)wpb * stage_words * 4;
-  SPERM_CUDA(cudaFuncSetAttribute(expand_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
-  SPERM_CUDA(cudaFuncSetAttribute(expand_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
-  const unsigned bthreads = 32u * wpb;
-  const unsigned blocks = (unsigned)((count * 32 + bthreads - 1) / bthreads);
-  int rc = SPERM_OK;
-  auto cleanup = [&]() {
-    cudaFreeAsync(kc, st);
-    cudaFreeAsync(off, st);
-    cudaFreeAsync(plans, st);
-  };
+  const int64_t tiles = (count + wpb - 1) / wpb;
+  // workspace: tile status [tiles] u64 | totals [2] i64 | ticket u32, err i32
+  unsigned long long* ws = nullptr;
+  SPERM_CUDA(cudaMallocAsync((void**)&ws, sizeof(unsigned long long) * (tiles + 3), st));
+  SPERM_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * (tiles + 3), st));
+  long long* totals = reinterpret_cast<long long*>(ws + tiles);
+  unsigned* ticket = reinterpret_cast<unsigned*>(ws + tiles + 2);
+  int* err = reinterpret_cast<int*>(ticket + 1);
+  SPERM_CUDA(cudaFuncSetAttribute(expand_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
   {
     TimingScope ts("expand", st);
     count_launch();
-    expand_count_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, n, count, kc, ec, km, err,
-                                                         stage_words, plans);
+    expand_level_kernel<<<(unsigned)tiles, 32u * wpb, esmem, st>>>(
+        d_in_mats, d_in_coef, d_in_job, n, count, stage_words, d_out_mats, d_out_coef, d_out_job, cap_out,
+        d_early_mats, d_early_coef, d_early_job, cap_early, ws, ticket, totals, err);
   }
   cudaError_t le = cudaGetLastError();
-  if (le != cudaSuccess) { cleanup(); return cuda_check(le, "expand_count_kernel"); }
-  // exclusive scans (count+1 entries: the last one is the total)
-  SPERM_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * (2 * count + 2), st));
-  size_t tmp_bytes = 0, tmp2 = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, kc, off + 1, count, st);
-  cub::DeviceScan::InclusiveSum(nullptr, tmp2, ec, eoff + 1, count, st);
-  tmp_bytes = std::max(tmp_bytes, tmp2);
-  void* tmp = nullptr;
-  SPERM_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
-  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, kc, off + 1, count, st);
-  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, ec, eoff + 1, count, st);
-  cudaFreeAsync(tmp, st);
-  int64_t tot[2] = {0, 0};
+  if (le != cudaSuccess) {
+    cudaFreeAsync(ws, st);
+    return cuda_check(le, "expand_level_kernel");
+  }
+  long long tot[2] = {0, 0};
   int herr = 0;
-  SPERM_CUDA(cudaMemcpyAsync(&tot[0], off + count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  SPERM_CUDA(cudaMemcpyAsync(&tot[1], eoff + count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SPERM_CUDA(cudaMemcpyAsync(tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, st));
   SPERM_CUDA(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(ws, st);
   le = cudaStreamSynchronize(st);
-  if (le != cudaSuccess) { cleanup(); return cuda_check(le, "sperm_expand count readback"); }
+  if (le != cudaSuccess) return cuda_check(le, "sperm_expand read-back");
   *h_out_count = tot[0];
   *h_early_count = tot[1];
-  if (herr) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_expand: merged entry or coefficient overflow"); }
-  if (tot[0] > cap_out || tot[1] > cap_early) {
-    cleanup();
+  if (herr & 1) return set_error(SPERM_ERR_RANGE, "sperm_expand: merged entry or coefficient overflow");
+  if (tot[0] > cap_out || tot[1] > cap_early)
     return set_error(SPERM_ERR_CAPACITY, "sperm_expand: output capacity too small");
-  }
-  if ((tot[0] > 0 && (!d_out_mats || !d_out_coef || !d_out_job)) ||
-      (tot[1] > 0 && (!d_early_mats || !d_early_coef || !d_early_job))) {
-    cleanup();
-    return set_error(SPERM_ERR_ARG, "sperm_expand: NULL output buffer");
-  }
-  {
-    TimingScope ts("expand", st);
-    count_launch();
-    // the emit pass stages the parent too (read once, then once per child from shared memory;
-    // measured on the config-5 fullerene: 1.46 s staged vs 1.73 s reading global memory)
-    expand_emit_kernel<<<blocks, bthreads, esmem, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, km, off, eoff,
-                                                        d_out_mats, d_out_coef, d_out_job, d_early_mats, d_early_coef,
-                                                        d_early_job, stage_words, plans);
-  }
-  le = cudaGetLastError();
-  cleanup();
-  if (le != cudaSuccess) return cuda_check(le, "expand_emit_kernel");
+  if (herr & 2) return set_error(SPERM_ERR_ARG, "sperm_expand: NULL output buffer");
   {
     // algorithmic bytes of the level: every parent read once (matrix + coef + job), every
     // child and early node written once
@@ -443,7 +477,7 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
                    (double)tot[1] * (4.0 * n * n + 12.0);
     g_exp_nodes += (double)count;
   }
-  return rc;
+  return SPERM_OK;
 }
 
 extern "C" int sperm_expand_stats(double* h_bytes, double* h_nodes, int reset) {
