@@ -193,27 +193,28 @@ __device__ int survives(const NodeView& A, const Child& ch, const int* __restric
   return ok ? 1 : 0;
 }
 
-// Words each lane moves per batch: all of a batch's loads are issued before its stores, so a
-// node's whole transfer is in flight at once (a node of order <= 22 is one batch) instead of
-// one dependent load round trip per row — the expansion levels are latency-bound otherwise.
-constexpr int kStageU = 16;
+// Staging moves US words per lane per batch: all of a batch's loads are issued before its
+// stores, so a node's whole transfer is in flight at once instead of one dependent load round
+// trip per row.  The kernel is instantiated for US = 4, 8, 12, 16 and launched with the
+// smallest that covers the node in one batch (n <= 22), so few predicated-off slots are issued.
 
 // Copies the warp's node (dense, row-major in global memory) into its shared-memory slot with
 // row stride stage_stride(n); `stage_words` = the slot size in words.
+template <int US>
 __device__ __forceinline__ NodeView stage_node(const int32_t* __restrict__ g, int n, int stage_words, int lane) {
   extern __shared__ int32_t esm[];
   int32_t* s = esm + (threadIdx.x >> 5) * stage_words;
   const int nn = n * n, ns = stage_stride(n);
   const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)n) + 1u;  // e / n for e * n < 2^32
-  for (int base = 0; base < nn; base += 32 * kStageU) {
-    int32_t r[kStageU];
+  for (int base = 0; base < nn; base += 32 * US) {
+    int32_t r[US];
 #pragma unroll
-    for (int u = 0; u < kStageU; ++u) {
+    for (int u = 0; u < US; ++u) {
       const int e = base + u * 32 + lane;
       r[u] = e < nn ? g[e] : 0;
     }
 #pragma unroll
-    for (int u = 0; u < kStageU; ++u) {
+    for (int u = 0; u < US; ++u) {
       const int e = base + u * 32 + lane;
       const int i = (int)__umulhi((uint32_t)e, magic);
       if (e < nn) s[i * ns + (e - i * n)] = r[u];
@@ -239,10 +240,13 @@ __device__ __forceinline__ void write_dense(const NodeView& A, const Child& ch, 
   const int dr = CHILD ? ch.del_row : 0x7fff, dc = CHILD ? ch.del_col : 0x7fff;
   // floor(e / m) = umulhi(e, ceil(2^32 / m)) exactly for e * m < 2^32 (e < 2^14 here)
   const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)m) + 1u;
-  for (int base = 0; base < mm; base += 32 * kStageU) {
-    int32_t r[kStageU];
+  // batches of 4 elements per lane: the loads come from shared memory and the stores need no
+  // round trip, so short batches cost no latency and waste fewer predicated-off slots
+  constexpr int UW = 4;
+  for (int base = 0; base < mm; base += 32 * UW) {
+    int32_t r[UW];
 #pragma unroll
-    for (int u = 0; u < kStageU; ++u) {
+    for (int u = 0; u < UW; ++u) {
       const int e = base + u * 32 + lane;
       int32_t v = 0;
       if (e < mm) {
@@ -259,7 +263,7 @@ __device__ __forceinline__ void write_dense(const NodeView& A, const Child& ch, 
       r[u] = v;
     }
 #pragma unroll
-    for (int u = 0; u < kStageU; ++u) {
+    for (int u = 0; u < UW; ++u) {
       const int e = base + u * 32 + lane;
       if (e < mm) out[e] = r[u];
     }
@@ -280,7 +284,8 @@ __device__ __forceinline__ unsigned long long st_pack(unsigned long long flag, l
 // preceding tiles by a decoupled look-back, and every warp then writes its children (and
 // early node) in natural order.  The node is read from HBM once.  err bits: 1 overflow of a
 // merged entry or coefficient, 2 output capacity exceeded or output buffer missing.
-__global__ void __launch_bounds__(kExpThreads) expand_level_kernel(
+template <int US>
+__global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, const int32_t* __restrict__ job,
     int n, int64_t count, int stage_words,
     int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef, int32_t* __restrict__ out_job, int64_t cap_out,
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(kExpThreads) expand_level_kernel(
   int kids = 0, mask = 0;
   int64_t cf = 1;
   if (live) {
-    A = stage_node(mats + node * (int64_t)n * n, n, stage_words, lane);
+    A = stage_node<US>(mats + node * (int64_t)n * n, n, stage_words, lane);
     cf = coef ? coef[node] : 1;
     int* rowcnt = s_cnt[w];
     int* colcnt = rowcnt + SPERM_EXPAND_NMAX;
@@ -443,11 +448,14 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   long long* totals = reinterpret_cast<long long*>(ws + tiles);
   unsigned* ticket = reinterpret_cast<unsigned*>(ws + tiles + 2);
   int* err = reinterpret_cast<int*>(ticket + 1);
-  SPERM_CUDA(cudaFuncSetAttribute(expand_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+  const int per_lane = (n * n + 31) / 32;
+  auto kern = per_lane <= 4 ? expand_level_kernel<4> : per_lane <= 8 ? expand_level_kernel<8>
+            : per_lane <= 12 ? expand_level_kernel<12> : expand_level_kernel<16>;
+  SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
   {
     TimingScope ts("expand", st);
     count_launch();
-    expand_level_kernel<<<(unsigned)tiles, 32u * wpb, esmem, st>>>(
+    kern<<<(unsigned)tiles, 32u * wpb, esmem, st>>>(
         d_in_mats, d_in_coef, d_in_job, n, count, stage_words, d_out_mats, d_out_coef, d_out_job, cap_out,
         d_early_mats, d_early_coef, d_early_job, cap_early, ws, ticket, totals, err);
   }
