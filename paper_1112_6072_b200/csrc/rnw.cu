@@ -718,44 +718,28 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
 }
 
 // ============================================================================ finalize
-__device__ __forceinline__ uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
-  uint64_t r = 1 % p;
-  b %= p;
-  while (e) {
-    if (e & 1) r = r * b % p;
-    b = b * b % p;
-    e >>= 1;
-  }
-  return r;
-}
-
 // Largest Montgomery exponent a plan can record in meta.y (generic: NP/G - 1 <= 47; tree:
-// NFIX/GF + 2 <= 22), so a finalize block tabulates the per-leaf scale factors once.
+// NFIX/GF - 1 + B <= 27).
 constexpr int kMaxMexp = 48;
 constexpr int kFinThreads = 256;  // 32 leaves x 8 primes per block iteration
 
-// Leaf residues per = (-1)^(n-1) 2^(1-n) R^mexp S mod p_q (R = 2^32: the kernels' Montgomery
-// factors), times the leaf coefficient; accumulated into the job rows and the total row.  A
-// grid-stride kernel: each block builds the factor table f[q][mexp] once, then handles 32
-// leaves per iteration and adds each (job, q) run of equal jobs with one atomic.
+// Per-call scale factors f[q][mexp] = (-1)^(n-1) 2^(1-n) R^mexp mod p_q (R = 2^32: the kernels'
+// Montgomery factors), computed on the host (fin_table) and passed by value.
+struct FinTable {
+  uint32_t f[SPERM_KMAX][kMaxMexp];
+};
+
+// Leaf residues per = f[q][mexp] S mod p_q, times the leaf coefficient; accumulated into the job
+// rows and the total row.  A grid-stride kernel: 32 leaves per block iteration, each (job, q)
+// run of equal jobs added with one atomic.
 __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
     int n, int64_t count, const int2* __restrict__ meta, const unsigned long long* __restrict__ leaf_acc,
     const int64_t* __restrict__ coef, const int32_t* __restrict__ job, uint32_t* __restrict__ leaf_res,
-    int32_t* __restrict__ leaf_k, unsigned long long* __restrict__ job_acc, int64_t num_jobs) {
+    int32_t* __restrict__ leaf_k, unsigned long long* __restrict__ job_acc, int64_t num_jobs, const FinTable tab) {
   __shared__ uint32_t s_f[SPERM_KMAX][kMaxMexp];
+  for (int t = threadIdx.x; t < SPERM_KMAX * kMaxMexp; t += blockDim.x) s_f[t / kMaxMexp][t % kMaxMexp] = tab.f[t / kMaxMexp][t % kMaxMexp];
   __shared__ unsigned long long s_val[kFinThreads];
   __shared__ int32_t s_job[kFinThreads / SPERM_KMAX];
-  for (int t = threadIdx.x; t < SPERM_KMAX * kMaxMexp; t += blockDim.x) {
-    const int q = t / kMaxMexp, y = t % kMaxMexp;
-    const uint64_t pq = (uint64_t)c_p[q];
-    uint64_t f = 1;
-    if (n > 0) {
-      f = powmod((pq + 1) / 2, (uint64_t)(n - 1), pq);
-      f = f * powmod(((uint64_t)1 << 32) % pq, (uint64_t)y, pq) % pq;
-      if ((n - 1) & 1) f = (pq - f) % pq;
-    }
-    s_f[q][y] = (uint32_t)f;
-  }
   __syncthreads();
   const int q = threadIdx.x % SPERM_KMAX, li = threadIdx.x / SPERM_KMAX;
   const uint64_t pq = (uint64_t)c_p[q];
@@ -1014,6 +998,24 @@ int first_plan() {
   return (p >= 0 && p < kNumPlans) ? p : 1;
 }
 
+// f[q][y] = (-1)^(n-1) 2^(1-n) (2^32)^y mod p_q (exact uint64 arithmetic on the host)
+FinTable fin_table(int n) {
+  FinTable t;
+  for (int q = 0; q < SPERM_KMAX; ++q) {
+    const uint64_t p = kPrimes[q];
+    uint64_t base = 1;  // 2^(1-n) = ((p+1)/2)^(n-1)
+    for (int i = 1; i < n; ++i) base = base * ((p + 1) / 2) % p;
+    if (n > 0 && ((n - 1) & 1)) base = (p - base) % p;
+    const uint64_t R = ((uint64_t)1 << 32) % p;
+    uint64_t f = base;
+    for (int y = 0; y < kMaxMexp; ++y) {
+      t.f[q][y] = (uint32_t)f;
+      f = f * R % p;
+    }
+  }
+  return t;
+}
+
 // ---------------------------------------------------------------------------- op model
 // Algorithmic 32-bit integer lane-operations of one evaluation, per the kernels' own
 // formulation.  IMAD.WIDE and IMAD.HI occupy the multiply (FMA) pipe twice
@@ -1244,7 +1246,8 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     count_launch();
     const int64_t fblocks = std::min<int64_t>((tot + kFinThreads - 1) / kFinThreads, (int64_t)sm_count() * 8);
     rnw_finalize_kernel<<<(unsigned)fblocks, kFinThreads, 0, st>>>(
-        n, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k, (unsigned long long*)d_job_acc, num_jobs);
+        n, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k, (unsigned long long*)d_job_acc, num_jobs,
+        fin_table(n));
   }
   cudaError_t le = cudaGetLastError();
   cleanup();
