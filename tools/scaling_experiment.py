@@ -51,7 +51,12 @@ def kendall_tau(x, y):
 
 def study(P, pipeline, name, a, J, L, Gs=(1, 2, 4, 8)):
     import torch
+    # device time of the replicated pre-expansion alone (every rank repeats it)
     P.sperm_timing_enable(True)
+    P.sperm_timing_reset()
+    pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=J)
+    torch.cuda.synchronize()
+    pre_ms = P.sperm_timing_get("expand")[0]
     P.sperm_timing_reset()
     t0 = time.perf_counter()
     r = pipeline.permanent(a, jobs_at_least=J, leaf_order=L, measure_jobs=True)
@@ -76,20 +81,32 @@ def study(P, pipeline, name, a, J, L, Gs=(1, 2, 4, 8)):
         "estimate": (est, "estimate", np.argsort(-est, kind="stable")),
         "exact": (T, "estimate", np.argsort(-T, kind="stable")),
     }
+    # projected whole-path efficiency on G GPUs from the measured single-GPU stage times: the
+    # pre-expansion is replicated, KKLLL sharded (1/G), the per-job work (expansion to leaves,
+    # prep, R-NW, finalize) split as the static plan deals the measured job costs T_i
+    kk_s = stage_ms["kklll"] * 1e-3
+    pre_s = pre_ms * 1e-3
+    eval_s = (stage_ms["expand"] - pre_ms + stage_ms["rnw_prep"] + stage_ms["rnw"] + stage_ms["rnw_finalize"]) * 1e-3
+    t1 = pre_s + kk_s + eval_s
+    res["projection"] = {"pre_expand_s": pre_s, "kklll_s": kk_s, "per_job_work_s": eval_s, "by_G": {}}
     for G in Gs:
         row = {}
+        proj = {}
         for pname, (w, code, dyn_order) in policies.items():
             ms_static, _ = static_plan(P, w, T, G, code)
             ms_dyn = dynamic_ls(dyn_order, T, G)
             row[pname] = {"static": total / (G * ms_static), "dynamic": total / (G * ms_dyn)}
+            tg = pre_s + kk_s / G + eval_s * ms_static / total
+            proj[pname] = {"wall_s": tg, "efficiency": t1 / (G * tg)}
         res["efficiency"][str(G)] = row
+        res["projection"]["by_G"][str(G)] = proj
     return res
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", default="48,160,1000", help="comma-separated J values (jobs_at_least)")
-    ap.add_argument("--leaf", type=int, default=22)
+    ap.add_argument("--leaf", type=int, default=16)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "scaling.json"))
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
@@ -109,6 +126,9 @@ def main():
             for G, row in res["efficiency"].items():
                 print(f"  G={G}: " + "  ".join(f"{p}: s{v['static']:.4f}/d{v['dynamic']:.4f}"
                                                for p, v in row.items()), flush=True)
+                pr = res["projection"]["by_G"][G]
+                print(f"  G={G} projected whole-path efficiency: " +
+                      "  ".join(f"{p}: {v['efficiency']:.3f}" for p, v in pr.items()), flush=True)
             with open(args.out, "w") as f:
                 json.dump(out, f, indent=1)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
