@@ -80,6 +80,18 @@ __constant__ int32_t c_p[SPERM_KMAX] = {2147483647, 2147483629, 2147483587, 2147
                                         2147483563, 2147483549, 2147483543, 2147483497};
 __constant__ int32_t c_pinv[SPERM_KMAX] = {2147483647, 1469330917, -1091344149, -591336077,
                                            -2096954621, -1062895947, -1493012441, -1066630951};
+// The same values as compile-time functions: in the fully unrolled per-prime loops of the R-NW
+// kernels q is a constant, so p and p^-1 become instruction immediates (no constant-bank loads).
+__host__ __device__ constexpr int32_t prime_p(int q) {
+  return q == 0 ? 2147483647 : q == 1 ? 2147483629 : q == 2 ? 2147483587 : q == 3 ? 2147483579
+       : q == 4 ? 2147483563 : q == 5 ? 2147483549 : q == 6 ? 2147483543 : 2147483497;
+}
+__host__ __device__ constexpr int32_t prime_pinv(int q) {
+  return q == 0 ? 2147483647 : q == 1 ? 1469330917 : q == 2 ? -1091344149 : q == 3 ? -591336077
+       : q == 4 ? -2096954621 : q == 5 ? -1062895947 : q == 6 ? -1493012441 : -1066630951;
+}
+static_assert(prime_p(7) == (int32_t)kPrimes[7] && prime_p(0) == (int32_t)kPrimes[0], "prime table");
+static_assert((int32_t)((uint32_t)prime_p(3) * (uint32_t)prime_pinv(3)) == 1, "p * p^-1 = 1 mod 2^32");
 
 // Signed Montgomery product a*b*2^-32 mod p for |a|,|b| < p < 2^31; result in (-p, p).
 __device__ __forceinline__ int32_t smont(int32_t a, int32_t b, int32_t p, int32_t pinv) {
@@ -398,7 +410,7 @@ __device__ __forceinline__ void term_product(const int32_t (&w)[NP], int k, int3
     if (q < k) {
       int32_t pr = gp[0];
 #pragma unroll
-      for (int g = 1; g < NG; ++g) pr = smont(pr, gp[g], c_p[q], c_pinv[q]);
+      for (int g = 1; g < NG; ++g) pr = smont(pr, gp[g], prime_p(q), prime_pinv(q));
       out[q] = pr;
     }
   }
@@ -691,7 +703,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
 #pragma unroll
       for (int q = 0; q < SPERM_KMAX; ++q) {
         if (q < k) {
-          const int32_t p = c_p[q], pinv = c_pinv[q];
+          const int32_t p = prime_p(q), pinv = prime_pinv(q);
           int32_t v = FG[0];
 #pragma unroll
           for (int g = 1; g < NGF; ++g) v = smont(v, FG[g], p, pinv);
