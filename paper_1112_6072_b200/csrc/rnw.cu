@@ -50,7 +50,7 @@ constexpr int KS = 3;             // slot rows per low column (tree plans)
 constexpr int kNumNFix = 7;
 constexpr int kPermRows = 64;     // per-leaf permutation record: 64 row bytes + 64 column bytes
 constexpr int kPermW = 128;
-constexpr int kPermGend = kPermW - 1;  // byte 127 (column bytes >= 48 are unused): E-group ends
+constexpr int kPermGend = kPermW - 1;  // byte 127 (column bytes >= 48 are unused): E mode
 constexpr int kNumKeys = 104;     // plan * 8 + nfix index
 
 __host__ __device__ constexpr int nfix_of(int i) {
@@ -278,16 +278,17 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   const int pl = lane + 1;
   bool feasible = false;
   int fi = 0, pmexp = 0;
-  unsigned gend = 0;  // bit c: an exact group of E_c ends at low column c
+  int emode = 0;  // exact E groups: 0 singles, 1 pairs, 2 quads
   unsigned long long slot_rows = 0;
   {
     const bool test = pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0;
     const int B = plan_b(pl), GF = plan_gf(pl);
-    // every slot product |Q_c| <= q_c < 2^30 keeps E_c = Q_c^0 - Q_c^1 in int32; consecutive
-    // E_c are multiplied exactly while the product of their bounds 2 q_c stays < 2^31 (a group
-    // ends at bit c of gend), each group then costs one Montgomery product per prime
-    bool qok = true;
-    int64_t gp = 1;
+    // every slot product |Q_c| <= q_c < 2^30 keeps E_c = Q_c^0 - Q_c^1 in int32 (|E_c| <= 2 q_c);
+    // the E_c are then multiplied exactly in fixed groups — quads (c = 4j..4j+3) if every quad's
+    // bound product is < 2^31, else pairs if every pair's is, else singly (the leaf's E mode) —
+    // and each group costs one Montgomery product per prime
+    bool qok = true, pair_ok = true, quad_ok = true;
+    int64_t pp = 1, qp = 1;
 #pragma unroll
     for (int c = 0; c < kMaxLow; ++c) {  // warp-uniform shuffles, per-lane plan bounds
       const int64_t q = __shfl_sync(0xffffffffu, my_q, c);
@@ -296,15 +297,14 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
         slot_rows |= sc;
         if (q >= ((int64_t)1 << 30)) qok = false;
         const int64_t e = 2 * q;
-        if (c > 0 && sat_mul(gp, e) >= ((int64_t)1 << 31)) {
-          gend |= 1u << (c - 1);
-          gp = e;
-        } else {
-          gp = c == 0 ? e : sat_mul(gp, e);
-        }
+        pp = (c & 1) ? sat_mul(pp, e) : e;
+        qp = (c & 3) ? sat_mul(qp, e) : e;
+        if (pp >= ((int64_t)1 << 31)) pair_ok = false;
+        if (qp >= ((int64_t)1 << 31)) quad_ok = false;
       }
     }
-    gend |= 1u << (B > 0 ? B - 1 : 0);
+    emode = quad_ok ? 2 : pair_ok ? 1 : 0;
+    const int ngroups = emode == 2 ? (B + 3) / 4 : emode == 1 ? (B + 1) / 2 : B;
     if (test && np >= B && n - 6 >= B) {
       bool ok = qok;
       const int nf = n - __popcll(slot_rows);
@@ -325,7 +325,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (bits > 30) ok = false;
       feasible = ok;
       // Montgomery factors per block value: NGF-1 (P_F chain) + one per exact E group
-      if (ok) pmexp = nfix_of(fi) / GF - 1 + __popc(gend);
+      if (ok) pmexp = nfix_of(fi) / GF - 1 + ngroups;
     }
   }
   const unsigned fmask = __ballot_sync(0xffffffffu, feasible);
@@ -371,7 +371,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     for (int f = n - __popcll(slot_rows) + lane; f < NF; f += 32) pr[B * KS + f] = -1;
     if (lane == 0) pc[n - 1] = (int8_t)nw;
     if (lane == win) {
-      pr[kPermGend] = (int8_t)gend;
+      pr[kPermGend] = (int8_t)emode;  // this lane tested the winning plan
       meta[leaf] = make_int2(k | (wpl << 8) | (wfi << 16), pmexp);
     }
   } else if (lane == 0) {
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
   int64_t cur_leaf = -1;
   int64_t prev_leaf = -1;
   long long t_item = 0;
-  unsigned gend = 0;
+  int emode = 0;
   while (true) {
     unsigned long long item = 0;
     if (lane == 0) item = atomicAdd(queue, 1ull);
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         const int row = pr[s];
         sm[L.delta + s] = row >= 0 ? 2 * a[row * n + pc[s / KS]] : 0;
       }
-      gend = (unsigned)(uint8_t)pr[kPermGend];
+      emode = pr[kPermGend];
       __syncwarp();
       cur_leaf = leaf;
     }
@@ -678,8 +678,11 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
         }
       }
-      // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1), exact per group
-      int32_t E[B];
+      // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1); exact products of
+      // pairs and quads of the E_c (used when the leaf's E mode says they fit int32; wrapped
+      // otherwise and then unused)
+      constexpr int NP2 = (B + 1) / 2, NP4 = (B + 3) / 4;
+      int32_t E[B], P2[NP2], P4[NP4];
 #pragma unroll
       for (int c = 0; c < B; ++c) {
         int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
@@ -689,8 +692,13 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           x1 *= W[c * KS + s] + D[c * KS + s];
         }
         E[c] = x0 - x1;
-        if (c > 0 && !((gend >> (c - 1)) & 1u)) E[c] *= E[c - 1];  // joins the previous group
       }
+#pragma unroll
+      for (int j = 0; j < NP2; ++j)
+        P2[j] = 2 * j + 1 < B ? (int32_t)((uint32_t)E[2 * j] * (uint32_t)E[2 * j + 1]) : E[2 * j];
+#pragma unroll
+      for (int j = 0; j < NP4; ++j)
+        P4[j] = 2 * j + 1 < NP2 ? (int32_t)((uint32_t)P2[2 * j] * (uint32_t)P2[2 * j + 1]) : P2[2 * j];
       int32_t FG[NGF];
 #pragma unroll
       for (int g = 0; g < NGF; ++g) {
@@ -707,9 +715,16 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           int32_t v = FG[0];
 #pragma unroll
           for (int g = 1; g < NGF; ++g) v = smont(v, FG[g], p, pinv);
+          if (emode == 2) {  // warp-uniform: per-leaf mode
 #pragma unroll
-          for (int c = 0; c < B; ++c)
-            if ((gend >> c) & 1u) v = smont(v, E[c], p, pinv);  // warp-uniform: per-leaf mask
+            for (int j = 0; j < NP4; ++j) v = smont(v, P4[j], p, pinv);
+          } else if (emode == 1) {
+#pragma unroll
+            for (int j = 0; j < NP2; ++j) v = smont(v, P2[j], p, pinv);
+          } else {
+#pragma unroll
+            for (int c = 0; c < B; ++c) v = smont(v, E[c], p, pinv);
+          }
           acc[q] += neg ? -(int64_t)v : (int64_t)v;
         }
       }
