@@ -140,6 +140,38 @@ def test_expand_c20_identical_job_lists():
         assert _gpu_jobs(a, J) == _oracle_jobs(a, J)
 
 
+def test_expand_c60_many_tiles_identical():
+    """Levels of thousands of nodes: the single-pass look-back spans hundreds of 8-node tiles
+    (beyond its 32-tile window), and the job list still equals the oracle's, in order."""
+    a = truncated_icosahedron()
+    assert _gpu_jobs(a, 3000) == _oracle_jobs(a, 3000)
+
+
+def test_expand_capacity_and_null_outputs():
+    """Raw C ABI: too small an output capacity -> SPERM_ERR_CAPACITY with the needed counts;
+    NULL output buffers with children to write -> SPERM_ERR_ARG."""
+    import ctypes
+    a = truncated_icosahedron()
+    s = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=500)[0]
+    (km, _, _), (em, _, _) = P.sperm_expand(s.mats, s.coef, s.job)
+    need = km.shape[0]
+    n = s.n
+    L = P.sperm.lib()
+    oc, ec = ctypes.c_int64(0), ctypes.c_int64(0)
+    small = need // 2
+    om = torch.empty((max(small, 1), n - 1, n - 1), dtype=torch.int32, device="cuda")
+    ocf = torch.empty(max(small, 1), dtype=torch.int64, device="cuda")
+    oj = torch.empty(max(small, 1), dtype=torch.int32, device="cuda")
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    rc = L.sperm_expand(ptr(s.mats), ptr(s.coef), ptr(s.job), n, s.count, ptr(om), ptr(ocf), ptr(oj), small,
+                        None, None, None, 0, ctypes.byref(oc), ctypes.byref(ec), None)
+    assert rc == P.sperm.ERR_CAPACITY and oc.value == need and ec.value == em.shape[0]
+    rc = L.sperm_expand(ptr(s.mats), ptr(s.coef), ptr(s.job), n, s.count, None, None, None, 2 * s.count,
+                        None, None, None, s.count, ctypes.byref(oc), ctypes.byref(ec), None)
+    assert rc == P.sperm.ERR_ARG and oc.value == need
+    torch.cuda.synchronize()
+
+
 def test_expand_random_signed_identical():
     """Row and column pivots, s = 1..4, zero-line children, s >= 5 early nodes."""
     rng = np.random.default_rng(77)
