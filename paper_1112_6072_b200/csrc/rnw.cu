@@ -37,6 +37,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -70,8 +71,9 @@ constexpr int kNumPlans = 13;
 // resident 256-thread CTAs per SM a tree kernel is compiled for: 3 (<= 85 registers, 24 warps to
 // hide the fixed-latency multiply chains of short blocks) where ptxas fits it without spilling
 // (-Xptxas -v over all plans and NFIX), else 2
-__host__ __device__ constexpr int tree_min_blocks(int B, int nfix) {
-  return (B <= 5 && 3 * B + nfix <= 24) || (B <= 3 && nfix <= 24) || (B <= 2 && nfix <= 32) ? 3 : 2;
+__host__ __device__ constexpr int tree_min_blocks(int B, int nfix, int gf) {
+  return gf == 4 ? ((B <= 4 && 3 * B + nfix <= 24) || (B == 5 && nfix <= 4) || (B <= 3 && nfix <= 16) ? 3 : 2)
+                 : (3 * B + nfix <= 20 ? 3 : 2);
 }
 constexpr int kMaxLow = 8;  // low columns picked per leaf
 
@@ -584,7 +586,7 @@ __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
 }
 
 template <int NFIX, int PLAN>
-__global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFIX)) rnw_tree_kernel(
+__global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFIX, plan_gf(PLAN))) rnw_tree_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
     uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
@@ -667,67 +669,81 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     for (int q = 0; q < SPERM_KMAX; ++q) acc[q] = 0;
     const uint64_t O0 = t0 >> B;
     const uint32_t nblk = 1u << (m - B);
-    for (uint32_t ob = 0; ob < nblk; ++ob) {
-      if (ob) {  // flip high Gray bit B + hh (warp-uniform column)
-        const int hh = __ffs(ob) - 1;
-        const bool add = !(((O0 + ob) >> (hh + 1)) & 1ull);
-        const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
+    // the block loop, instantiated for the leaf's prime count K = 1, 2, 3 (straight-line prime
+    // loops) and for K = SPERM_KMAX with a runtime bound; the E mode is tested once per block.
+    // (measured: configs[1] kernel 0.235 -> 0.186 ms/step, order-15 leaves 34 -> 26 ms / 4M)
+    auto blocks = [&](auto kc) {
+      constexpr int K = decltype(kc)::value;
+      for (uint32_t ob = 0; ob < nblk; ++ob) {
+        if (ob) {  // flip high Gray bit B + hh (warp-uniform column)
+          const int hh = __ffs(ob) - 1;
+          const bool add = !(((O0 + ob) >> (hh + 1)) & 1ull);
+          const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
 #pragma unroll
-        for (int v = 0; v < S4 / 4; ++v) {
-          const int4 d = col[v];
-          W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
-        }
-      }
-      // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1); exact products of
-      // pairs and quads of the E_c (used when the leaf's E mode says they fit int32; wrapped
-      // otherwise and then unused)
-      constexpr int NP2 = (B + 1) / 2, NP4 = (B + 3) / 4;
-      int32_t E[B], P2[NP2], P4[NP4];
-#pragma unroll
-      for (int c = 0; c < B; ++c) {
-        int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
-#pragma unroll
-        for (int s = 1; s < KS; ++s) {
-          x0 *= W[c * KS + s];
-          x1 *= W[c * KS + s] + D[c * KS + s];
-        }
-        E[c] = x0 - x1;
-      }
-#pragma unroll
-      for (int j = 0; j < NP2; ++j)
-        P2[j] = 2 * j + 1 < B ? (int32_t)((uint32_t)E[2 * j] * (uint32_t)E[2 * j + 1]) : E[2 * j];
-#pragma unroll
-      for (int j = 0; j < NP4; ++j)
-        P4[j] = 2 * j + 1 < NP2 ? (int32_t)((uint32_t)P2[2 * j] * (uint32_t)P2[2 * j + 1]) : P2[2 * j];
-      int32_t FG[NGF];
-#pragma unroll
-      for (int g = 0; g < NGF; ++g) {
-        int32_t x = W[NS + g * GF];
-#pragma unroll
-        for (int r = 1; r < GF; ++r) x *= W[NS + g * GF + r];
-        FG[g] = x;
-      }
-      const bool neg = (O0 + ob) & 1ull;  // (-1)^{|high Gray bits|}
-#pragma unroll
-      for (int q = 0; q < SPERM_KMAX; ++q) {
-        if (q < k) {
-          const int32_t p = prime_p(q), pinv = prime_pinv(q);
-          int32_t v = FG[0];
-#pragma unroll
-          for (int g = 1; g < NGF; ++g) v = smont(v, FG[g], p, pinv);
-          if (emode == 2) {  // warp-uniform: per-leaf mode
-#pragma unroll
-            for (int j = 0; j < NP4; ++j) v = smont(v, P4[j], p, pinv);
-          } else if (emode == 1) {
-#pragma unroll
-            for (int j = 0; j < NP2; ++j) v = smont(v, P2[j], p, pinv);
-          } else {
-#pragma unroll
-            for (int c = 0; c < B; ++c) v = smont(v, E[c], p, pinv);
+          for (int v = 0; v < S4 / 4; ++v) {
+            const int4 d = col[v];
+            W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
           }
-          acc[q] += neg ? -(int64_t)v : (int64_t)v;
         }
+        // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1); exact products
+        // of pairs and quads of the E_c (used when the leaf's E mode says they fit int32;
+        // wrapped otherwise and then unused)
+        constexpr int NP2 = (B + 1) / 2, NP4 = (B + 3) / 4;
+        int32_t E[B], P2[NP2], P4[NP4];
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+          int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
+#pragma unroll
+          for (int s = 1; s < KS; ++s) {
+            x0 *= W[c * KS + s];
+            x1 *= W[c * KS + s] + D[c * KS + s];
+          }
+          E[c] = x0 - x1;
+        }
+#pragma unroll
+        for (int j = 0; j < NP2; ++j)
+          P2[j] = 2 * j + 1 < B ? (int32_t)((uint32_t)E[2 * j] * (uint32_t)E[2 * j + 1]) : E[2 * j];
+#pragma unroll
+        for (int j = 0; j < NP4; ++j)
+          P4[j] = 2 * j + 1 < NP2 ? (int32_t)((uint32_t)P2[2 * j] * (uint32_t)P2[2 * j + 1]) : P2[2 * j];
+        int32_t FG[NGF];
+#pragma unroll
+        for (int g = 0; g < NGF; ++g) {
+          int32_t x = W[NS + g * GF];
+#pragma unroll
+          for (int r = 1; r < GF; ++r) x *= W[NS + g * GF + r];
+          FG[g] = x;
+        }
+        const bool neg = (O0 + ob) & 1ull;  // (-1)^{|high Gray bits|}
+        // per prime: P_F's chain, then the exact E groups of the leaf's mode
+        auto chain = [&](auto gsz, const int32_t* grp) {
+          constexpr int NGR = decltype(gsz)::value;
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            if (K == SPERM_KMAX && q >= k) break;
+            const int32_t p = prime_p(q), pinv = prime_pinv(q);
+            int32_t v = FG[0];
+#pragma unroll
+            for (int g = 1; g < NGF; ++g) v = smont(v, FG[g], p, pinv);
+#pragma unroll
+            for (int j = 0; j < NGR; ++j) v = smont(v, grp[j], p, pinv);
+            acc[q] += neg ? -(int64_t)v : (int64_t)v;
+          }
+        };
+        if (emode == 2) chain(std::integral_constant<int, NP4>{}, P4);  // warp-uniform per leaf
+        else if (emode == 1) chain(std::integral_constant<int, NP2>{}, P2);
+        else chain(std::integral_constant<int, B>{}, E);
       }
+    };
+    if constexpr (NRT <= 40) {
+      switch (k) {
+        case 1: blocks(std::integral_constant<int, 1>{}); break;
+        case 2: blocks(std::integral_constant<int, 2>{}); break;
+        case 3: blocks(std::integral_constant<int, 3>{}); break;
+        default: blocks(std::integral_constant<int, SPERM_KMAX>{}); break;
+      }
+    } else {  // many register-resident rows: one copy of the loop (no spills)
+      blocks(std::integral_constant<int, SPERM_KMAX>{});
     }
 #pragma unroll
     for (int q = 0; q < SPERM_KMAX; ++q) {
