@@ -119,6 +119,17 @@ __global__ void breg_init_kernel() {
 // then the tree plan: 32 lanes run the greedy disjoint-support column pick from 32
 // rotations of the start column, the best (lowest lane on ties) wins; the first plan whose
 // exact-arithmetic bounds hold is taken.
+// row/column masks of a leaf: 32-bit words for n <= 32, 64-bit for n <= 48
+__device__ __forceinline__ int mpop(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int mpop(unsigned long long x) { return __popcll(x); }
+__device__ __forceinline__ int mffs(uint32_t x) { return __ffs((int)x); }
+__device__ __forceinline__ int mffs(unsigned long long x) { return __ffsll((long long)x); }
+template <typename M>
+__device__ __forceinline__ M mask_below(int n) {  // bits 0..n-1
+  return n >= (int)(8 * sizeof(M)) ? ~M(0) : (M(1) << n) - 1;
+}
+
+template <typename M>
 __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
                                 const int64_t* __restrict__ coef, int min_primes, int max_primes, int allow_tree,
                                 int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err) {
@@ -156,17 +167,17 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   }
   const int32_t* a = sa;
   __shared__ int64_t sR[8][SPERM_NMAX];
-  __shared__ unsigned long long sSupp[8][SPERM_NMAX];
+  __shared__ M sSupp[8][SPERM_NMAX];
   __shared__ int sCnt[8][SPERM_NMAX];
   __shared__ int sBl[8][SPERM_NMAX];  // bit length of each row bound: R_i < 2^bl_i
   int64_t* R = sR[wib];
-  unsigned long long* supp = sSupp[wib];
+  M* supp = sSupp[wib];
   int* cnt = sCnt[wib];
   double lr = 0.0, lc = 0.0, br = 0.0, bc = 0.0;  // log2 of row/col sum bounds, Bregman-Minc
   bool zero = false, range_bad = false, binary = true;
   for (int i = lane; i < n; i += 32) {
     int64_t r = 0, c = 0;
-    unsigned long long sm = 0;
+    M sm = 0;
     int nz = 0;
     for (int j = 0; j < n; ++j) {
       const int32_t u = a[i * ns + j];
@@ -174,7 +185,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (u != 0 && u != 1) binary = false;
       const int32_t v = a[j * ns + i];
       c += llabs((long long)v);
-      if (v != 0) { sm |= 1ull << j; ++nz; }
+      if (v != 0) { sm |= M(1) << j; ++nz; }
     }
     R[i] = r;
     sBl[wib][i] = r ? 64 - __clzll(r) : 0;
@@ -213,19 +224,19 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   unsigned long long packed = 0;
   int np = 0;
   if (allow_tree && n >= 8 && !range_bad) {
-    unsigned long long used = 0;
+    M used = 0;
     const int l0 = lane % n;
-    const unsigned long long nmask = (1ull << n) - 1;  // n <= 48
+    const M nmask = mask_below<M>(n);
     for (int lvl = 1; lvl <= KS; ++lvl) {
       // columns with exactly lvl nonzeros, visited in the lane's rotated order l0, l0+1, ...
-      unsigned long long m = 0;
+      M m = 0;
       for (int c0 = 0; c0 < n; c0 += 32) {
         const int j = c0 + lane;
-        m |= (unsigned long long)__ballot_sync(0xffffffffu, j < n && cnt[j] == lvl) << c0;
+        m |= (M)__ballot_sync(0xffffffffu, j < n && cnt[j] == lvl) << c0;
       }
-      unsigned long long rot = l0 ? ((m >> l0) | (m << (n - l0))) & nmask : m;
+      M rot = l0 ? ((m >> l0) | (m << (n - l0))) & nmask : m;
       while (rot) {
-        int j = __ffsll((long long)rot) - 1 + l0;
+        int j = mffs(rot) - 1 + l0;
         rot &= rot - 1;
         j -= j >= n ? n : 0;
         if (!(supp[j] & used) && np < kMaxLow && np < n - 2) {
@@ -251,11 +262,11 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     const int64_t p = x * y;
     return p > ((int64_t)1 << 40) ? ((int64_t)1 << 40) : p;
   };
-  unsigned long long my_supp = 0;
+  M my_supp = 0;
   int64_t my_q = 1;
   if (lane < np) {
     my_supp = supp[(packed >> (8 * lane)) & 0xff];
-    for (unsigned long long b = my_supp; b; b &= b - 1) my_q = sat_mul(my_q, R[__ffsll((long long)b) - 1]);
+    for (M b = my_supp; b; b &= b - 1) my_q = sat_mul(my_q, R[mffs(b) - 1]);
   }
 
   // ---- number of primes (lane 0)
@@ -281,7 +292,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   bool feasible = false;
   int fi = 0, pmexp = 0;
   int emode = 0;  // exact E groups: 0 singles, 1 pairs, 2 quads
-  unsigned long long slot_rows = 0;
+  M slot_rows = 0;
   {
     const bool test = pl >= allow_tree && allow_tree >= 1 && pl < kNumPlans && np > 0;
     const int B = plan_b(pl), GF = plan_gf(pl);
@@ -294,7 +305,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
 #pragma unroll
     for (int c = 0; c < kMaxLow; ++c) {  // warp-uniform shuffles, per-lane plan bounds
       const int64_t q = __shfl_sync(0xffffffffu, my_q, c);
-      const unsigned long long sc = __shfl_sync(0xffffffffu, my_supp, c);
+      const M sc = __shfl_sync(0xffffffffu, my_supp, c);
       if (c < B) {
         slot_rows |= sc;
         if (q >= ((int64_t)1 << 30)) qok = false;
@@ -309,7 +320,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     const int ngroups = emode == 2 ? (B + 3) / 4 : emode == 1 ? (B + 1) / 2 : B;
     if (test && np >= B && n - 6 >= B) {
       bool ok = qok;
-      const int nf = n - __popcll(slot_rows);
+      const int nf = n - mpop(slot_rows);
       while (fi < kNumNFix && nfix_of(fi) < nf) ++fi;
       if (fi == kNumNFix) ok = false;
       // every exact group of GF consecutive fixed rows: prod R_i < 2^(sum bl_i) <= 2^30
@@ -317,7 +328,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       const int* bl = sBl[wib];
       int pos = 0, bits = 0;
       for (int i = 0; i < n; ++i) {
-        if ((slot_rows >> i) & 1ull) continue;
+        if ((slot_rows >> i) & 1) continue;
         bits += bl[i];
         if ((++pos & (GF - 1)) == 0) {
           if (bits > 30) ok = false;
@@ -342,35 +353,35 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     // columns, high columns ascending, nw]
     int8_t* pr = perm + leaf * kPermW;
     int8_t* pc = pr + kPermRows;
-    const unsigned long long nmask = n == 64 ? ~0ull : ((1ull << n) - 1);
-    const unsigned long long fixed = ~slot_rows & nmask;
-    unsigned long long low = 0;
-    for (int c = 0; c < B; ++c) low |= 1ull << ((packed >> (8 * c)) & 0xff);
+    const M nmask = mask_below<M>(n);
+    const M fixed = ~slot_rows & nmask;
+    M low = 0;
+    for (int c = 0; c < B; ++c) low |= M(1) << ((packed >> (8 * c)) & 0xff);
     // nw column: the non-low column with most nonzeros (highest index on ties)
     int nwkey = -1;
     for (int j = lane; j < n; j += 32)
-      if (!((low >> j) & 1ull)) nwkey = max(nwkey, (cnt[j] << 8) | j);
+      if (!((low >> j) & 1)) nwkey = max(nwkey, (cnt[j] << 8) | j);
     for (int o = 16; o; o >>= 1) nwkey = max(nwkey, __shfl_xor_sync(0xffffffffu, nwkey, o));
     const int nw = nwkey & 0xff;
-    const unsigned long long high = nmask & ~low & ~(1ull << nw);
+    const M high = nmask & ~low & ~(M(1) << nw);
     for (int i = lane; i < n; i += 32) {
-      const unsigned long long below = (1ull << i) - 1;
-      if ((fixed >> i) & 1ull) {
-        pr[B * KS + __popcll(fixed & below)] = (int8_t)i;
+      const M below = (M(1) << i) - 1;
+      if ((fixed >> i) & 1) {
+        pr[B * KS + mpop(fixed & below)] = (int8_t)i;
       } else {
         for (int c = 0; c < B; ++c) {
-          const unsigned long long sc = supp[(packed >> (8 * c)) & 0xff];
-          if ((sc >> i) & 1ull) pr[c * KS + __popcll(sc & below)] = (int8_t)i;
+          const M sc = supp[(packed >> (8 * c)) & 0xff];
+          if ((sc >> i) & 1) pr[c * KS + mpop(sc & below)] = (int8_t)i;
         }
       }
-      if ((high >> i) & 1ull) pc[B + __popcll(high & below)] = (int8_t)i;
+      if ((high >> i) & 1) pc[B + mpop(high & below)] = (int8_t)i;
     }
     if (lane < B) {
       const int j = (packed >> (8 * lane)) & 0xff;
       pc[lane] = (int8_t)j;
-      for (int s = __popcll(supp[j]); s < KS; ++s) pr[lane * KS + s] = -1;
+      for (int s = mpop(supp[j]); s < KS; ++s) pr[lane * KS + s] = -1;
     }
-    for (int f = n - __popcll(slot_rows) + lane; f < NF; f += 32) pr[B * KS + f] = -1;
+    for (int f = n - mpop(slot_rows) + lane; f < NF; f += 32) pr[B * KS + f] = -1;
     if (lane == 0) pc[n - 1] = (int8_t)nw;
     if (lane == win) {
       pr[kPermGend] = (int8_t)emode;  // this lane tested the winning plan
@@ -1202,8 +1213,9 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     const int64_t threads = count * 32;
     count_launch();
     const size_t prep_smem = (size_t)8 * n * (n + 1) * sizeof(int32_t);  // padded rows, 8 warps
-    SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
-    rnw_prep_kernel<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
+    auto prep = n <= 32 ? rnw_prep_kernel<uint32_t> : rnw_prep_kernel<unsigned long long>;
+    SPERM_TRY(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
+    prep<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
     count_launch();
