@@ -13,6 +13,7 @@
 //   row pivot r, cofactor at p:     delete row r, column p;   coef *= a_rp
 //   column pivot c (= row pivot of A^T, reading R2): the same with rows and columns exchanged.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 
@@ -451,7 +452,17 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   const int per_lane = (n * n + 31) / 32;
   auto kern = per_lane <= 4 ? expand_level_kernel<4> : per_lane <= 8 ? expand_level_kernel<8>
             : per_lane <= 12 ? expand_level_kernel<12> : expand_level_kernel<16>;
-  SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+  {  // the attribute once per device and kernel, at the 200 KB staging budget (host time per level)
+    static std::atomic<unsigned> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned bit = 1u << (dev & 31);
+    if (!(attr_done.load() & bit)) {
+      for (auto k : {expand_level_kernel<4>, expand_level_kernel<8>, expand_level_kernel<12>, expand_level_kernel<16>})
+        SPERM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_done.fetch_or(bit);
+    }
+  }
   {
     TimingScope ts("expand", st);
     count_launch();

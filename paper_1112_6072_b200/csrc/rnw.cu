@@ -34,9 +34,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <type_traits>
 #include <vector>
 
@@ -860,25 +863,29 @@ __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order
     keys[i] = (uint8_t)key;
     ids[i] = leaf;
   }
-  // block histogram in shared memory, then one global atomic per nonzero bin
-  __shared__ int s_h[kNumKeys], s_hk[kNumKeys];
-  __shared__ unsigned long long s_hx[kNumKeys];
-  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
-    s_h[t] = s_hk[t] = 0;
-    s_hx[t] = 0ull;
-  }
+  // block histogram in shared memory (32-bit: <= 256 leaves x 8 x 47 per bin), warp-aggregated
+  // per key (leaves mostly share a few keys), then one global atomic per nonzero bin
+  __shared__ int s_h[kNumKeys], s_hk[kNumKeys], s_hx[kNumKeys];
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) s_h[t] = s_hk[t] = s_hx[t] = 0;
   __syncthreads();
-  if (i < count) {
-    atomicAdd(&s_h[key], 1);
-    atomicAdd(&s_hk[key], meta_k(mt));
-    atomicAdd(&s_hx[key], (unsigned long long)(meta_k(mt) * mt.y));
+  {
+    const bool live = i < count;
+    const unsigned same = __match_any_sync(0xffffffffu, live ? key : -1);
+    const int kk = live ? meta_k(mt) : 0;
+    const int c1 = __popc(same), ck = __reduce_add_sync(same, (unsigned)kk),
+              cx = __reduce_add_sync(same, (unsigned)(kk * mt.y));
+    if (live && (threadIdx.x & 31) == __ffs(same) - 1) {
+      atomicAdd(&s_h[key], c1);
+      atomicAdd(&s_hk[key], ck);
+      atomicAdd(&s_hx[key], cx);
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x)
     if (s_h[t]) {
       atomicAdd(hist + t, s_h[t]);
       atomicAdd(hist_k + t, s_hk[t]);
-      atomicAdd(hist_kx + t, s_hx[t]);
+      atomicAdd(hist_kx + t, (unsigned long long)s_hx[t]);
     }
 }
 
@@ -947,9 +954,30 @@ int choose_m(int n, int64_t nleaves, int mmin) {
 
 template <typename K>
 int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bool tree) {
-  SPERM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // attribute + occupancy query cached per (kernel, shared-memory size, device): host time per call
+  // (the dynamic shared-memory attribute only ever grows: the largest size requested so far)
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int>, int> cache;
+  static std::map<std::pair<const void*, int>, size_t> attr_max;
+  int dev = 0;
+  cudaGetDevice(&dev);
   int per_sm = 0;
-  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRnwThreads, smem));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& amax = attr_max[std::make_pair((const void*)kernel, dev)];
+    if (smem > amax) {
+      SPERM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      amax = smem;
+    }
+    const auto key = std::make_tuple((const void*)kernel, smem, dev);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRnwThreads, smem));
+      cache[key] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
   if (per_sm < 1) return set_error(SPERM_ERR_ARG, "sperm_permanent: kernel does not fit on an SM");
   uint64_t grid = (uint64_t)sm_count() * per_sm;
   const uint64_t blocks_needed = (total + kRnwThreads / 32 - 1) / (kRnwThreads / 32);
@@ -1214,7 +1242,19 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     count_launch();
     const size_t prep_smem = (size_t)8 * n * (n + 1) * sizeof(int32_t);  // padded rows, 8 warps
     auto prep = n <= 32 ? rnw_prep_kernel<uint32_t> : rnw_prep_kernel<unsigned long long>;
-    SPERM_TRY(cudaFuncSetAttribute(prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)prep_smem));
+    {  // the attribute once per device, for the largest order (host time per call)
+      static std::atomic<unsigned> prep_attr{0};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const unsigned bit = 1u << (dev & 31);
+      if (!(prep_attr.load() & bit)) {
+        const int max_smem = 8 * SPERM_NMAX * (SPERM_NMAX + 1) * (int)sizeof(int32_t);
+        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       max_smem));
+        prep_attr.fetch_or(bit);
+      }
+    }
     prep<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
@@ -1222,15 +1262,34 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist, hist + kNumKeys, hist_kx);
     SPERM_TRY(cudaGetLastError());
   }
+  // leaves grouped by plan key, evaluation order kept inside each group (stable radix sort on
+  // the 7-bit keys), queued before the histogram read-back so that the host's only work after
+  // the synchronization is launching the plan groups
+  const int32_t* sorted = ids + count;
+  {
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 7, st);
+    SPERM_TRY(cudaMallocAsync(&sort_tmp, tmp_bytes, st));
+    SPERM_TRY(cub::DeviceRadixSort::SortPairs(sort_tmp, tmp_bytes, keys, keys + count, ids, ids + count,
+                                              (int)count, 0, 7, st));
+  }
+  // one read-back of the whole small block (err, histograms, queues, kx) into a per-thread
+  // pinned buffer (a pageable copy is staged and slower)
+  thread_local void* h_small_pinned = nullptr;
+  if (!h_small_pinned) SPERM_TRY(cudaMallocHost(&h_small_pinned, small_bytes));
+  SPERM_TRY(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, st));
+  SPERM_TRY(cudaStreamSynchronize(st));
   int hsmall[4 + 2 * kNumKeys];
   unsigned long long h_kx[kNumKeys];
-  SPERM_TRY(cudaMemcpyAsync(hsmall, small, sizeof(hsmall), cudaMemcpyDeviceToHost, st));
-  SPERM_TRY(cudaMemcpyAsync(h_kx, hist_kx, sizeof(h_kx), cudaMemcpyDeviceToHost, st));
-  SPERM_TRY(cudaStreamSynchronize(st));
+  memcpy(hsmall, h_small_pinned, sizeof(hsmall));
+  memcpy(h_kx, static_cast<const char*>(h_small_pinned) + sizeof(int) * (4 + 2 * kNumKeys) +
+                   sizeof(unsigned long long) * kNumKeys,
+         sizeof(h_kx));
   if (hsmall[2] & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
   if (hsmall[2] & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
   const int* h_hist = hsmall + 4;
-  if (getenv("SPERM_DEBUG")) {  // plan histogram of this call (diagnostics)
+  static const bool debug = getenv("SPERM_DEBUG") != nullptr;
+  if (debug) {  // plan histogram of this call (diagnostics)
     fprintf(stderr, "[sperm] permanent n=%d count=%lld:", n, (long long)count);
     for (int key = 0; key < kNumKeys; ++key)
       if (h_hist[key])
@@ -1244,16 +1303,6 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   }
   int nonzero_keys = 0;
   for (int q = 0; q < kNumKeys; ++q) nonzero_keys += h_hist[q] > 0;
-  // leaves grouped by plan key, evaluation order kept inside each group (stable sort)
-  const int32_t* sorted = ids;
-  if (nonzero_keys > 1) {
-    size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 7, st);
-    SPERM_TRY(cudaMallocAsync(&sort_tmp, tmp_bytes, st));
-    SPERM_TRY(cub::DeviceRadixSort::SortPairs(sort_tmp, tmp_bytes, keys, keys + count, ids, ids + count,
-                                              (int)count, 0, 7, st));
-    sorted = ids + count;
-  }
   int rc = SPERM_OK;
   if (n > 0) {
     // One persistent launch per plan group, each on its own stream of a small pool forked

@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="c100", choices=["c100", "c60", "fullerene96"])
+    ap.add_argument("--workload", default="c100", choices=["c100", "c60", "fullerene96", "configs1"])
     ap.add_argument("--jobs", type=int, default=159)
     ap.add_argument("--leaf", type=int, default=16)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.json"))
@@ -29,13 +29,30 @@ def main():
     from workloads import dodecahedron, paper_graph, random_fullerene
     if args.workload == "fullerene96":
         a, _ = random_fullerene(96, 2024, 0)
+    elif args.workload == "configs1":
+        a = None
     else:
         a = paper_graph("C100" if args.workload == "c100" else "C60")
     pipeline.permanent(dodecahedron(), jobs_at_least=8, leaf_order=12)
     torch.cuda.synchronize()
+    if args.workload == "configs1":  # the bench step: one sperm_permanent over 256 n=24 matrices, x10
+        import paper_1112_6072_b200 as P
+        from workloads import random_3perm_batch
+        mats = torch.tensor(random_3perm_batch(256, 24, 2024), dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            P.sperm_permanent(mats, min_primes=1)
+        torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         t0 = time.perf_counter()
-        r = pipeline.permanent(a, jobs_at_least=args.jobs, leaf_order=args.leaf)
+        if args.workload == "configs1":
+            for _ in range(10):
+                res, k = P.sperm_permanent(mats, min_primes=1)
+
+            class _R:
+                value = "configs1 x10"
+            r = _R()
+        else:
+            r = pipeline.permanent(a, jobs_at_least=args.jobs, leaf_order=args.leaf)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     ev = []
