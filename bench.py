@@ -201,7 +201,8 @@ def main():
                      "frac": (achieved / peak_ops) if peak_ops else None,
                      # dram__bytes_read.sum + dram__bytes_write.sum of the step's four R-NW launches
                      # (ncu --set full, profiles/r01_final_ncu.txt): the kernel is not memory bound
-                     "traffic": 816128, "traffic_note": "bytes per step, ncu capture (profiles/r01_final_ncu.txt)",
+                     "traffic": 832000, "traffic_note": "dram read+write bytes of the step's three R-NW launches, "
+                                                         "ncu --set full (profiles/r01_v8_rnw_tree_ncu.txt)",
                      "kernel": "rnw_tree_kernel / rnw_generic_kernel (all R-NW launches of the step)",
                      "kernel_ms_per_step": rnw_avg_s * 1e3, "launches_per_step": rnw_launches / max(args.steps, 1),
                      "kernel_share_of_step": (rnw_ms / args.steps) / (total_ms / args.steps),
