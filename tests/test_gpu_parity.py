@@ -338,6 +338,22 @@ def test_rnw_tree_plans_signed_sparse():
         _plans_agree(a[None], [h_per(a)])
 
 
+@pytest.mark.parametrize("wmax", [60, 2000])
+def test_rnw_many_primes_every_plan(wmax):
+    """Heavy weights need k = 4..8 primes: the tree kernel's generic-K block loop (k > 3) and the
+    generic kernel, with every tree plan forced in turn, against the oracle."""
+    rng = np.random.default_rng(wmax)
+    mats = []
+    for _ in range(6):
+        n = int(rng.integers(16, 23))
+        a = random_3perm(n, rng) * rng.integers(1, wmax + 1, size=(n, n))
+        mats.append(a)
+    for a in mats:
+        res, k = P.sperm_permanent(dev(a[None]))
+        assert int(k[0]) >= 4
+        _plans_agree(a[None], [h_per(a)])
+
+
 def test_rnw_prime_count_bregman_and_cap():
     """0/1 leaves size their prime count by Bregman-Minc (configs[1] 0/1 half: 1 prime);
     max_primes caps it, leaving every residue correct modulo the primes kept."""
