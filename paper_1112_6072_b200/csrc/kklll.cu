@@ -118,6 +118,7 @@ __global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int6
         const int i = k + 1 + e / w, j = k + 1 + (e - (e / w) * w);
         const double lr = re[i * n + k], li = im[i * n + k];
         const double ur = re[k * n + j], ui = im[k * n + j];
+        if ((ur == 0.0 && ui == 0.0) || (lr == 0.0 && li == 0.0)) continue;  // see kk_update
         re[i * n + j] = __dsub_rn(re[i * n + j], __dsub_rn(__dmul_rn(lr, ur), __dmul_rn(li, ui)));
         im[i * n + j] = __dsub_rn(im[i * n + j], __dadd_rn(__dmul_rn(lr, ui), __dmul_rn(li, ur)));
       }
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
         for (int j = 1; j < NC; ++j) {  // j > k (static trip count keeps re/im in registers)
           if (j <= k) continue;
           const double2 u = prow[j];
+          if (u.x == 0.0 && u.y == 0.0) continue;  // sparse pivot row: see kk_update
           re[j] = __dsub_rn(re[j], __dsub_rn(__dmul_rn(lr, u.x), __dmul_rn(li, u.y)));
           im[j] = __dsub_rn(im[j], __dadd_rn(__dmul_rn(lr, u.y), __dmul_rn(li, u.x)));
         }
@@ -301,6 +303,10 @@ __device__ __forceinline__ void kk_update(double (&cr)[RL], double (&ci)[RL], co
     if (ra == pa) { ur = cr[ra]; ui = ci[ra]; }
   ur = __shfl_sync(0xffffffffu, ur, plane);
   ui = __shfl_sync(0xffffffffu, ui, plane);
+  // u = 0 (the pivot row is sparse until fill-in): every b_ij - l_i * 0 is b_ij up to the sign
+  // of a zero, and a zero's sign never reaches a pivot magnitude |b|^2, a nonzero sum or the
+  // product of the d_k — so X is bit-identical with the update skipped (warp-uniform branch)
+  if (ur == 0.0 && ui == 0.0) return;
 #pragma unroll
   for (int ra = 0; ra < RL; ++ra) {
     if (act[ra]) {
