@@ -10,6 +10,7 @@
 //           div_by; K2), so the value equals the reference evaluation bit for bit.
 // The estimate is the trial-order sum of X divided by N (K3).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -412,6 +413,116 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
   }
 }
 
+// Shared-memory-resident variant for 32 < n <= 112: one 128-thread CTA per trial, B row-major
+// in shared memory (16-byte complex entries), several trials (CTAs) per SM so one trial's
+// pivot search and barriers overlap the others' updates.  Per elimination step: warp 0 finds the
+// pivot (first maximal |b_ik|^2 over rows k..n-1, the oracle's rule on physically swapped rows),
+// the rows k and p are swapped (columns >= k: earlier columns hold spent multipliers), the
+// multipliers l_i go to a shared vector (one reciprocal per step + Markstein, div_by), and
+// the m x m trailing block is updated by all threads (thread = (row group, column): contiguous
+// 16-byte accesses, the multiplier a broadcast).  Same operations in the same order as the
+// oracle on every entry, so X is bit-identical; updates by a zero pivot-row entry are skipped
+// (see kk_update).
+constexpr int kKsThreads = 128;
+__global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+                                                                const int32_t* __restrict__ ids, int trials,
+                                                                uint64_t seed, double* __restrict__ xout) {
+  extern __shared__ double2 ksm2[];  // b[n][ns] (row stride ns = n | 1: column scans conflict-free) | lv[n]
+  const int ns = n | 1;
+  double2* b = ksm2;
+  double2* lv = ksm2 + n * ns;
+  __shared__ double s_d;
+  __shared__ int s_p;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const double S32 = 0.8660254037844386;
+  const int64_t items = count * (int64_t)trials;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t job = item / trials;
+    const int trial = (int)(item % trials);
+    const int32_t* a = mats + job * (int64_t)n * n;
+    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
+    __syncthreads();  // the previous trial is done with b
+    for (int e = t; e < n * n; e += kKsThreads) {
+      const int i = e / n, j = e - (e / n) * n;
+      double r = 0.0, s = 0.0;
+      if (a[e] != 0) {
+        const int ri = root_index(key, (uint64_t)i, (uint64_t)j);
+        r = ri == 0 ? 1.0 : -0.5;
+        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
+      }
+      b[i * ns + j] = make_double2(r, s);
+    }
+    __syncthreads();
+    double x = 1.0;
+    for (int k = 0; k < n; ++k) {
+      if (w == 0) {
+        // pivot: first row i >= k with maximal re^2 + im^2 (ascending per lane, strict >)
+        double bm = -1.0;
+        int bi = n;
+        for (int i = k + lane; i < n; i += 32) {
+          const double2 v = b[i * ns + k];
+          const double m = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+          if (m > bm) { bm = m; bi = i; }
+        }
+        for (int o = 16; o; o >>= 1) {
+          const double om = __shfl_xor_sync(0xffffffffu, bm, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (om > bm || (om == bm && oi < bi)) { bm = om; bi = oi; }
+        }
+        if (lane == 0) {
+          s_d = bm;
+          s_p = bi;
+        }
+      }
+      __syncthreads();
+      const double d = s_d;
+      const int p = s_p;
+      if (d == 0.0) { x = 0.0; break; }  // CTA-uniform
+      x = __dmul_rn(x, d);
+      if (k + 1 == n) break;
+      if (p != k)
+        for (int j = k + t; j < n; j += kKsThreads) {
+          const double2 u = b[k * ns + j];
+          b[k * ns + j] = b[p * ns + j];
+          b[p * ns + j] = u;
+        }
+      __syncthreads();
+      {
+        const double2 pk = b[k * ns + k];
+        const double y = __drcp_rn(d);
+        const bool d_ok = div_range_ok(d);
+        for (int i = k + 1 + t; i < n; i += kKsThreads) {
+          const double2 v = b[i * ns + k];
+          lv[i] = make_double2(div_by(__dadd_rn(__dmul_rn(v.x, pk.x), __dmul_rn(v.y, pk.y)), d, y, d_ok),
+                               div_by(__dsub_rn(__dmul_rn(v.y, pk.x), __dmul_rn(v.x, pk.y)), d, y, d_ok));
+        }
+      }
+      __syncthreads();
+      {
+        // trailing m x m block: thread t -> column j = k+1 + t % m, rows k+1 + t / m + G * r
+        const int m = n - k - 1;
+        const int G = m >= kKsThreads ? 1 : kKsThreads / m;
+        const int g = t / m, j = k + 1 + (t - g * m);
+        if (g < G && j < n) {
+          const double2 u = b[k * ns + j];
+          if (u.x != 0.0 || u.y != 0.0) {
+#pragma unroll 4
+            for (int i = k + 1 + g; i < n; i += G) {
+              const double2 l = lv[i];
+              double2 v = b[i * ns + j];
+              v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
+              v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
+              b[i * ns + j] = v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (t == 0) xout[item] = x;
+  }
+}
+
 __global__ void kklll_mean_kernel(const double* __restrict__ xs, int64_t count, int trials,
                                   double* __restrict__ est) {
   const int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -450,8 +561,20 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     TimingScope ts("kklll", st);
     count_launch();
     kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+  } else if (!getenv("SPERM_KKLLL_CTA")) {
+    // shared-memory-resident LU, one 128-thread CTA per trial, as many trials per SM as fit
+    const size_t smem = sizeof(double2) * ((size_t)n * (n | 1) + n);
+    SPERM_CUDA(cudaFuncSetAttribute(kklll_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_smem_kernel, kKsThreads, smem));
+    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+    grid = std::max<int64_t>(1, std::min(grid, items));
+    TimingScope ts("kklll", st);
+    count_launch();
+    kklll_smem_kernel<<<(unsigned)grid, kKsThreads, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else if (n <= 96) {
-    // CTA-distributed registers: rows per lane RL = ceil(n/32), column slots per thread CS = ceil(n/8)
+    // A-B (SPERM_KKLLL_CTA=1): CTA-distributed registers: rows per lane RL = ceil(n/32), column
+    // slots per thread CS = ceil(n/8)
     const int CSn = (n + 7) / 8;
     auto kern = n <= 64 ? kklll_cta_kernel<2, 8> : CSn <= 9 ? kklll_cta_kernel<3, 9>
                                              : CSn <= 10 ? kklll_cta_kernel<3, 10> : kklll_cta_kernel<3, 12>;
