@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
   }
 }
 
-// Shared-memory-resident variant for 32 < n <= 112: one 128-thread CTA per trial, B row-major
+// Shared-memory-resident variant for 32 < n <= 112: one 256-thread CTA per trial, B row-major
 // in shared memory (16-byte complex entries), several trials (CTAs) per SM so one trial's
 // pivot search and barriers overlap the others' updates.  Per elimination step: warp 0 finds the
 // pivot (first maximal |b_ik|^2 over rows k..n-1, the oracle's rule on physically swapped rows),
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
 // 16-byte accesses, the multiplier a broadcast).  Same operations in the same order as the
 // oracle on every entry, so X is bit-identical; updates by a zero pivot-row entry are skipped
 // (see kk_update).
-constexpr int kKsThreads = 128;
+constexpr int kKsThreads = 256;
 __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
                                                                 const int32_t* __restrict__ ids, int trials,
                                                                 uint64_t seed, double* __restrict__ xout) {
@@ -562,7 +562,8 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     count_launch();
     kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else if (!getenv("SPERM_KKLLL_CTA")) {
-    // shared-memory-resident LU, one 128-thread CTA per trial, as many trials per SM as fit
+    // shared-memory-resident LU, one 256-thread CTA per trial, as many trials per SM as fit
+    // (measured on the fullerene-96 jobs: 128 threads 1.37 s, 256 1.31 s, 512 1.97 s)
     const size_t smem = sizeof(double2) * ((size_t)n * (n | 1) + n);
     SPERM_CUDA(cudaFuncSetAttribute(kklll_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
