@@ -550,7 +550,11 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
   double* xs = d_trials_out;
   if (!xs) SPERM_CUDA(cudaMallocAsync((void**)&xs, sizeof(double) * count * trials, st));
   const int64_t items = count * (int64_t)trials;
-  if (n <= 32) {
+  static const int smem_min = [] {  // A-B knob: smallest order for the shared-memory kernel
+    const char* e = getenv("SPERM_KKLLL_SMEM_MIN");  // measured crossover: n = 23 register kernel
+    return e ? atoi(e) : 28;                          // 76 vs 267 ms, 27: 170 vs 163, 32: 115 vs 80
+  }();
+  if (n <= 32 && n < smem_min) {
     const int NC = n <= 8 ? 8 : n <= 16 ? 16 : n <= 24 ? 24 : 32;
     auto kern = NC == 8 ? kklll_reg_kernel<8> : NC == 16 ? kklll_reg_kernel<16> : NC == 24 ? kklll_reg_kernel<24>
                                                                                           : kklll_reg_kernel<32>;

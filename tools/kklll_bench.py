@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="fullerene96", choices=["fullerene96", "c100"])
+    ap.add_argument("--workload", default="fullerene96", choices=["fullerene96", "c100", "c60", "c20"])
     ap.add_argument("--jobs", type=int, default=1000)
     ap.add_argument("--trials", type=int, default=0)
     ap.add_argument("--limit", type=int, default=0, help="estimate only the first LIMIT jobs of each order")
@@ -24,8 +24,10 @@ def main():
     import torch
     import paper_1112_6072_b200 as P
     from paper_1112_6072_b200 import pipeline
-    from workloads import paper_graph, random_fullerene
-    a = random_fullerene(96, 2024, 0)[0] if args.workload == "fullerene96" else paper_graph("C100")
+    from workloads import dodecahedron, paper_graph, random_fullerene, truncated_icosahedron
+    a = (random_fullerene(96, 2024, 0)[0] if args.workload == "fullerene96" else
+         truncated_icosahedron() if args.workload == "c60" else
+         dodecahedron() if args.workload == "c20" else paper_graph("C100"))
     sets = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=args.jobs)
     if args.limit:
         sets = [pipeline.NodeSet(s.n, s.mats[:args.limit], s.coef[:args.limit], s.job[:args.limit]) for s in sets]
