@@ -257,7 +257,7 @@ def bench_expand(P, torch, jobs_at_least: int = 200000, reps: int = 3):
     gbs = nbytes / (ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
             "frac": gbs / pk["hbm_gbs"] if pk.get("hbm_gbs") else None, "traffic": None,
-            "kernel": "expand_count_kernel + expand_emit_kernel", "level": {"n": s.n, "nodes": s.count},
+            "kernel": "expand_level_kernel (one pass per level)", "level": {"n": s.n, "nodes": s.count},
             "ms_per_level": ms / reps, "algorithmic_bytes_per_level": nbytes / reps,
             "peak_note": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy)"}
 

@@ -79,6 +79,10 @@ int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
  *   per(A) = (-1)^(n-1) 2^(1-n) sum_{t=0}^{2^(n-1)-1} (-1)^t prod_i w_i(g(t)),
  *   w_i(S) = 2 a_{i,n-1} - sum_j a_ij + 2 sum_{j in S} a_ij,   g(t) = t ^ (t>>1).
  *
+ * (Rows and columns may be renumbered first: per(A) is invariant.  The device sums each
+ * aligned block of 2^B Gray-code terms in closed form when B low columns have disjoint
+ * supports — the same exact sum.)
+ *
  *  d_mats     [count][n][n] int32 leaves (device), 0 <= n <= SPERM_NMAX.
  *  d_coef     [count] int64 leaf coefficients (device) or NULL (all 1): the
  *             leaf contributes coef * per(leaf) (the scalars Eq. (2),
