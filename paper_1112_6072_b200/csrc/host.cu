@@ -199,32 +199,50 @@ int sperm_crt_batch(const uint32_t* h_residues, int64_t count, int stride, const
   return SPERM_OK;
 }
 
+namespace {
+// inv[j][i] = p_j^-1 mod p_i (j < i), Fermat, computed once
+struct CrtTables {
+  uint64_t inv[SPERM_KMAX][SPERM_KMAX];
+  CrtTables() {
+    for (int i = 0; i < SPERM_KMAX; ++i)
+      for (int j = 0; j < SPERM_KMAX; ++j) {
+        const uint64_t p = kPrimes[i];
+        uint64_t r = 1, b = kPrimes[j] % p, e = p - 2;
+        while (e) {
+          if (e & 1) r = r * b % p;
+          b = b * b % p;
+          e >>= 1;
+        }
+        inv[j][i] = r;
+      }
+  }
+};
+const CrtTables& crt_tables() {
+  static const CrtTables t;
+  return t;
+}
+}  // namespace
+
 int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int* h_sign) {
   if (!h_residues || !h_mag || !h_sign || k < 1 || k > SPERM_KMAX || limbs < k + 1)
     return set_error(SPERM_ERR_ARG, "sperm_crt: bad arguments");
+  // Garner: mixed-radix digits v_i with x = v_0 + p_0 (v_1 + p_1 (v_2 + ...))
+  const CrtTables& T = crt_tables();
   uint64_t v[SPERM_KMAX];
   for (int i = 0; i < k; ++i) {
-    uint64_t p = kPrimes[i];
+    const uint64_t p = kPrimes[i];
     uint64_t x = h_residues[i] % p;
-    for (int j = 0; j < i; ++j) {
-      // x = (x - v_j) * inverse(p_j) mod p
-      uint64_t pj = kPrimes[j] % p;
-      uint64_t inv = 1, b = pj, e = p - 2;  // Fermat
-      while (e) {
-        if (e & 1) inv = inv * b % p;
-        b = b * b % p;
-        e >>= 1;
-      }
-      x = (x + p - v[j] % p) % p * inv % p;
-    }
+    for (int j = 0; j < i; ++j) x = (x + p - v[j] % p) % p * T.inv[j][i] % p;
     v[i] = x;
   }
-  // x = Horner over the mixed radix, in limbs
-  std::vector<uint32_t> X(limbs + 1, 0), M(limbs + 1, 0);
-  auto mul_add = [&](std::vector<uint32_t>& a, uint32_t m, uint32_t add) {
+  // x = Horner over the mixed radix, in limbs (k + 2 limbs hold 2x and M: every p_i < 2^31)
+  constexpr int LW = SPERM_KMAX + 2;
+  uint32_t X[LW] = {0}, M[LW] = {0}, X2[LW];
+  const int nl = k + 2;
+  auto mul_add = [&](uint32_t* a, uint32_t m, uint32_t add) {
     uint64_t carry = add;
-    for (size_t t = 0; t < a.size(); ++t) {
-      uint64_t cur = (uint64_t)a[t] * m + carry;
+    for (int t = 0; t < nl; ++t) {
+      const uint64_t cur = (uint64_t)a[t] * m + carry;
       a[t] = (uint32_t)cur;
       carry = cur >> 32;
     }
@@ -234,27 +252,28 @@ int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int
   M[0] = 1;
   for (int i = 0; i < k; ++i) mul_add(M, kPrimes[i], 0);
   // compare 2X with M
-  std::vector<uint32_t> X2(X);
+  for (int t = 0; t < nl; ++t) X2[t] = X[t];
   mul_add(X2, 2, 0);
   int cmp = 0;
-  for (int t = (int)X2.size() - 1; t >= 0 && cmp == 0; --t)
+  for (int t = nl - 1; t >= 0 && cmp == 0; --t)
     if (X2[t] != M[t]) cmp = X2[t] > M[t] ? 1 : -1;
   int sign = 1;
   if (cmp > 0) {  // x - M < 0: magnitude M - X
     int64_t borrow = 0;
-    for (size_t t = 0; t < X.size(); ++t) {
-      int64_t d = (int64_t)M[t] - X[t] - borrow;
+    for (int t = 0; t < nl; ++t) {
+      const int64_t d = (int64_t)M[t] - X[t] - borrow;
       borrow = d < 0;
       X[t] = (uint32_t)(d + (borrow ? (int64_t)1 << 32 : 0));
     }
     sign = -1;
   }
+  for (int t = limbs; t < nl; ++t)
+    if (X[t] != 0) return set_error(SPERM_ERR_ARG, "sperm_crt: too few limbs");
   bool zero = true;
   for (int t = 0; t < limbs; ++t) {
-    h_mag[t] = X[t];
-    if (X[t]) zero = false;
+    h_mag[t] = t < nl ? X[t] : 0u;
+    if (t < nl && X[t]) zero = false;
   }
-  if (X[limbs] != 0) return set_error(SPERM_ERR_ARG, "sperm_crt: too few limbs");
   *h_sign = zero ? 0 : sign;
   return SPERM_OK;
 }

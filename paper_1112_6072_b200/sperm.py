@@ -201,12 +201,15 @@ def residues_to_ints(res, k) -> List[int]:
     sign = np.zeros(count, dtype=np.int32)
     _check(lib().sperm_crt_batch(res.ctypes.data, count, res.shape[1], ks.ctypes.data, 0, mag.ctypes.data,
                                  limbs, sign.ctypes.data))
-    # little-endian uint32 limbs -> Python ints (marshalling)
-    out = []
-    for r in range(count):
-        v = int.from_bytes(mag[r].tobytes(), "little")
-        out.append(int(sign[r]) * v)
-    return out
+    # little-endian uint32 limbs -> Python ints (marshalling): values below 2^64 in one vectorized
+    # step, the rest row by row
+    small = (~mag[:, 2:].any(axis=1)).tolist()
+    lo = (mag[:, 0].astype(np.uint64) | (mag[:, 1].astype(np.uint64) << np.uint64(32))).tolist()
+    sg = sign.tolist()
+    buf = mag.tobytes()
+    w = 4 * mag.shape[1]
+    return [s_ * (v if sm else int.from_bytes(buf[r * w:(r + 1) * w], "little"))
+            for r, (s_, v, sm) in enumerate(zip(sg, lo, small))]
 
 
 # --------------------------------------------------------------------- expansion
