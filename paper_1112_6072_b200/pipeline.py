@@ -219,6 +219,23 @@ def gather_estimates(est_part, group=None):
     return est_part
 
 
+def dynamic_chunks(order, chunk: int, store, key: str):
+    """The paper's dynamic Step 3 across ranks (each job goes to the
+    first free processor, in estimate order): every rank repeatedly claims the next `chunk` jobs
+    of the shared order from one atomic counter in the torch.distributed store (store.add), so a
+    rank that finishes early takes more.  Yields the claimed job ids; over all ranks every job is
+    claimed exactly once."""
+    order = np.asarray(order)
+    while True:
+        start = int(store.add(key, chunk)) - chunk
+        if start >= len(order):
+            return
+        yield order[start:start + chunk]
+
+
+_dynamic_calls = 0
+
+
 def allreduce_accumulators(acc, group=None):
     """Algorithm PH Step 4 across GPUs: one SUM all-reduce of the
     [jobs + 1][8] residue accumulators (NCCL on GPUs).  Each rank added residues < 2^31
@@ -236,12 +253,16 @@ def reconstruct(res, k: int):
 
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
-              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30) -> PHResult:
+              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30,
+              assignment: str = "static", store=None, dynamic_chunk: int = 0) -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
 
     With a torch.distributed `group` of world size G, every rank replicates the
-    (cheap, deterministic) pre-expansion, estimation and scheduling, evaluates only
-    the jobs LPT assigned to it, and one all-reduce sums the residue accumulators."""
+    (cheap, deterministic) pre-expansion and scheduling, estimates its share of the jobs,
+    evaluates only the jobs assigned to it, and one all-reduce sums the residue accumulators.
+    assignment="static": the LPT plan of sperm_schedule (S1); "dynamic": ranks claim chunks of
+    the policy's job order from a shared counter in `store` (default: the process group's
+    store) as they finish — the paper's first-free-processor rule across GPUs."""
     import torch
     import torch.distributed as dist
     rank, world = (dist.get_rank(group), dist.get_world_size(group)) if group is not None else (0, 1)
@@ -289,33 +310,52 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     acc.record_stream(rnw_stream)
     if measure_jobs:
         job_cycles.record_stream(rnw_stream)
-    for s in jobsets:
-        ids = s.job.cpu().numpy()
-        sel = np.nonzero(pos[ids] >= 0)[0]
-        sel = sel[np.argsort(pos[ids[sel]], kind="stable")]
-        for b0 in range(0, len(sel), batch_jobs):
-            idx = torch.tensor(sel[b0:b0 + batch_jobs], dtype=torch.int64, device=device)
-            batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
-                            s.job.index_select(0, idx))
-            for lv in iter_leaves(batch, leaf_order, leaf_budget_bytes, stats):
-                if lv.n > S.NMAX:
-                    raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
-                stats["leaf_sets"] += 1
-                t_r = time.perf_counter()
-                rnw_stream.wait_stream(main)  # the leaves were written on the main stream
-                for t in (lv.mats, lv.coef, lv.job):
-                    t.record_stream(rnw_stream)  # keep them alive until the R-NW batch is done
-                with torch.cuda.stream(rnw_stream):
-                    cyc = torch.zeros(lv.count, dtype=torch.int64, device=device) if measure_jobs else None
-                    S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
-                                      max_primes=k_total if nonneg else 0, job_acc=acc, leaf_cycles=cyc,
-                                      stream=rnw_stream)
-                    if measure_jobs:  # measured job cost T_i = SM cycles of its leaves
-                        job_cycles.index_add_(0, lv.job.long(), cyc)
-                stats["rnw_calls"] += 1
-                stats["rnw_host_s"] += time.perf_counter() - t_r
-                leaves += lv.count
-                terms += S.sperm_rnw_terms(lv.n, lv.count)
+    # the job batches this rank evaluates: (jobset, indices within it), in evaluation order
+    def static_batches():
+        for s in jobsets:
+            ids = s.job.cpu().numpy()
+            sel = np.nonzero(pos[ids] >= 0)[0]
+            sel = sel[np.argsort(pos[ids[sel]], kind="stable")]
+            for b0 in range(0, len(sel), batch_jobs):
+                yield s, sel[b0:b0 + batch_jobs]
+
+    def dynamic_batches():
+        global _dynamic_calls
+        _dynamic_calls += 1
+        st = store if store is not None else dist.distributed_c10d._get_default_store()
+        starts = np.cumsum([0] + [s.count for s in jobsets])  # job ids are numbered set by set
+        chunk = dynamic_chunk or max(1, num_jobs // (16 * world))
+        for jobs in dynamic_chunks(order, chunk, st, f"sperm_dynamic_{_dynamic_calls}"):
+            which = np.searchsorted(starts, jobs, side="right") - 1
+            for si, s in enumerate(jobsets):
+                mine = jobs[which == si] - starts[si]
+                if len(mine):
+                    yield s, mine
+
+    dynamic = assignment == "dynamic" and (world > 1 or store is not None)
+    for s, sel in (dynamic_batches() if dynamic else static_batches()):
+        idx = torch.tensor(sel, dtype=torch.int64, device=device)
+        batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
+                        s.job.index_select(0, idx))
+        for lv in iter_leaves(batch, leaf_order, leaf_budget_bytes, stats):
+            if lv.n > S.NMAX:
+                raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
+            stats["leaf_sets"] += 1
+            t_r = time.perf_counter()
+            rnw_stream.wait_stream(main)  # the leaves were written on the main stream
+            for t in (lv.mats, lv.coef, lv.job):
+                t.record_stream(rnw_stream)  # keep them alive until the R-NW batch is done
+            with torch.cuda.stream(rnw_stream):
+                cyc = torch.zeros(lv.count, dtype=torch.int64, device=device) if measure_jobs else None
+                S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
+                                  max_primes=k_total if nonneg else 0, job_acc=acc, leaf_cycles=cyc,
+                                  stream=rnw_stream)
+                if measure_jobs:  # measured job cost T_i = SM cycles of its leaves
+                    job_cycles.index_add_(0, lv.job.long(), cyc)
+            stats["rnw_calls"] += 1
+            stats["rnw_host_s"] += time.perf_counter() - t_r
+            leaves += lv.count
+            terms += S.sperm_rnw_terms(lv.n, lv.count)
     main.wait_stream(rnw_stream)
     stats["t_loop_s"] = time.perf_counter() - t_loop
     allreduce_accumulators(acc, group)

@@ -92,3 +92,57 @@ def test_two_rank_partition_and_residue_allreduce(policy):
     for rank, total, jobs_ok, owned_once, same_sched in out:
         assert total == 1392  # per(C20) (tests/golden/oracle_values.txt)
         assert jobs_ok and owned_once and same_sched
+
+
+def _dyn_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import time
+        from oracle.hybrid import node_permanent, pre_expand
+        from workloads import dodecahedron
+        jobs = pre_expand(dodecahedron(), jobs_at_least=60)
+        J = len(jobs)
+        vals = [node_permanent(j) for j in jobs]
+        order = np.argsort(-np.array([abs(v) for v in vals]), kind="stable")  # any shared order
+        store = dist.distributed_c10d._get_default_store()
+        mine = []
+        for chunk in pipeline.dynamic_chunks(order, 3, store, "test_dynamic"):
+            mine.extend(int(j) for j in chunk)
+            time.sleep(0.002 * (rank + 1))  # ranks of different speed: the faster claims more
+        k = P.sperm_bound_primes(dodecahedron())
+        acc = torch.zeros((J + 1, P.KMAX), dtype=torch.int64)
+        for j in mine:
+            for qq in range(k):
+                r = vals[j] % P.sperm_prime(qq)
+                acc[j, qq] += r
+                acc[J, qq] += r
+        pipeline.allreduce_accumulators(acc, dist.group.WORLD)
+        red = np.zeros((J + 1, P.KMAX), dtype=np.uint32)
+        for qq in range(k):
+            red[:, qq] = (acc[:, qq].numpy() % P.sperm_prime(qq)).astype(np.uint32)
+        job_values, total = pipeline.reconstruct(red, k)
+        claimed = [None] * world
+        dist.all_gather_object(claimed, mine)
+        q.put((rank, total, job_values == vals, sorted(sum(claimed, [])) == list(range(J)), len(mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_dynamic_assignment():
+    """pipeline.dynamic_chunks over the process group's store: every job claimed by exactly one
+    rank (the faster rank claims more), and the residue all-reduce still gives per(C20)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dyn_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, total, jobs_ok, all_once, n_mine in out:
+        assert total == 1392 and jobs_ok and all_once and n_mine > 0

@@ -292,6 +292,23 @@ def test_pipeline_measure_jobs_and_signed_input():
     assert pipeline.permanent(b, jobs_at_least=20, leaf_order=12).value == h_per(b)
 
 
+def test_pipeline_dynamic_assignment_single_rank():
+    """assignment="dynamic" with an explicit store (one rank): chunks claimed from the store's
+    counter map back to their job sets; value and every job value unchanged."""
+    import socket
+    from torch.distributed import TCPStore
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    store = TCPStore("127.0.0.1", port, 1, True)
+    a = truncated_icosahedron()
+    r1 = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
+    r2 = pipeline.permanent(a, jobs_at_least=128, leaf_order=18, assignment="dynamic", store=store, dynamic_chunk=5)
+    assert r2.value == r1.value == golden("C60_truncated_icosahedron")
+    assert r2.job_values == r1.job_values
+
+
 def test_pipeline_c60_leaf16():
     a = truncated_icosahedron()
     r = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
