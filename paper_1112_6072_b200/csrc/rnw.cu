@@ -728,7 +728,9 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           for (int r = 1; r < GF; ++r) x *= W[NS + g * GF + r];
           FG[g] = x;
         }
-        const bool neg = (O0 + ob) & 1ull;  // (-1)^{|high Gray bits|}
+        // the sign (-1)^{|high Gray bits|} rides on the first factor (prime-independent): the
+        // Montgomery chain then yields a residue of the signed block value, congruent mod p
+        const int32_t f0 = ((O0 + ob) & 1ull) ? -FG[0] : FG[0];
         // per prime: P_F's chain, then the exact E groups of the leaf's mode
         auto chain = [&](auto gsz, const int32_t* grp) {
           constexpr int NGR = decltype(gsz)::value;
@@ -736,12 +738,12 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           for (int q = 0; q < K; ++q) {
             if (K == SPERM_KMAX && q >= k) break;
             const int32_t p = prime_p(q), pinv = prime_pinv(q);
-            int32_t v = FG[0];
+            int32_t v = f0;
 #pragma unroll
             for (int g = 1; g < NGF; ++g) v = smont(v, FG[g], p, pinv);
 #pragma unroll
             for (int j = 0; j < NGR; ++j) v = smont(v, grp[j], p, pinv);
-            acc[q] += neg ? -(int64_t)v : (int64_t)v;
+            acc[q] += (int64_t)v;
           }
         };
         if (emode == 2) chain(std::integral_constant<int, NP4>{}, P4);  // warp-uniform per leaf
@@ -1127,13 +1129,14 @@ void record_stats(int key, int NPg, int n, int64_t leaves, int64_t sum_k, double
     const double blocks = std::ldexp(T, -B);  // per leaf
     // per block, prime-independent: W update (S4 adds), slot products 2 (KS - 1) muls + KS adds
     // + 1 subtract per low column, <= B - 1 group joins, NGF (GF - 1) fixed-row products, ~8 ops
-    // of loop / Gray bookkeeping; per prime: the block's smont chain (sum_kx) + 4-op accumulate
+    // of loop / Gray bookkeeping, the sign on the first factor (2 ops); per prime: the block's
+    // smont chain (sum_kx) + a 64-bit accumulate (2 ops)
     const double f_sh = B * 2.0 * (KS - 1) + (B - 1) + NGF * (GF - 1.0);
     const double a_sh = S4 + B * (KS + 1.0) + 8;
     // ptxas issues about half of the 32-bit adds as IMAD.IADD on the multiply pipe (SASS mix of
     // the tree kernels): split them evenly
-    fma_terms = blocks * ((f_sh + 0.5 * a_sh) * (double)leaves + 5.5 * sum_kx + 2.0 * sum_k);
-    alu_terms = blocks * (0.5 * a_sh * (double)leaves + 0.5 * sum_kx + 2.0 * sum_k);
+    fma_terms = blocks * ((f_sh + 0.5 * a_sh + 1.0) * (double)leaves + 5.5 * sum_kx + 1.0 * sum_k);
+    alu_terms = blocks * ((0.5 * a_sh + 1.0) * (double)leaves + 0.5 * sum_kx + 1.0 * sum_k);
   }
   std::lock_guard<std::mutex> lk(g_stats_mu);
   g_stats.terms += T * leaves;
