@@ -374,7 +374,9 @@ __global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
     int* colcnt = rowcnt + SPERM_EXPAND_NMAX;
     pl = plan_node(A, cf, lane, rowcnt, colcnt);
     bool ovf = false;
-    for (int c = 0; c < pl.nkids; ++c) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {  // static bound: the plan stays in registers
+      if (c >= pl.nkids) break;
       if (!pl.kid[c].valid) ovf = true;
       if (survives(A, pl.kid[c], rowcnt, colcnt, lane, &ovf)) {
         ++kids;
@@ -461,7 +463,8 @@ __global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
     return;
   }
   const int64_t m2 = (int64_t)(n - 1) * (n - 1);
-  for (int c = 0; c < pl.nkids; ++c) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
     if ((mask >> c) & 1) {
       write_dense<true>(A, pl.kid[c], out_mats + ok_ * m2, lane);
       if (lane == 0) {
