@@ -100,10 +100,12 @@ __device__ Plan plan_node(const NodeView& A, int64_t coef, int lane, int* rowcnt
       const int l = __ffs(b) - 1;
       b &= b - 1;
       const int32_t vv = __shfl_sync(0xffffffffu, v, l);
-      if (cnt < 4) {
-        pos[cnt] = c0 + l;
-        val[cnt] = vv;
-      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)  // static indices: pos/val stay in registers
+        if (cnt == t) {
+          pos[t] = c0 + l;
+          val[t] = vv;
+        }
       ++cnt;
     }
   }
