@@ -936,15 +936,15 @@ StreamPool& stream_pool() {
   return p;
 }
 
-// Terms per lane 2^m: small enough that a group has >= ~8 work items per resident warp of the
-// GPU (fine-grained tail), at least mmin (the tree block size), at most 2^14 and such that a
-// leaf holds at least one 32-lane chunk.
+// Terms per lane 2^m: small enough that a group has 1-2x per_warp work items per resident warp
+// of the GPU (16 per SM; items of equal size, pulled dynamically), at least mmin (the tree block
+// size), at most 2^14 and such that a leaf holds at least one 32-lane chunk.
 int choose_m(int n, int64_t nleaves, int mmin) {
   const int tb = n - 1;
-  static const double per_warp = [] {  // A-B knob: SPERM_RNW_ITEMS_PER_WARP (default 2, measured
-    const char* e = getenv("SPERM_RNW_ITEMS_PER_WARP");  // best of 1/2/4/8 on configs[1])
-    const double v = e ? atof(e) : 0.0;
-    return v > 0.0 ? v : 2.0;
+  static const double per_warp = [] {  // A-B knob: SPERM_RNW_ITEMS_PER_WARP (default 1: with the
+    const char* e = getenv("SPERM_RNW_ITEMS_PER_WARP");  // closed-form blocks measured best of
+    const double v = e ? atof(e) : 0.0;                  // 0.75/1/1.5/2/4 on configs[1], 0.169 vs
+    return v > 0.0 ? v : 1.0;                            // 0.190 ms at 2; fullerene96 R-NW -8 %)
   }();
   const double target_items = (double)sm_count() * 16.0 * per_warp;
   const double per_lane = std::ldexp((double)nleaves, tb) / (32.0 * target_items);
