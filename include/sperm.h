@@ -64,6 +64,14 @@ int sperm_crt(const uint32_t* h_residues, int k, uint32_t* h_mag, int limbs, int
 int sperm_crt_batch(const uint32_t* h_residues, int64_t count, int stride, const int32_t* h_k, int k_all,
                     uint32_t* h_mag, int limbs, int* h_sign);
 
+/* sperm_crt_batch on the device (asynchronous on `stream`): the same Garner CRT per row, one
+ * thread per row; d_out[r*(limbs+1) .. r*(limbs+1)+limbs) receives the magnitude's little-endian
+ * uint32 limbs and d_out[r*(limbs+1)+limbs] the sign (-1, 0, +1), so one device-to-host copy
+ * returns a whole batch.  d_residues [count][stride] uint32, d_k [count] int32 or NULL (k_all
+ * primes per row), k + 1 <= limbs <= SPERM_KMAX + 2.  Errors: SPERM_ERR_ARG. */
+int sperm_crt_device(const uint32_t* d_residues, int64_t count, int stride, const int32_t* d_k, int k_all,
+                     uint32_t* d_out, int limbs, void* stream);
+
 /* Number of CRT primes that reconstruct per(A) of one HOST matrix h_mat [n][n] (host,
  * synchronous): |per(A)| <= min(prod_i sum_j |a_ij|, prod_j sum_i |a_ij|), and for a 0/1
  * matrix the Bregman-Minc bound prod_i (r_i!)^(1/r_i) (rows and columns).  SPERM_ERR_PRIMES

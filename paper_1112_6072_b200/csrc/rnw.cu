@@ -1163,6 +1163,126 @@ extern "C" double sperm_rnw_terms(int n, int64_t count) {
   return (double)count * std::ldexp(1.0, n - 1);
 }
 
+namespace sperm {
+namespace {
+// Garner inverses inv[j][i] = p_j^-1 mod p_i (j < i), computed on the host once, passed by value
+struct CrtInv {
+  uint32_t inv[SPERM_KMAX][SPERM_KMAX];
+};
+const CrtInv& crt_inv() {
+  static const CrtInv t = [] {
+    CrtInv c{};
+    for (int i = 0; i < SPERM_KMAX; ++i)
+      for (int j = 0; j < SPERM_KMAX; ++j) {
+        const uint64_t p = kPrimes[i];
+        uint64_t r = 1, b = kPrimes[j] % p, e = p - 2;
+        while (e) {
+          if (e & 1) r = r * b % p;
+          b = b * b % p;
+          e >>= 1;
+        }
+        c.inv[j][i] = (uint32_t)r;
+      }
+    return c;
+  }();
+  return t;
+}
+
+// one row per thread: Garner digits, Horner in 32-bit limbs, symmetric range (as sperm_crt)
+__global__ void crt_kernel(const uint32_t* __restrict__ res, int64_t count, int stride, const int32_t* __restrict__ kk,
+                           int k_all, uint32_t* __restrict__ out, int limbs, const CrtInv tab) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= count) return;
+  const int k = kk ? kk[r] : k_all;
+  uint32_t* o = out + r * (limbs + 1);
+  if (k < 1 || k > SPERM_KMAX) {
+    for (int t = 0; t <= limbs; ++t) o[t] = 0u;
+    return;
+  }
+  uint64_t v[SPERM_KMAX];
+#pragma unroll
+  for (int i = 0; i < SPERM_KMAX; ++i) {
+    if (i < k) {
+      const uint64_t p = (uint32_t)prime_p(i);
+      uint64_t x = res[r * stride + i] % p;
+#pragma unroll
+      for (int j = 0; j < SPERM_KMAX; ++j)
+        if (j < i) x = (x + p - v[j] % p) % p * tab.inv[j][i] % p;
+      v[i] = x;
+    }
+  }
+  constexpr int LW = SPERM_KMAX + 2;
+  uint32_t X[LW], M[LW];
+#pragma unroll
+  for (int t = 0; t < LW; ++t) X[t] = M[t] = 0u;
+  X[0] = (uint32_t)v[k - 1];
+  M[0] = 1u;
+  for (int i = k - 2; i >= 0; --i) {  // X = X * p_i + v_i
+    uint64_t carry = v[i];
+#pragma unroll
+    for (int t = 0; t < LW; ++t) {
+      const uint64_t cur = (uint64_t)X[t] * (uint32_t)prime_p(i) + carry;
+      X[t] = (uint32_t)cur;
+      carry = cur >> 32;
+    }
+  }
+  for (int i = 0; i < k; ++i) {
+    uint64_t carry = 0;
+#pragma unroll
+    for (int t = 0; t < LW; ++t) {
+      const uint64_t cur = (uint64_t)M[t] * (uint32_t)prime_p(i) + carry;
+      M[t] = (uint32_t)cur;
+      carry = cur >> 32;
+    }
+  }
+  int cmp = 0;  // compare 2X with M, most significant limb first
+  {
+    uint32_t hi_carry = 0;
+    uint32_t X2[LW];
+#pragma unroll
+    for (int t = 0; t < LW; ++t) {
+      X2[t] = (X[t] << 1) | hi_carry;
+      hi_carry = X[t] >> 31;
+    }
+#pragma unroll
+    for (int t = LW - 1; t >= 0; --t)
+      if (cmp == 0 && X2[t] != M[t]) cmp = X2[t] > M[t] ? 1 : -1;
+  }
+  int sign = 1;
+  if (cmp > 0) {  // x - M < 0: magnitude M - X
+    int64_t borrow = 0;
+#pragma unroll
+    for (int t = 0; t < LW; ++t) {
+      const int64_t d = (int64_t)M[t] - X[t] - borrow;
+      borrow = d < 0;
+      X[t] = (uint32_t)(d + (borrow ? (int64_t)1 << 32 : 0));
+    }
+    sign = -1;
+  }
+  bool zero = true;
+  for (int t = 0; t < limbs; ++t) {
+    const uint32_t x = t < LW ? X[t] : 0u;
+    o[t] = x;
+    zero = zero && x == 0u;
+  }
+  o[limbs] = (uint32_t)(zero ? 0 : sign);
+}
+}  // namespace
+}  // namespace sperm
+
+extern "C" int sperm_crt_device(const uint32_t* d_residues, int64_t count, int stride, const int32_t* d_k, int k_all,
+                                uint32_t* d_out, int limbs, void* stream) {
+  if (count < 0 || stride < 1 || limbs > SPERM_KMAX + 2 || limbs < 2 ||
+      (count > 0 && (!d_residues || !d_out)) || (!d_k && (k_all < 1 || k_all > SPERM_KMAX || limbs < k_all + 1)))
+    return set_error(SPERM_ERR_ARG, "sperm_crt_device: bad arguments");
+  if (count == 0) return SPERM_OK;
+  count_launch();
+  crt_kernel<<<(unsigned)((count + 127) / 128), 128, 0, (cudaStream_t)stream>>>(d_residues, count, stride, d_k, k_all,
+                                                                                 d_out, limbs, crt_inv());
+  SPERM_LAUNCH_CHECK("crt_kernel");
+  return SPERM_OK;
+}
+
 extern "C" int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d_out, void* stream) {
   if (rows < 0 || (rows > 0 && (!d_acc || !d_out))) return set_error(SPERM_ERR_ARG, "sperm_reduce_mod: bad args");
   if (rows == 0) return SPERM_OK;

@@ -41,6 +41,7 @@ _SIGS = {
     "sperm_prime": (ctypes.c_uint32, [_I]),
     "sperm_crt": (_I, [_P, _I, _P, _I, _P]),
     "sperm_crt_batch": (_I, [_P, _I64, _I, _P, _I, _P, _I, _P]),
+    "sperm_crt_device": (_I, [_P, _I64, _I, _P, _I, _P, _I, _P]),
     "sperm_bound_primes": (_I, [_P, _I, _P]),
     "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P]),
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
@@ -182,6 +183,29 @@ def sperm_reduce_mod(acc, stream=None):
     out = torch.empty((rows, KMAX), dtype=torch.int32, device=acc.device)
     _check(lib().sperm_reduce_mod(_ptr(acc), rows, _ptr(out), _stream(stream)))
     return out
+
+
+def residues_to_ints_device(res, k, stream=None) -> List[int]:
+    """residues_to_ints with the CRT on the GPU (sperm_crt_device): one device-to-host copy of
+    [count][limbs + 1] words (magnitude limbs, sign), then marshalling to Python ints."""
+    import torch
+    res = _dev(res, torch.int32)
+    count, stride = int(res.shape[0]), int(res.shape[1])
+    if count == 0:
+        return []
+    k = _dev(k, torch.int32)
+    limbs = KMAX + 2
+    out = torch.empty((count, limbs + 1), dtype=torch.int32, device=res.device)
+    _check(lib().sperm_crt_device(_ptr(res), count, stride, _ptr(k), 0, _ptr(out), limbs, _stream(stream)))
+    h = out.cpu().numpy().view(np.uint32)
+    mag, sign = h[:, :limbs], h[:, limbs].view(np.int32)
+    small = (~mag[:, 2:].any(axis=1)).tolist()
+    lo = (mag[:, 0].astype(np.uint64) | (mag[:, 1].astype(np.uint64) << np.uint64(32))).tolist()
+    sg = sign.tolist()
+    buf = np.ascontiguousarray(mag).tobytes()
+    w = 4 * limbs
+    return [s_ * (v if sm else int.from_bytes(buf[r * w:(r + 1) * w], "little"))
+            for r, (s_, v, sm) in enumerate(zip(sg, lo, small))]
 
 
 def residues_to_ints(res, k) -> List[int]:

@@ -371,6 +371,18 @@ def test_rnw_many_primes_every_plan(wmax):
         _plans_agree(a[None], [h_per(a)])
 
 
+def test_crt_device_matches_host():
+    """sperm_crt_device (GPU Garner + limbs) = sperm_crt (host) on random residues, every k, signs."""
+    rng = np.random.default_rng(9)
+    res = rng.integers(0, 2**31 - 1, size=(300, P.KMAX), dtype=np.int64).astype(np.uint32)
+    ks = rng.integers(1, P.KMAX + 1, size=300).astype(np.int32)
+    res[0, :] = 0  # zero
+    got = P.residues_to_ints_device(torch.tensor(res.view(np.int32), device="cuda"),
+                                    torch.tensor(ks, device="cuda"))
+    want = [P.sperm_crt(res[i], int(ks[i])) for i in range(300)]
+    assert got == want and got[0] == 0 and any(v < 0 for v in got)
+
+
 def test_rnw_prime_count_bregman_and_cap():
     """0/1 leaves size their prime count by Bregman-Minc (configs[1] 0/1 half: 1 prime);
     max_primes caps it, leaving every residue correct modulo the primes kept."""
