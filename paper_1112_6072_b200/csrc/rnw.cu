@@ -132,7 +132,7 @@ __device__ __forceinline__ M mask_below(int n) {  // bits 0..n-1
   return n >= (int)(8 * sizeof(M)) ? ~M(0) : (M(1) << n) - 1;
 }
 
-template <typename M>
+template <typename M, int U>
 __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
                                 const int64_t* __restrict__ coef, int min_primes, int max_primes, int allow_tree,
                                 int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err) {
@@ -146,9 +146,9 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   const int ns = n + 1;  // padded row stride: the row scans a[i*ns + j] hit distinct banks
   int32_t* sa = prep_sm + wib * (n * ns);
   {
-    // every load of a batch is issued before its stores (one batch covers n <= 22), so the
-    // leaf arrives in one memory round trip instead of n*n/32 dependent ones
-    constexpr int U = 16;
+    // every load of a batch is issued before its stores (U = the smallest of 4, 8, 12, 16 words
+    // per lane that covers the leaf, else batches of 16), so the leaf arrives in one memory round
+    // trip instead of n*n/32 dependent ones, with few predicated-off slots
     const int32_t* g = mats + leaf * (int64_t)n * n;
     const int nn = n * n;
     const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)n) + 1u;  // e / n for e < 2^16
@@ -1364,7 +1364,10 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     const int64_t threads = count * 32;
     count_launch();
     const size_t prep_smem = (size_t)8 * n * (n + 1) * sizeof(int32_t);  // padded rows, 8 warps
-    auto prep = n <= 32 ? rnw_prep_kernel<uint32_t> : rnw_prep_kernel<unsigned long long>;
+    const int per_lane = (n * n + 31) / 32;
+    auto prep = n > 32 ? rnw_prep_kernel<unsigned long long, 16>
+              : per_lane <= 4 ? rnw_prep_kernel<uint32_t, 4> : per_lane <= 8 ? rnw_prep_kernel<uint32_t, 8>
+              : per_lane <= 12 ? rnw_prep_kernel<uint32_t, 12> : rnw_prep_kernel<uint32_t, 16>;
     {  // the attribute once per device, for the largest order (host time per call)
       static std::atomic<unsigned> prep_attr{0};
       int dev = 0;
@@ -1372,8 +1375,10 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       const unsigned bit = 1u << (dev & 31);
       if (!(prep_attr.load() & bit)) {
         const int max_smem = 8 * SPERM_NMAX * (SPERM_NMAX + 1) * (int)sizeof(int32_t);
-        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        for (auto kf : {rnw_prep_kernel<uint32_t, 4>, rnw_prep_kernel<uint32_t, 8>, rnw_prep_kernel<uint32_t, 12>,
+                        rnw_prep_kernel<uint32_t, 16>})
+          SPERM_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<unsigned long long, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        max_smem));
         prep_attr.fetch_or(bit);
       }
