@@ -480,19 +480,21 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
       if (d == 0.0) { x = 0.0; break; }  // CTA-uniform
       x = __dmul_rn(x, d);
       if (k + 1 == n) break;
+      // one phase, one barrier: the row exchange of columns > k (column k is never read again
+      // for X) and the multipliers, which read column k only — with the exchange applied on the
+      // fly: the pivot value is row p's, and row i = p (after the exchange: old row k) reads row k's
       if (p != k)
-        for (int j = k + t; j < n; j += kKsThreads) {
+        for (int j = k + 1 + t; j < n; j += kKsThreads) {
           const double2 u = b[k * ns + j];
           b[k * ns + j] = b[p * ns + j];
           b[p * ns + j] = u;
         }
-      __syncthreads();
       {
-        const double2 pk = b[k * ns + k];
+        const double2 pk = b[p * ns + k];
         const double y = __drcp_rn(d);
         const bool d_ok = div_range_ok(d);
         for (int i = k + 1 + t; i < n; i += kKsThreads) {
-          const double2 v = b[i * ns + k];
+          const double2 v = b[(i == p ? k : i) * ns + k];
           lv[i] = make_double2(div_by(__dadd_rn(__dmul_rn(v.x, pk.x), __dmul_rn(v.y, pk.y)), d, y, d_ok),
                                div_by(__dsub_rn(__dmul_rn(v.y, pk.x), __dmul_rn(v.x, pk.y)), d, y, d_ok));
         }
