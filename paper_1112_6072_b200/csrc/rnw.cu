@@ -307,6 +307,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     int64_t pp = 1, qp = 1;
 #pragma unroll
     for (int c = 0; c < kMaxLow; ++c) {  // warp-uniform shuffles, per-lane plan bounds
+      if (c >= np) break;                  // warp-uniform: no plan uses more than np columns
       const int64_t q = __shfl_sync(0xffffffffu, my_q, c);
       const M sc = __shfl_sync(0xffffffffu, my_supp, c);
       if (c < B) {
