@@ -423,6 +423,31 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
 // 16-byte accesses, the multiplier a broadcast).  Same operations in the same order as the
 // oracle on every entry, so X is bit-identical; updates by a zero pivot-row entry are skipped
 // (see kk_update).
+// pivot of column k (rows >= k): first row with maximal re^2 + im^2 — per lane ascending with a
+// strict >, then a (larger value, then smaller row) butterfly; lane 0 publishes it
+__device__ __forceinline__ void pivot_reduce(double bm, int bi, int lane, double& s_d, int& s_p) {
+  for (int o = 16; o; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, bm, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (om > bm || (om == bm && oi < bi)) { bm = om; bi = oi; }
+  }
+  if (lane == 0) {
+    s_d = bm;
+    s_p = bi;
+  }
+}
+__device__ __forceinline__ void pivot_scan(const double2* b, int ns, int n, int k, int lane, double& s_d,
+                                           int& s_p) {
+  double bm = -1.0;
+  int bi = n;
+  for (int i = k + lane; i < n; i += 32) {
+    const double2 v = b[i * ns + k];
+    const double mg = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+    if (mg > bm) { bm = mg; bi = i; }
+  }
+  pivot_reduce(bm, bi, lane, s_d, s_p);
+}
+
 constexpr int kKsThreads = 256;
 __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
                                                                 const int32_t* __restrict__ ids, int trials,
@@ -454,27 +479,9 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
     }
     __syncthreads();
     double x = 1.0;
+    if (w == 0) pivot_scan(b, ns, n, 0, lane, s_d, s_p);  // later pivots come out of the update
+    __syncthreads();
     for (int k = 0; k < n; ++k) {
-      if (w == 0) {
-        // pivot: first row i >= k with maximal re^2 + im^2 (ascending per lane, strict >)
-        double bm = -1.0;
-        int bi = n;
-        for (int i = k + lane; i < n; i += 32) {
-          const double2 v = b[i * ns + k];
-          const double m = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
-          if (m > bm) { bm = m; bi = i; }
-        }
-        for (int o = 16; o; o >>= 1) {
-          const double om = __shfl_xor_sync(0xffffffffu, bm, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (om > bm || (om == bm && oi < bi)) { bm = om; bi = oi; }
-        }
-        if (lane == 0) {
-          s_d = bm;
-          s_p = bi;
-        }
-      }
-      __syncthreads();
       const double d = s_d;
       const int p = s_p;
       if (d == 0.0) { x = 0.0; break; }  // CTA-uniform
@@ -500,12 +507,33 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
         }
       }
       __syncthreads();
-      {
-        // trailing m x m block: thread t -> column j = k+1 + t % m, rows k+1 + t / m + G * r
-        const int m = n - k - 1;
-        const int G = m >= kKsThreads ? 1 : kKsThreads / m;
-        const int g = t / m, j = k + 1 + (t - g * m);
-        if (g < G && j < n) {
+      if (w == 0) {
+        // warp 0: column k+1 (the next pivot column), then the next pivot search over it while
+        // the update of columns > k+1 is still running — s_d/s_p were last read before the barrier
+        const int j = k + 1;
+        const double2 u = b[k * ns + j];
+        const bool nz = u.x != 0.0 || u.y != 0.0;
+        double bm = -1.0;
+        int bi = n;
+        for (int i = j + lane; i < n; i += 32) {
+          double2 v = b[i * ns + j];
+          if (nz) {
+            const double2 l = lv[i];
+            v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
+            v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
+            b[i * ns + j] = v;
+          }
+          const double mg = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+          if (mg > bm) { bm = mg; bi = i; }
+        }
+        pivot_reduce(bm, bi, lane, s_d, s_p);
+      } else {
+        // columns > k+1: thread t' = t - 32 -> column j = k+2 + t' % m, rows k+1 + t' / m + G * r
+        const int m = n - k - 2;
+        const int tt = t - 32;
+        const int G = m >= kKsThreads - 32 ? 1 : (kKsThreads - 32) / max(m, 1);
+        const int g = tt / max(m, 1), j = k + 2 + (tt - g * max(m, 1));
+        if (m > 0 && g < G && j < n) {
           const double2 u = b[k * ns + j];
           if (u.x != 0.0 || u.y != 0.0) {
 #pragma unroll 4
