@@ -38,6 +38,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <atomic>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <tuple>
 #include <type_traits>
@@ -485,7 +486,9 @@ template <int NP>
 __global__ void __launch_bounds__(kRnwThreads) rnw_generic_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, unsigned long long* __restrict__ queue, uint64_t total_items,
-    unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
+    unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles,
+    const int* __restrict__ go) {
+  if (go && *go == 0) return;  // a speculative launch whose plan histogram did not match
   using L = GLayout<NP>;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
@@ -604,7 +607,9 @@ template <int NFIX, int PLAN>
 __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFIX, plan_gf(PLAN))) rnw_tree_kernel(
     const int32_t* __restrict__ mats, int n, int m, int cbits, const int32_t* __restrict__ leaves,
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
-    uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles) {
+    uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles,
+    const int* __restrict__ go) {
+  if (go && *go == 0) return;  // a speculative launch whose plan histogram did not match
   constexpr int B = plan_b(PLAN), GF = plan_gf(PLAN);
   constexpr int NS = B * KS;       // slot rows
   constexpr int NRT = NS + NFIX;   // row sums held in registers
@@ -892,6 +897,24 @@ __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order
     }
 }
 
+// Speculative plan-group launch: the host launches the previous call's groups (same device, order,
+// count and prime bounds) before it has read this call's histogram back; this kernel sets the go
+// flag they test iff the histogram (hence every group's leaf range and launch shape) is the one
+// they were launched for and prep raised no error.  The host compares the same two histograms.
+struct KeyHist {
+  int h[kNumKeys];
+};
+__global__ void rnw_spec_check_kernel(const int* __restrict__ hist, const int* __restrict__ err, KeyHist pred,
+                                      int* __restrict__ go) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = *err;
+  __syncthreads();
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x)
+    if (hist[t] != pred.h[t]) atomicOr(&bad, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) *go = bad == 0;
+}
+
 // ============================================================================ launch helpers
 struct Launch {
   const int32_t* mats;
@@ -904,6 +927,7 @@ struct Launch {
   unsigned long long* leaf_acc;
   cudaStream_t st;
   unsigned long long* leaf_cycles;  // optional per-leaf SM-cycle counters
+  const int* go;                    // speculative launch: run only if *go != 0 (else NULL)
 };
 
 // A per-process pool of non-blocking streams and reusable events for the plan groups.
@@ -988,7 +1012,7 @@ int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bo
   (void)tree;
   count_launch();
   kernel<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, L.m, L.cbits, L.leaves, L.meta, L.perm,
-                                                        L.queue, total, L.leaf_acc, L.leaf_cycles);
+                                                        L.queue, total, L.leaf_acc, L.leaf_cycles, L.go);
   SPERM_LAUNCH_CHECK("rnw kernel");
   return SPERM_OK;
 }
@@ -1009,7 +1033,7 @@ int launch_generic(const Launch& L) {
   grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
   count_launch();
   kern<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, m, cbits, L.leaves, L.meta, L.queue, total,
-                                                    L.leaf_acc, L.leaf_cycles);
+                                                    L.leaf_acc, L.leaf_cycles, L.go);
   SPERM_LAUNCH_CHECK("rnw_generic_kernel");
   return SPERM_OK;
 }
@@ -1403,19 +1427,83 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
                                               (int)count, 0, 7, st));
   }
   // one read-back of the whole small block (err, histograms, queues, kx) into a per-thread
-  // pinned buffer (a pageable copy is staged and slower)
+  // pinned buffer (a pageable copy is staged and slower), marked by a per-thread event
   thread_local void* h_small_pinned = nullptr;
+  thread_local std::map<int, cudaEvent_t> rb_events;
+  int dev = 0;
+  SPERM_TRY(cudaGetDevice(&dev));
   if (!h_small_pinned) SPERM_TRY(cudaMallocHost(&h_small_pinned, small_bytes));
+  cudaEvent_t& rb = rb_events[dev];
+  if (!rb) SPERM_TRY(cudaEventCreateWithFlags(&rb, cudaEventDisableTiming));
   SPERM_TRY(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, st));
-  SPERM_TRY(cudaStreamSynchronize(st));
+  SPERM_TRY(cudaEventRecord(rb, st));
+
+  // One persistent launch per plan group, each on its own stream of a small pool forked from `st`
+  // (a later group's CTAs fill the SMs freed by an earlier group's tail), joined back into `st`.
+  // Each group has its own work counter; groups are launched largest work first.
+  int rc = SPERM_OK;
+  auto launch_groups = [&](const int* hh, const std::vector<int>& order_keys, const int* go) -> int {
+    StreamPool& pool = stream_pool();
+    cudaEvent_t fork = pool.event();
+    SPERM_CUDA(cudaEventRecord(fork, st));
+    int64_t offs[kNumKeys];
+    int64_t off = 0;
+    for (int key = 0; key < kNumKeys; ++key) {
+      offs[key] = off;
+      off += hh[key];
+    }
+    int g = 0;
+    for (int key : order_keys) {
+      cudaStream_t gs = order_keys.size() > 1 ? pool.stream(g) : st;
+      if (gs != st) SPERM_CUDA(cudaStreamWaitEvent(gs, fork, 0));
+      Launch L{d_mats, n, 0, 0, sorted + offs[key], hh[key], meta, perm, queue + key, leaf_acc, gs,
+               (unsigned long long*)d_leaf_cycles, go};
+      const int r = launch_key(key, NPg, L);
+      if (gs != st) {
+        cudaEvent_t join = pool.event();
+        SPERM_CUDA(cudaEventRecord(join, gs));
+        SPERM_CUDA(cudaStreamWaitEvent(st, join, 0));
+      }
+      if (r != SPERM_OK) return r;
+      ++g;
+    }
+    return SPERM_OK;
+  };
+  // the previous call's groups, launched before the read-back completes when this call has the same
+  // shape (repeated batches): the host's synchronization then overlaps the R-NW kernels
+  struct Spec {
+    int dev = -1, n = -1, NPg = 0, minp = 0, maxp = 0, plan0 = -1;
+    int64_t count = -1;
+    KeyHist hist;
+    std::vector<int> order;
+  };
+  thread_local Spec spec;
+  static const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables
+    const char* e = getenv("SPERM_SPECULATE");
+    return !(e && e[0] == '0');
+  }();
+  const bool speculate = spec_on && n > 0 && spec.dev == dev && spec.n == n && spec.count == count &&
+                         spec.NPg == NPg && spec.minp == min_primes && spec.maxp == max_primes &&
+                         spec.plan0 == first_plan();
+  int* go = small;  // small[0]: zeroed above
+  std::unique_ptr<TimingScope> ts_rnw;
+  if (speculate) {
+    ts_rnw.reset(new TimingScope("rnw", st));
+    count_launch();
+    rnw_spec_check_kernel<<<1, 128, 0, st>>>(hist, err, spec.hist, go);
+    SPERM_TRY(cudaGetLastError());
+    rc = launch_groups(spec.hist.h, spec.order, go);
+    if (rc != SPERM_OK) { ts_rnw.reset(); cleanup(); return rc; }
+  }
+  SPERM_TRY(cudaEventSynchronize(rb));
   int hsmall[4 + 2 * kNumKeys];
   unsigned long long h_kx[kNumKeys];
   memcpy(hsmall, h_small_pinned, sizeof(hsmall));
   memcpy(h_kx, static_cast<const char*>(h_small_pinned) + sizeof(int) * (4 + 2 * kNumKeys) +
                    sizeof(unsigned long long) * kNumKeys,
          sizeof(h_kx));
-  if (hsmall[2] & 1) { cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
-  if (hsmall[2] & 2) { cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
+  if (hsmall[2] & 1) { ts_rnw.reset(); cleanup(); return set_error(SPERM_ERR_RANGE, "sperm_permanent: a row abs sum is >= 2^30"); }
+  if (hsmall[2] & 2) { ts_rnw.reset(); cleanup(); return set_error(SPERM_ERR_PRIMES, "sperm_permanent: bound needs > 8 primes"); }
   const int* h_hist = hsmall + 4;
   static const bool debug = getenv("SPERM_DEBUG") != nullptr;
   if (debug) {  // plan histogram of this call (diagnostics)
@@ -1424,54 +1512,34 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       if (h_hist[key])
         fprintf(stderr, " key%d(plan%d,nfix%d)=%d sum_k=%d", key, key / 8, key ? nfix_of(key % 8) : 0, h_hist[key],
                 hsmall[4 + kNumKeys + key]);
-    fprintf(stderr, "\n");
+    fprintf(stderr, "%s\n", speculate ? " (speculative launch)" : "");
   }
   if (n > 0) {
     for (int key = 0; key < kNumKeys; ++key)
       if (h_hist[key]) record_stats(key, NPg, n, h_hist[key], hsmall[4 + kNumKeys + key], (double)h_kx[key]);
   }
-  int nonzero_keys = 0;
-  for (int q = 0; q < kNumKeys; ++q) nonzero_keys += h_hist[q] > 0;
-  int rc = SPERM_OK;
   if (n > 0) {
-    // One persistent launch per plan group, each on its own stream of a small pool forked
-    // from `st` (a later group's CTAs fill the SMs freed by an earlier group's tail), joined
-    // back into `st`.  Each group has its own work counter.
-    TimingScope ts("rnw", st);
-    StreamPool& pool = stream_pool();
-    cudaEvent_t fork = pool.event();
-    SPERM_TRY(cudaEventRecord(fork, st));
-    // group offsets in the sorted list (key order); launch the groups largest work first so the
-    // small groups fill the SMs the large ones release in their tails
-    int64_t offs[kNumKeys];
     std::vector<int> order_keys;
-    {
-      int64_t off = 0;
-      for (int key = 0; key < kNumKeys; ++key) {
-        offs[key] = off;
-        off += h_hist[key];
-        if (h_hist[key]) order_keys.push_back(key);
-      }
-      const int* h_sumk = hsmall + 4 + kNumKeys;
-      std::stable_sort(order_keys.begin(), order_keys.end(),
-                       [&](int a, int b) { return h_sumk[a] > h_sumk[b]; });
-    }
-    int g = 0;
-    for (int key : order_keys) {
-      if (rc != SPERM_OK) break;
-      cudaStream_t gs = nonzero_keys > 1 ? pool.stream(g) : st;
-      if (gs != st) SPERM_TRY(cudaStreamWaitEvent(gs, fork, 0));
-      Launch L{d_mats, n, 0, 0, sorted + offs[key], h_hist[key], meta, perm, queue + key, leaf_acc, gs,
-               (unsigned long long*)d_leaf_cycles};
-      rc = launch_key(key, NPg, L);
-      if (gs != st) {
-        cudaEvent_t join = pool.event();
-        SPERM_TRY(cudaEventRecord(join, gs));
-        SPERM_TRY(cudaStreamWaitEvent(st, join, 0));
-      }
-      ++g;
+    for (int key = 0; key < kNumKeys; ++key)
+      if (h_hist[key]) order_keys.push_back(key);
+    const int* h_sumk = hsmall + 4 + kNumKeys;
+    std::stable_sort(order_keys.begin(), order_keys.end(), [&](int a, int b) { return h_sumk[a] > h_sumk[b]; });
+    const bool matched = speculate && memcmp(spec.hist.h, h_hist, sizeof(spec.hist.h)) == 0;
+    spec.dev = dev;
+    spec.n = n;
+    spec.count = count;
+    spec.NPg = NPg;
+    spec.minp = min_primes;
+    spec.maxp = max_primes;
+    spec.plan0 = first_plan();
+    memcpy(spec.hist.h, h_hist, sizeof(spec.hist.h));
+    spec.order = order_keys;
+    if (!matched) {  // the speculative kernels (if any) found go == 0 and exited
+      if (!ts_rnw) ts_rnw.reset(new TimingScope("rnw", st));
+      rc = launch_groups(h_hist, order_keys, nullptr);
     }
   }
+  ts_rnw.reset();
   if (rc != SPERM_OK) { cleanup(); return rc; }
   {
     TimingScope ts("rnw_finalize", st);

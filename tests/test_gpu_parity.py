@@ -327,6 +327,19 @@ def _plans_agree(mats, want):
         assert got == want, pmin
 
 
+def test_rnw_speculative_groups_repeat_and_change():
+    """Same-shape calls launch the previous call's plan groups before the histogram read-back
+    (csrc/rnw.cu rnw_spec_check_kernel): repeats, same-shape batches with other contents and other
+    plan histograms must all stay exact."""
+    a = random_3perm_batch(16, 20, seed=11)
+    a2 = random_3perm_batch(16, 20, seed=12)
+    rng = np.random.default_rng(7)
+    b = (rng.integers(-3, 4, size=(16, 20, 20)) * (rng.random((16, 20, 20)) < 0.2)).astype(np.int64)
+    want = {id(x): [h_per(m) for m in x] for x in (a, a2, b)}
+    for x in (a, a, a2, b, b, a, a2, a2):
+        assert gpu_per(x) == want[id(x)]
+
+
 def test_rnw_tree_plans_3regular():
     for n, seed in ((12, 1), (17, 2), (20, 3), (26, 4)):
         mats = random_3perm_batch(12, n, seed=seed)
