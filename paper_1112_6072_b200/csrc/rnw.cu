@@ -915,6 +915,82 @@ __global__ void rnw_spec_check_kernel(const int* __restrict__ hist, const int* _
   if (threadIdx.x == 0) *go = bad == 0;
 }
 
+// Small batches (count <= kSmallGroup): the keys kernel, the radix sort and the speculation check
+// in one single-CTA kernel — key histogram, exclusive scan, scatter of the leaf ids into their
+// groups (warp-aggregated cursors: the order inside a group is not kept, and nothing depends on it:
+// every leaf has its own accumulators), histogram store and the go flag.
+constexpr int kSmallGroup = 4096;
+constexpr int kSmallGroupThreads = 1024;
+__global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
+    int count, const int32_t* __restrict__ order, const int2* __restrict__ meta, int32_t* __restrict__ sorted,
+    int* __restrict__ hist, int* __restrict__ hist_k, unsigned long long* __restrict__ hist_kx,
+    const int* __restrict__ err, KeyHist pred, int spec, int* __restrict__ go) {
+  __shared__ int s_h[kNumKeys], s_hk[kNumKeys], s_cur[kNumKeys];
+  __shared__ unsigned long long s_hx[kNumKeys];
+  __shared__ int s_bad;
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
+    s_h[t] = s_hk[t] = 0;
+    s_hx[t] = 0;
+  }
+  __syncthreads();
+  for (int base = 0; base < count; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool live = i < count;
+    int key = -1, kk = 0, y = 0;
+    if (live) {
+      const int2 mt = meta[order ? order[i] : i];
+      const int plan = meta_plan(mt);
+      key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
+      kk = meta_k(mt);
+      y = mt.y;
+    }
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int c1 = __popc(same), ck = __reduce_add_sync(same, (unsigned)kk),
+              cx = __reduce_add_sync(same, (unsigned)(kk * y));
+    if (live && lane == __ffs(same) - 1) {
+      atomicAdd(&s_h[key], c1);
+      atomicAdd(&s_hk[key], ck);
+      atomicAdd(&s_hx[key], (unsigned long long)(unsigned)cx);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int off = 0;
+    for (int k = 0; k < kNumKeys; ++k) {
+      s_cur[k] = off;
+      off += s_h[k];
+    }
+    s_bad = *err;
+  }
+  __syncthreads();
+  for (int base = 0; base < count; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool live = i < count;
+    int key = -1, leaf = 0;
+    if (live) {
+      leaf = order ? order[i] : i;
+      const int2 mt = meta[leaf];
+      const int plan = meta_plan(mt);
+      key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
+    }
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(same) - 1;
+    int pos0 = 0;
+    if (live && lane == leader) pos0 = atomicAdd(&s_cur[key], __popc(same));
+    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+    if (live) sorted[pos0 + __popc(same & ((1u << lane) - 1u))] = leaf;
+  }
+  for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
+    hist[t] = s_h[t];
+    hist_k[t] = s_hk[t];
+    hist_kx[t] = s_hx[t];
+    if (spec && s_h[t] != pred.h[t]) atomicOr(&s_bad, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *go = spec && s_bad == 0;
+}
+
 // ============================================================================ launch helpers
 struct Launch {
   const int32_t* mats;
@@ -1384,6 +1460,26 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   unsigned long long* hist_kx = queue + kNumKeys;
   int* err = small + 2;
   int* hist = small + 4;
+  // the previous call's groups, launched before the read-back completes when this call has the same
+  // shape (repeated batches): the host's synchronization then overlaps the R-NW kernels
+  struct Spec {
+    int dev = -1, n = -1, NPg = 0, minp = 0, maxp = 0, plan0 = -1;
+    int64_t count = -1;
+    KeyHist hist;
+    std::vector<int> order;
+  };
+  thread_local Spec spec;
+  static const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables
+    const char* e = getenv("SPERM_SPECULATE");
+    return !(e && e[0] == '0');
+  }();
+  int dev = 0;
+  SPERM_TRY(cudaGetDevice(&dev));
+  const bool speculate = spec_on && n > 0 && spec.dev == dev && spec.n == n && spec.count == count &&
+                         spec.NPg == NPg && spec.minp == min_primes && spec.maxp == max_primes &&
+                         spec.plan0 == first_plan();
+  int* go = small;  // small[0]: zeroed above
+  const bool small_group = count <= kSmallGroup;
   {
     TimingScope ts("rnw_prep", st);
     const int64_t threads = count * 32;
@@ -1412,14 +1508,20 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
                                                                        first_plan(), meta, perm, err);
     SPERM_TRY(cudaGetLastError());
     count_launch();
-    rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist, hist + kNumKeys, hist_kx);
+    if (small_group)
+      rnw_group_small_kernel<<<1, kSmallGroupThreads, 0, st>>>((int)count, d_order, meta, ids + count, hist,
+                                                               hist + kNumKeys, hist_kx, err, spec.hist,
+                                                               speculate ? 1 : 0, go);
+    else
+      rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist,
+                                                                       hist + kNumKeys, hist_kx);
     SPERM_TRY(cudaGetLastError());
   }
   // leaves grouped by plan key, evaluation order kept inside each group (stable radix sort on
   // the 7-bit keys), queued before the histogram read-back so that the host's only work after
   // the synchronization is launching the plan groups
   const int32_t* sorted = ids + count;
-  {
+  if (!small_group) {
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 7, st);
     SPERM_TRY(cudaMallocAsync(&sort_tmp, tmp_bytes, st));
@@ -1430,8 +1532,6 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   // pinned buffer (a pageable copy is staged and slower), marked by a per-thread event
   thread_local void* h_small_pinned = nullptr;
   thread_local std::map<int, cudaEvent_t> rb_events;
-  int dev = 0;
-  SPERM_TRY(cudaGetDevice(&dev));
   if (!h_small_pinned) SPERM_TRY(cudaMallocHost(&h_small_pinned, small_bytes));
   cudaEvent_t& rb = rb_events[dev];
   if (!rb) SPERM_TRY(cudaEventCreateWithFlags(&rb, cudaEventDisableTiming));
@@ -1469,29 +1569,14 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     }
     return SPERM_OK;
   };
-  // the previous call's groups, launched before the read-back completes when this call has the same
-  // shape (repeated batches): the host's synchronization then overlaps the R-NW kernels
-  struct Spec {
-    int dev = -1, n = -1, NPg = 0, minp = 0, maxp = 0, plan0 = -1;
-    int64_t count = -1;
-    KeyHist hist;
-    std::vector<int> order;
-  };
-  thread_local Spec spec;
-  static const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables
-    const char* e = getenv("SPERM_SPECULATE");
-    return !(e && e[0] == '0');
-  }();
-  const bool speculate = spec_on && n > 0 && spec.dev == dev && spec.n == n && spec.count == count &&
-                         spec.NPg == NPg && spec.minp == min_primes && spec.maxp == max_primes &&
-                         spec.plan0 == first_plan();
-  int* go = small;  // small[0]: zeroed above
   std::unique_ptr<TimingScope> ts_rnw;
   if (speculate) {
+    if (!small_group) {
+      count_launch();
+      rnw_spec_check_kernel<<<1, 128, 0, st>>>(hist, err, spec.hist, go);
+      SPERM_TRY(cudaGetLastError());
+    }
     ts_rnw.reset(new TimingScope("rnw", st));
-    count_launch();
-    rnw_spec_check_kernel<<<1, 128, 0, st>>>(hist, err, spec.hist, go);
-    SPERM_TRY(cudaGetLastError());
     rc = launch_groups(spec.hist.h, spec.order, go);
     if (rc != SPERM_OK) { ts_rnw.reset(); cleanup(); return rc; }
   }

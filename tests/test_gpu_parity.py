@@ -338,6 +338,13 @@ def test_rnw_speculative_groups_repeat_and_change():
     want = {id(x): [h_per(m) for m in x] for x in (a, a2, b)}
     for x in (a, a, a2, b, b, a, a2, a2):
         assert gpu_per(x) == want[id(x)]
+    # above the single-CTA grouping size (keys kernel + radix sort + separate check kernel)
+    c = random_3perm_batch(5000, 12, seed=13)
+    c2 = c.copy()
+    c2[::3] = (rng.integers(-3, 4, size=(1667, 12, 12)) * (rng.random((1667, 12, 12)) < 0.4)).astype(np.int64)
+    want = {id(x): [per_ryser_nw_c(m) for m in x] for x in (c, c2)}
+    for x in (c, c, c2, c2, c):
+        assert gpu_per(x) == want[id(x)]
 
 
 def test_rnw_tree_plans_3regular():
