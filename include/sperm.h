@@ -127,8 +127,12 @@ int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
  *  stream     cudaStream_t.
  * Errors: SPERM_ERR_ARG (n > SPERM_NMAX, count < 0), SPERM_ERR_RANGE (some
  * row or column abs sum >= 2^30), SPERM_ERR_PRIMES.  RANGE/PRIMES are
- * detected on the device and reported synchronously (the call synchronizes
- * `stream` once after the bound pass). */
+ * detected on the device and reported synchronously (the call waits once for
+ * the read-back of the bound pass and plan histogram; when the calling thread's
+ * previous call had the same device, n, count and prime bounds, the previous
+ * plan groups are launched before that wait and run only if the device finds
+ * the same histogram — results are identical either way; SPERM_SPECULATE=0
+ * turns this off). */
 int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* d_coef,
                     const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
                     int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
