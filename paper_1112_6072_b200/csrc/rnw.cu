@@ -1535,14 +1535,15 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   if (!h_small_pinned) SPERM_TRY(cudaMallocHost(&h_small_pinned, small_bytes));
   cudaEvent_t& rb = rb_events[dev];
   if (!rb) SPERM_TRY(cudaEventCreateWithFlags(&rb, cudaEventDisableTiming));
-  SPERM_TRY(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, st));
-  SPERM_TRY(cudaEventRecord(rb, st));
-
   // One persistent launch per plan group, each on its own stream of a small pool forked from `st`
   // (a later group's CTAs fill the SMs freed by an earlier group's tail), joined back into `st`.
   // Each group has its own work counter; groups are launched largest work first.
   int rc = SPERM_OK;
-  auto launch_groups = [&](const int* hh, const std::vector<int>& order_keys, const int* go) -> int {
+  // (joins: the group streams' completion events, waited on by `st` afterwards — by the caller, so
+  // that the read-back can be queued on `st` between the speculative launches and their joins)
+  std::vector<cudaEvent_t> joins;
+  auto launch_groups = [&](const int* hh, const std::vector<int>& order_keys, const int* go,
+                           bool pooled) -> int {
     StreamPool& pool = stream_pool();
     cudaEvent_t fork = pool.event();
     SPERM_CUDA(cudaEventRecord(fork, st));
@@ -1554,7 +1555,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     }
     int g = 0;
     for (int key : order_keys) {
-      cudaStream_t gs = order_keys.size() > 1 ? pool.stream(g) : st;
+      cudaStream_t gs = pooled || order_keys.size() > 1 ? pool.stream(g) : st;
       if (gs != st) SPERM_CUDA(cudaStreamWaitEvent(gs, fork, 0));
       Launch L{d_mats, n, 0, 0, sorted + offs[key], hh[key], meta, perm, queue + key, leaf_acc, gs,
                (unsigned long long*)d_leaf_cycles, go};
@@ -1562,7 +1563,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       if (gs != st) {
         cudaEvent_t join = pool.event();
         SPERM_CUDA(cudaEventRecord(join, gs));
-        SPERM_CUDA(cudaStreamWaitEvent(st, join, 0));
+        joins.push_back(join);
       }
       if (r != SPERM_OK) return r;
       ++g;
@@ -1577,9 +1578,23 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       SPERM_TRY(cudaGetLastError());
     }
     ts_rnw.reset(new TimingScope("rnw", st));
-    rc = launch_groups(spec.hist.h, spec.order, go);
-    if (rc != SPERM_OK) { ts_rnw.reset(); cleanup(); return rc; }
+    rc = launch_groups(spec.hist.h, spec.order, go, true);
   }
+  auto join_groups = [&]() -> int {
+    for (cudaEvent_t j : joins) SPERM_CUDA(cudaStreamWaitEvent(st, j, 0));
+    joins.clear();
+    return SPERM_OK;
+  };
+  // the read-back, queued on `st` after the grouping (and ahead of the speculative groups' joins)
+  auto ok = [](cudaError_t e, const char* what) { return e == cudaSuccess ? SPERM_OK : cuda_check(e, what); };
+  if (rc == SPERM_OK)
+    rc = ok(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, st), "read-back");
+  if (rc == SPERM_OK) rc = ok(cudaEventRecord(rb, st), "read-back event");
+  {
+    const int rj = join_groups();
+    if (rc == SPERM_OK) rc = rj;
+  }
+  if (rc != SPERM_OK) { ts_rnw.reset(); cleanup(); return rc; }
   SPERM_TRY(cudaEventSynchronize(rb));
   int hsmall[4 + 2 * kNumKeys];
   unsigned long long h_kx[kNumKeys];
@@ -1621,7 +1636,9 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     spec.order = order_keys;
     if (!matched) {  // the speculative kernels (if any) found go == 0 and exited
       if (!ts_rnw) ts_rnw.reset(new TimingScope("rnw", st));
-      rc = launch_groups(h_hist, order_keys, nullptr);
+      rc = launch_groups(h_hist, order_keys, nullptr, false);
+      const int rj = join_groups();
+      if (rc == SPERM_OK) rc = rj;
     }
   }
   ts_rnw.reset();
