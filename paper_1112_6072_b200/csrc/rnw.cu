@@ -136,11 +136,13 @@ __device__ __forceinline__ M mask_below(int n) {  // bits 0..n-1
 template <typename M, int U>
 __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
                                 const int64_t* __restrict__ coef, int min_primes, int max_primes, int allow_tree,
-                                int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err) {
+                                int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err,
+                                unsigned long long* __restrict__ leaf_acc) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (leaf >= count) return;
+  if (lane < SPERM_KMAX) leaf_acc[leaf * SPERM_KMAX + lane] = 0;  // the R-NW accumulators
   // stage the leaf in shared memory with coalesced loads; the per-lane row/column scans
   // below then read shared memory (one warp per leaf, 8 warps per CTA)
   extern __shared__ int32_t prep_sm[];
@@ -1453,7 +1455,6 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
   const size_t small_bytes = sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * 2 * kNumKeys;
   SPERM_TRY(cudaMallocAsync((void**)&small, small_bytes, st));
-  SPERM_TRY(cudaMemsetAsync(leaf_acc, 0, sizeof(unsigned long long) * count * SPERM_KMAX, st));
   SPERM_TRY(cudaMemsetAsync(small, 0, small_bytes, st));
   // per-group work counters after the histograms (8-byte aligned: 4 + 2*48 ints = 400 bytes)
   unsigned long long* queue = reinterpret_cast<unsigned long long*>(small + 4 + 2 * kNumKeys);
@@ -1505,7 +1506,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       }
     }
     prep<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
-                                                                       first_plan(), meta, perm, err);
+                                                                       first_plan(), meta, perm, err, leaf_acc);
     SPERM_TRY(cudaGetLastError());
     count_launch();
     if (small_group)
@@ -1539,14 +1540,16 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   // (a later group's CTAs fill the SMs freed by an earlier group's tail), joined back into `st`.
   // Each group has its own work counter; groups are launched largest work first.
   int rc = SPERM_OK;
-  // (joins: the group streams' completion events, waited on by `st` afterwards — by the caller, so
-  // that the read-back can be queued on `st` between the speculative launches and their joins)
+  // The largest group runs on `st` itself, the others on pool streams 1..7 (stream 0 carries the
+  // speculative path's read-back); joins: their completion events, waited on by `st` afterwards.
   std::vector<cudaEvent_t> joins;
-  auto launch_groups = [&](const int* hh, const std::vector<int>& order_keys, const int* go,
-                           bool pooled) -> int {
+  auto launch_groups = [&](const int* hh, const std::vector<int>& order_keys, const int* go) -> int {
     StreamPool& pool = stream_pool();
-    cudaEvent_t fork = pool.event();
-    SPERM_CUDA(cudaEventRecord(fork, st));
+    cudaEvent_t fork = nullptr;
+    if (order_keys.size() > 1) {
+      fork = pool.event();
+      SPERM_CUDA(cudaEventRecord(fork, st));
+    }
     int64_t offs[kNumKeys];
     int64_t off = 0;
     for (int key = 0; key < kNumKeys; ++key) {
@@ -1555,7 +1558,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     }
     int g = 0;
     for (int key : order_keys) {
-      cudaStream_t gs = pooled || order_keys.size() > 1 ? pool.stream(g) : st;
+      cudaStream_t gs = g == 0 ? st : pool.stream(1 + (g - 1) % 7);
       if (gs != st) SPERM_CUDA(cudaStreamWaitEvent(gs, fork, 0));
       Launch L{d_mats, n, 0, 0, sorted + offs[key], hh[key], meta, perm, queue + key, leaf_acc, gs,
                (unsigned long long*)d_leaf_cycles, go};
@@ -1578,18 +1581,26 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       SPERM_TRY(cudaGetLastError());
     }
     ts_rnw.reset(new TimingScope("rnw", st));
-    rc = launch_groups(spec.hist.h, spec.order, go, true);
+    // the read-back on pool stream 0, forked before the groups (`st` waits for it with the joins)
+    StreamPool& pool = stream_pool();
+    cudaEvent_t cf = pool.event();
+    cudaStream_t cs = pool.stream(0);
+    SPERM_TRY(cudaEventRecord(cf, st));
+    SPERM_TRY(cudaStreamWaitEvent(cs, cf, 0));
+    SPERM_TRY(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, cs));
+    SPERM_TRY(cudaEventRecord(rb, cs));
+    joins.push_back(rb);
+    rc = launch_groups(spec.hist.h, spec.order, go);
   }
   auto join_groups = [&]() -> int {
     for (cudaEvent_t j : joins) SPERM_CUDA(cudaStreamWaitEvent(st, j, 0));
     joins.clear();
     return SPERM_OK;
   };
-  // the read-back, queued on `st` after the grouping (and ahead of the speculative groups' joins)
-  auto ok = [](cudaError_t e, const char* what) { return e == cudaSuccess ? SPERM_OK : cuda_check(e, what); };
-  if (rc == SPERM_OK)
-    rc = ok(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, st), "read-back");
-  if (rc == SPERM_OK) rc = ok(cudaEventRecord(rb, st), "read-back event");
+  if (!speculate) {  // the read-back on `st` after the grouping
+    SPERM_TRY(cudaMemcpyAsync(h_small_pinned, small, small_bytes, cudaMemcpyDeviceToHost, st));
+    SPERM_TRY(cudaEventRecord(rb, st));
+  }
   {
     const int rj = join_groups();
     if (rc == SPERM_OK) rc = rj;
@@ -1636,7 +1647,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     spec.order = order_keys;
     if (!matched) {  // the speculative kernels (if any) found go == 0 and exited
       if (!ts_rnw) ts_rnw.reset(new TimingScope("rnw", st));
-      rc = launch_groups(h_hist, order_keys, nullptr, false);
+      rc = launch_groups(h_hist, order_keys, nullptr);
       const int rj = join_groups();
       if (rc == SPERM_OK) rc = rj;
     }
