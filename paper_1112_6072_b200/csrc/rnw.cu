@@ -57,6 +57,7 @@ constexpr int kPermRows = 64;     // per-leaf permutation record: 64 row bytes +
 constexpr int kPermW = 128;
 constexpr int kPermGend = kPermW - 1;  // byte 127 (column bytes >= 48 are unused): E mode
 constexpr int kNumKeys = 104;     // plan * 8 + nfix index
+static_assert(kNumKeys <= 128, "rnw_group_small_kernel scans 4 keys per lane");
 
 __host__ __device__ constexpr int nfix_of(int i) {
   return i == 0 ? 4 : i == 1 ? 8 : i == 2 ? 12 : i == 3 ? 16 : i == 4 ? 24 : i == 5 ? 32 : 40;
@@ -957,13 +958,27 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int off = 0;
-    for (int k = 0; k < kNumKeys; ++k) {
-      s_cur[k] = off;
-      off += s_h[k];
+  if (threadIdx.x < 32) {  // exclusive scan of the key counts: 4 keys per lane, then a warp scan
+    int c[4], tot = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = lane * 4 + u;
+      c[u] = k < kNumKeys ? s_h[k] : 0;
+      tot += c[u];
     }
-    s_bad = *err;
+    int inc = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    int off = inc - tot;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = lane * 4 + u;
+      if (k < kNumKeys) s_cur[k] = off;
+      off += c[u];
+    }
+    if (lane == 0) s_bad = *err;
   }
   __syncthreads();
   for (int base = 0; base < count; base += blockDim.x) {
@@ -1510,7 +1525,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     SPERM_TRY(cudaGetLastError());
     count_launch();
     if (small_group)
-      rnw_group_small_kernel<<<1, kSmallGroupThreads, 0, st>>>((int)count, d_order, meta, ids + count, hist,
+      rnw_group_small_kernel<<<1, (unsigned)std::min<int64_t>(kSmallGroupThreads, (count + 31) / 32 * 32), 0, st>>>((int)count, d_order, meta, ids + count, hist,
                                                                hist + kNumKeys, hist_kx, err, spec.hist,
                                                                speculate ? 1 : 0, go);
     else
