@@ -1,6 +1,8 @@
 """Summarise ncu outputs into small text files for profiles/ (run here, no GPU).
 
-    python tools/ncu_summary.py launches <launches.csv>          # per-kernel share of the step
+    python tools/ncu_summary.py launches <launches.csv> [UNTIL]  # per-kernel share of the step
+                                                                 # (launches before the first kernel
+                                                                 #  matching the regex UNTIL)
     python tools/ncu_summary.py report <file.ncu-rep> [...]      # key counters of a --set full capture
 """
 import csv
@@ -38,7 +40,8 @@ KEYS = [
 ]
 
 
-def launches(path):
+def launches(path, until=None):
+    import re
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
@@ -50,10 +53,13 @@ def launches(path):
         v = float(r[vi].replace(",", ""))
         v = v / 1e3 if r[ui] == "ns" else (v * 1e3 if r[ui] == "ms" else v)
         name = r[ki].split("(")[0]
+        if until and re.search(until, name):
+            break
         t[name] += v
         c[name] += 1
     tot = sum(t.values())
-    out = [f"# ncu --metrics gpu__time_duration.sum --clock-control none ({path}); cold-cache, serialised",
+    out = [f"# ncu --metrics gpu__time_duration.sum --clock-control none ({path}); cold-cache, serialised"
+           + (f"; launches before the first /{until}/" if until else ""),
            f"{'kernel':70s} {'launches':>8s} {'total_us':>12s} {'share':>7s}"]
     for k in sorted(t, key=lambda k: -t[k]):
         out.append(f"{k[-70:]:70s} {c[k]:8d} {t[k]:12.1f} {100 * t[k] / tot:6.1f}%")
@@ -77,6 +83,6 @@ def report(path):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        print(launches(sys.argv[2]))
+        print(launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None))
     else:
         print("\n\n".join(report(p) for p in sys.argv[2:]))
