@@ -1136,7 +1136,11 @@ int launch_tree(const Launch& L) {
   constexpr int B = plan_b(PLAN);
   constexpr int NS = B * KS, NRT = NS + NFIX;
   const int tb = L.n - 1;
-  const int m = choose_m(L.n, L.nleaves, std::min(B + 2, L.n - 6));
+  static const int min_block_bits = [] {  // A-B knob: SPERM_RNW_MIN_BLOCK_BITS (log2 blocks per lane per item)
+    const char* e = getenv("SPERM_RNW_MIN_BLOCK_BITS");
+    return e ? std::max(0, std::min(8, atoi(e))) : 4;  // 2 3 4 5 6: configs[1] 0.220 0.215 0.210 0.213 0.220 ms
+  }();
+  const int m = choose_m(L.n, L.nleaves, std::min(B + min_block_bits, L.n - 6));
   if (m > tb - 5) return set_error(SPERM_ERR_ARG, "sperm_permanent: leaf too small for the tree plan");
   const int cbits = tb - 5 - m;
   const uint64_t total = (uint64_t)L.nleaves << cbits;
