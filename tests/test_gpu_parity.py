@@ -336,6 +336,7 @@ def test_rnw_speculative_groups_repeat_and_change():
     rng = np.random.default_rng(7)
     b = (rng.integers(-3, 4, size=(16, 20, 20)) * (rng.random((16, 20, 20)) < 0.2)).astype(np.int64)
     want = {id(x): [h_per(m) for m in x] for x in (a, a2, b)}
+    want_a = want[id(a)]
     for x in (a, a, a2, b, b, a, a2, a2):
         assert gpu_per(x) == want[id(x)]
     # above the single-CTA grouping size (keys kernel + radix sort + separate check kernel)
@@ -345,6 +346,14 @@ def test_rnw_speculative_groups_repeat_and_change():
     want = {id(x): [per_ryser_nw_c(m) for m in x] for x in (c, c2)}
     for x in (c, c, c2, c2, c):
         assert gpu_per(x) == want[id(x)]
+    # a same-shape call whose prep reports an error: the speculative groups must not run, the
+    # error is raised, and the next call is exact again
+    bad = a.copy()
+    bad[3, 5, :] = 1 << 26  # row abs sum 20 * 2^26 >= 2^30
+    gpu_per(a)
+    with pytest.raises(P.SpermError):
+        gpu_per(bad)
+    assert gpu_per(a) == want_a
 
 
 def test_rnw_tree_plans_3regular():
