@@ -196,8 +196,14 @@ def residues_to_ints_device(res, k, stream=None) -> List[int]:
     k = _dev(k, torch.int32)
     limbs = KMAX + 2
     out = torch.empty((count, limbs + 1), dtype=torch.int32, device=res.device)
-    _check(lib().sperm_crt_device(_ptr(res), count, stride, _ptr(k), 0, _ptr(out), limbs, _stream(stream)))
-    h = out.cpu().numpy().view(np.uint32)
+    st = stream if stream is not None else torch.cuda.current_stream(res.device)
+    _check(lib().sperm_crt_device(_ptr(res), count, stride, _ptr(k), 0, _ptr(out), limbs, st.cuda_stream))
+    # read-back into pinned memory (torch's host caching allocator) on the launching stream
+    hp = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    with torch.cuda.stream(st):
+        hp.copy_(out, non_blocking=True)
+    st.synchronize()
+    h = hp.numpy().view(np.uint32)
     mag, sign = h[:, :limbs], h[:, limbs].view(np.int32)
     small = (~mag[:, 2:].any(axis=1)).tolist()
     lo = (mag[:, 0].astype(np.uint64) | (mag[:, 1].astype(np.uint64) << np.uint64(32))).tolist()
