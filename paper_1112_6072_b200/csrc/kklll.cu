@@ -448,8 +448,8 @@ __device__ __forceinline__ void pivot_scan(const double2* b, int ns, int n, int 
   pivot_reduce(bm, bi, lane, s_d, s_p);
 }
 
-constexpr int kKsThreads = 256;
-__global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+template <int NT>
+__global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
                                                                 const int32_t* __restrict__ ids, int trials,
                                                                 uint64_t seed, double* __restrict__ xout) {
   extern __shared__ double2 ksm2[];  // b[n][ns] (row stride ns = n | 1: column scans conflict-free) | lv[n]
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
     const int32_t* a = mats + job * (int64_t)n * n;
     const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
     __syncthreads();  // the previous trial is done with b
-    for (int e = t; e < n * n; e += kKsThreads) {
+    for (int e = t; e < n * n; e += NT) {
       const int i = e / n, j = e - (e / n) * n;
       double r = 0.0, s = 0.0;
       if (a[e] != 0) {
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
       // for X) and the multipliers, which read column k only — with the exchange applied on the
       // fly: the pivot value is row p's, and row i = p (after the exchange: old row k) reads row k's
       if (p != k)
-        for (int j = k + 1 + t; j < n; j += kKsThreads) {
+        for (int j = k + 1 + t; j < n; j += NT) {
           const double2 u = b[k * ns + j];
           b[k * ns + j] = b[p * ns + j];
           b[p * ns + j] = u;
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
         const double2 pk = b[p * ns + k];
         const double y = __drcp_rn(d);
         const bool d_ok = div_range_ok(d);
-        for (int i = k + 1 + t; i < n; i += kKsThreads) {
+        for (int i = k + 1 + t; i < n; i += NT) {
           const double2 v = b[(i == p ? k : i) * ns + k];
           lv[i] = make_double2(div_by(__dadd_rn(__dmul_rn(v.x, pk.x), __dmul_rn(v.y, pk.y)), d, y, d_ok),
                                div_by(__dsub_rn(__dmul_rn(v.y, pk.x), __dmul_rn(v.x, pk.y)), d, y, d_ok));
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kKsThreads) kklll_smem_kernel(const int32_t* _
         // columns > k+1: thread t' = t - 32 -> column j = k+2 + t' % m, rows k+1 + t' / m + G * r
         const int m = n - k - 2;
         const int tt = t - 32;
-        const int G = m >= kKsThreads - 32 ? 1 : (kKsThreads - 32) / max(m, 1);
+        const int G = m >= NT - 32 ? 1 : (NT - 32) / max(m, 1);
         const int g = tt / max(m, 1), j = k + 2 + (tt - g * max(m, 1));
         if (m > 0 && g < G && j < n) {
           const double2 u = b[k * ns + j];
@@ -598,15 +598,24 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
   } else if (!getenv("SPERM_KKLLL_CTA")) {
     // shared-memory-resident LU, one 256-thread CTA per trial, as many trials per SM as fit
     // (measured on the fullerene-96 jobs: 128 threads 1.37 s, 256 1.31 s, 512 1.97 s)
+    // (128-thread CTAs below order SPERM_KKLLL_T128_MAX: more trials per SM, cheaper barriers)
+    // (measured, 128 vs 256 threads: C60 jobs, order 32: 44.5 vs 75.1 ms; fullerene-96, order 67:
+    // 1287 vs 1080 ms; C100, order 72: 2595 vs 1919 ms — bit-identical trials either way)
+    static const int t128_max = [] {
+      const char* e = getenv("SPERM_KKLLL_T128_MAX");
+      return e ? atoi(e) : 48;
+    }();
+    const int nt = n < t128_max ? 128 : 256;
+    auto kern = nt == 128 ? kklll_smem_kernel<128> : kklll_smem_kernel<256>;
     const size_t smem = sizeof(double2) * ((size_t)n * (n | 1) + n);
-    SPERM_CUDA(cudaFuncSetAttribute(kklll_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_smem_kernel, kKsThreads, smem));
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
     int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
     grid = std::max<int64_t>(1, std::min(grid, items));
     TimingScope ts("kklll", st);
     count_launch();
-    kklll_smem_kernel<<<(unsigned)grid, kKsThreads, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+    kern<<<(unsigned)grid, nt, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else if (n <= 96) {
     // A-B (SPERM_KKLLL_CTA=1): CTA-distributed registers: rows per lane RL = ceil(n/32), column
     // slots per thread CS = ceil(n/8)
