@@ -528,24 +528,29 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
         }
         pivot_reduce(bm, bi, lane, s_d, s_p);
       } else {
-        // columns > k+1: thread t' = t - 32 -> column j = k+2 + t' % m, rows k+1 + t' / m + G * r
+        // columns > k+1: thread t' = t - 32 -> column j = k+2 + t' % m, rows k+1 + t' / m + G * r;
+        // when the m columns outnumber the NT - 32 threads, whole columns j = k+2 + t' + (NT-32) * c
         const int m = n - k - 2;
         const int tt = t - 32;
-        const int G = m >= NT - 32 ? 1 : (NT - 32) / max(m, 1);
-        const int g = tt / max(m, 1), j = k + 2 + (tt - g * max(m, 1));
-        if (m > 0 && g < G && j < n) {
-          const double2 u = b[k * ns + j];
-          if (u.x != 0.0 || u.y != 0.0) {
+        const bool wide = m >= NT - 32;
+        const int G = wide ? 1 : (NT - 32) / max(m, 1);
+        const int g = wide ? 0 : tt / max(m, 1);
+        const int cstep = wide ? NT - 32 : max(m, 1);
+        if (m > 0 && g < G)
+          for (int jj = tt - g * (wide ? 0 : m); jj < m; jj += cstep) {
+            const int j = k + 2 + jj;
+            const double2 u = b[k * ns + j];
+            if (u.x != 0.0 || u.y != 0.0) {
 #pragma unroll 4
-            for (int i = k + 1 + g; i < n; i += G) {
-              const double2 l = lv[i];
-              double2 v = b[i * ns + j];
-              v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
-              v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
-              b[i * ns + j] = v;
+              for (int i = k + 1 + g; i < n; i += G) {
+                const double2 l = lv[i];
+                double2 v = b[i * ns + j];
+                v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
+                v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
+                b[i * ns + j] = v;
+              }
             }
           }
-        }
       }
       __syncthreads();
     }
@@ -605,8 +610,12 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
       const char* e = getenv("SPERM_KKLLL_T128_MAX");
       return e ? atoi(e) : 48;
     }();
-    const int nt = n < t128_max ? 128 : 256;
-    auto kern = nt == 128 ? kklll_smem_kernel<128> : kklll_smem_kernel<256>;
+    static const int t64_max = [] {  // 64-thread CTAs below this order (C60 jobs: 39.8 vs 44.5 ms)
+      const char* e = getenv("SPERM_KKLLL_T64_MAX");
+      return e ? atoi(e) : 40;
+    }();
+    const int nt = n < t64_max ? 64 : n < t128_max ? 128 : 256;
+    auto kern = nt == 64 ? kklll_smem_kernel<64> : nt == 128 ? kklll_smem_kernel<128> : kklll_smem_kernel<256>;
     const size_t smem = sizeof(double2) * ((size_t)n * (n | 1) + n);
     SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;

@@ -210,9 +210,10 @@ def test_kklll_bit_exact_trials():
             assert abs(float(est[j]) - e) <= 1e-12 * abs(e)
 
 
-@pytest.mark.parametrize("n", [33, 47, 64, 65, 77, 96, 100])
+@pytest.mark.parametrize("n", [33, 36, 39, 47, 64, 65, 77, 96, 100])
 def test_kklll_bit_exact_large_orders(n):
-    """CTA-distributed kernel (32 < n <= 96) and the shared-memory kernel (n > 96):
+    """Shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
+    threads), 128 (n < 48) and 256 threads (SPERM_KKLLL_T64_MAX / _T128_MAX move the bounds):
     every trial bit-identical to the oracle, including singular (zero) trials (24 trials:
     ~1e4-1e5 multiplier quotients per order through the reciprocal-based division)."""
     rng = np.random.default_rng(n)
