@@ -532,25 +532,27 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
         // when the m columns outnumber the NT - 32 threads, whole columns j = k+2 + t' + (NT-32) * c
         const int m = n - k - 2;
         const int tt = t - 32;
-        const bool wide = m >= NT - 32;
-        const int G = wide ? 1 : (NT - 32) / max(m, 1);
-        const int g = wide ? 0 : tt / max(m, 1);
-        const int cstep = wide ? NT - 32 : max(m, 1);
-        if (m > 0 && g < G)
-          for (int jj = tt - g * (wide ? 0 : m); jj < m; jj += cstep) {
-            const int j = k + 2 + jj;
-            const double2 u = b[k * ns + j];
-            if (u.x != 0.0 || u.y != 0.0) {
+        auto column = [&](int j, int g, int G) {
+          const double2 u = b[k * ns + j];
+          if (u.x != 0.0 || u.y != 0.0) {
 #pragma unroll 4
-              for (int i = k + 1 + g; i < n; i += G) {
-                const double2 l = lv[i];
-                double2 v = b[i * ns + j];
-                v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
-                v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
-                b[i * ns + j] = v;
-              }
+            for (int i = k + 1 + g; i < n; i += G) {
+              const double2 l = lv[i];
+              double2 v = b[i * ns + j];
+              v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
+              v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
+              b[i * ns + j] = v;
             }
           }
+        };
+        static_assert(kKNmax - 2 < 256 - 32, "256 threads cover every trailing column");
+        if (NT < 256 && m >= NT - 32) {
+          for (int jj = tt; jj < m; jj += NT - 32) column(k + 2 + jj, 0, 1);
+        } else if (m > 0) {
+          const int G = (NT - 32) / m;
+          const int g = tt / m;
+          if (g < G) column(k + 2 + (tt - g * m), g, G);
+        }
       }
       __syncthreads();
     }
