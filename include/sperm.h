@@ -151,6 +151,13 @@ int sperm_rnw_stats(double* h_terms, double* h_fma_units, double* h_alu_ops, int
 /* Reduce accumulators mod the primes: out[r][q] = acc[r][q] mod p_q (device). */
 int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d_out, void* stream);
 
+/* Fold accumulators mod the primes IN PLACE: acc[r][q] := acc[r][q] mod p_q (device,
+ * asynchronous on `stream`).  d_job_acc of sperm_permanent gains < 2^31 per leaf and row, so a
+ * caller accumulating more than 2^32 leaves (PH Step 4's sum, over a long run) or
+ * summing accumulators over GPUs folds them first; the residues mod p_q are unchanged.
+ * Errors: SPERM_ERR_ARG (rows < 0, NULL d_acc). */
+int sperm_fold_mod(uint64_t* d_acc, int64_t rows, void* stream);
+
 /* ---------------------------------------------------------------- expansion */
 /* sperm_expand — one breadth-first level of Algorithm PH Step 2
  * (PAPER.md:161-174): every node (coef, A) of order n is split by Eq. (2)

@@ -1,7 +1,8 @@
 // kklll.cu — Algorithm KKLLL: approximate permanents used as the
 // job weights of the improved Step 3.
 //
-// One warp per (job, trial).  B lives in shared memory as two fp64 planes (re, im):
+// Per (job, trial): n < 28 one warp with B in registers (kklll_reg_kernel), else one CTA with
+// B in shared memory (kklll_smem_kernel).
 //   Step 1: B_ij = 0 where a_ij = 0, else the cube root of unity w_r, r = root_index(
 //           trial_key(seed, id, trial), i, j)  (counter-based SplitMix64; K1)
 //   Step 2: X = |det B|^2 by LU with partial pivoting (first maximal |b_ik|^2), every real
@@ -37,11 +38,13 @@ __device__ __forceinline__ int root_index(uint64_t key, uint64_t i, uint64_t j) 
 // elimination step instead of a full division per multiplier): q0 = RN(a y) is within one ulp
 // of a/d, r = a - q0 d is exact (FMA), and RN(q0 + r y) is the correctly rounded quotient
 // (Markstein's theorem), i.e. the same double as the reference's a / d.  The theorem needs no
-// over/underflow in the intermediates: d_ok (warp-uniform) and the |a| range select the plain
-// IEEE division otherwise.  A zero numerator returns a * y, which keeps the sign of a / d.
+// over/underflow in the intermediates: with |a| and d both in [2^-450, 2^450], a*y, q0 and the
+// quotient stay in [2^-901, 2^901], far from overflow and from the subnormal range, so q0 has no
+// double rounding; d_ok (warp-uniform) and the |a| range select the plain IEEE division
+// otherwise.  A zero numerator returns a * y, which keeps the sign of a / d.
 __device__ __forceinline__ bool div_range_ok(double v) {
   const double av = fabs(v);
-  return av >= 0x1p-900 && av <= 0x1p900;
+  return av >= 0x1p-450 && av <= 0x1p450;
 }
 __device__ __forceinline__ double div_by(double a, double d, double y, bool d_ok) {
   if (!d_ok || (a != 0.0 && !div_range_ok(a))) return __ddiv_rn(a, d);
@@ -49,84 +52,6 @@ __device__ __forceinline__ double div_by(double a, double d, double y, bool d_ok
   if (a == 0.0) return q0;
   const double r = __fma_rn(-q0, d, a);
   return __fma_rn(r, y, q0);
-}
-
-__global__ void kklll_trial_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
-                                   const int32_t* __restrict__ ids, int trials, uint64_t seed,
-                                   double* __restrict__ xout) {
-  extern __shared__ double ksm[];
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  double* re = ksm + (size_t)(threadIdx.x >> 5) * 2 * n * n;
-  double* im = re + n * n;
-  const double S32 = 0.8660254037844386;  // nearest double to sqrt(3)/2
-  const int64_t items = count * (int64_t)trials;
-  for (int64_t item = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); item < items;
-       item += (int64_t)gridDim.x * wpb) {
-    const int64_t job = item / trials;
-    const int trial = (int)(item % trials);
-    const int32_t* a = mats + job * (int64_t)n * n;
-    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
-    __syncwarp();
-    for (int e = lane; e < n * n; e += 32) {
-      const int i = e / n, j = e - (e / n) * n;
-      double r = 0.0, s = 0.0;
-      if (a[e] != 0) {
-        const int ri = root_index(key, (uint64_t)i, (uint64_t)j);
-        r = ri == 0 ? 1.0 : -0.5;
-        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
-      }
-      re[e] = r;
-      im[e] = s;
-    }
-    __syncwarp();
-    double x = 1.0;
-    for (int k = 0; k < n; ++k) {
-      // pivot: first row i >= k with maximal re^2 + im^2
-      double bm = -1.0;
-      int bi = n;
-      for (int i = k + lane; i < n; i += 32) {
-        const double m = __dadd_rn(__dmul_rn(re[i * n + k], re[i * n + k]), __dmul_rn(im[i * n + k], im[i * n + k]));
-        if (m > bm) { bm = m; bi = i; }  // ascending i per lane: strict > keeps the first
-      }
-      for (int o = 16; o; o >>= 1) {
-        const double om = __shfl_xor_sync(0xffffffffu, bm, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (om > bm || (om == bm && oi < bi)) { bm = om; bi = oi; }
-      }
-      const double d = bm;
-      if (d == 0.0) { x = 0.0; break; }
-      if (bi != k) {
-        for (int j = lane; j < n; j += 32) {
-          double t = re[k * n + j]; re[k * n + j] = re[bi * n + j]; re[bi * n + j] = t;
-          t = im[k * n + j]; im[k * n + j] = im[bi * n + j]; im[bi * n + j] = t;
-        }
-        __syncwarp();
-      }
-      x = __dmul_rn(x, d);
-      if (k + 1 == n) break;
-      const double pr = re[k * n + k], pi = im[k * n + k];
-      const double y = __drcp_rn(d);
-      const bool d_ok = div_range_ok(d);
-      for (int i = k + 1 + lane; i < n; i += 32) {
-        const double xr = re[i * n + k], xi = im[i * n + k];
-        re[i * n + k] = div_by(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d, y, d_ok);
-        im[i * n + k] = div_by(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d, y, d_ok);
-      }
-      __syncwarp();
-      const int w = n - k - 1;
-      for (int e = lane; e < w * w; e += 32) {
-        const int i = k + 1 + e / w, j = k + 1 + (e - (e / w) * w);
-        const double lr = re[i * n + k], li = im[i * n + k];
-        const double ur = re[k * n + j], ui = im[k * n + j];
-        if ((ur == 0.0 && ui == 0.0) || (lr == 0.0 && li == 0.0)) continue;  // see kk_update
-        re[i * n + j] = __dsub_rn(re[i * n + j], __dsub_rn(__dmul_rn(lr, ur), __dmul_rn(li, ui)));
-        im[i * n + j] = __dsub_rn(im[i * n + j], __dadd_rn(__dmul_rn(lr, ui), __dmul_rn(li, ur)));
-      }
-      __syncwarp();
-    }
-    if (lane == 0) xout[item] = x;
-  }
 }
 
 
@@ -218,7 +143,7 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
         for (int j = 1; j < NC; ++j) {  // j > k (static trip count keeps re/im in registers)
           if (j <= k) continue;
           const double2 u = prow[j];
-          if (u.x == 0.0 && u.y == 0.0) continue;  // sparse pivot row: see kk_update
+          if (u.x == 0.0 && u.y == 0.0) continue;  // sparse pivot row: see kklll_smem_kernel
           re[j] = __dsub_rn(re[j], __dsub_rn(__dmul_rn(lr, u.x), __dmul_rn(li, u.y)));
           im[j] = __dsub_rn(im[j], __dadd_rn(__dmul_rn(lr, u.y), __dmul_rn(li, u.x)));
         }
@@ -226,190 +151,6 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
       __syncwarp();
     }
     if (lane == 0) xout[item] = x;
-  }
-}
-
-// CTA-distributed register variant for 32 < n <= 8*CS, n <= 32*RL: one 256-thread CTA per
-// trial.  Thread (w, l) holds rows l + 32a (a < RL) and columns w + 8s (s < CS) of B in
-// registers.  Column k lives in warp k % 8, so the pivot search is one warp's REDUX; that warp
-// writes the pivot and the multipliers of every active row to shared memory (double-buffered),
-// the pivot row's entries reach the other warps by shuffles, and every thread updates its own
-// entries.  Look-ahead: during elimination step k the warp that owns column k+1 updates that
-// column first and then already chooses pivot k+1 and writes its multipliers, while the other
-// warps are still applying step k — one __syncthreads per step and the pivot search off the
-// critical path.  Same arithmetic on every entry, in the same order, and the same
-// first-maximum pivot rule (by position) as the reference, so values are bit-identical.
-template <int RL>
-__device__ __forceinline__ void kk_pivot(int k, int buf, const double (&cr)[RL], const double (&ci)[RL],
-                                         const int (&pos)[RL], const bool (&act)[RL], int l, double2* lbuf,
-                                         double* pivd, int* pivi) {
-  // pivot over the active rows: my rows, then the warp (hi/lo bit pattern, position)
-  double bm = -1.0;
-  int bpos = 0x7fffffff, ba = 0;
-#pragma unroll
-  for (int ra = 0; ra < RL; ++ra) {
-    if (act[ra]) {
-      const double m = __dadd_rn(__dmul_rn(cr[ra], cr[ra]), __dmul_rn(ci[ra], ci[ra]));
-      if (m > bm || (m == bm && pos[ra] < bpos)) { bm = m; bpos = pos[ra]; ba = ra; }
-    }
-  }
-  const bool any = bpos != 0x7fffffff;
-  const unsigned mh = any ? (unsigned)__double2hiint(bm) : 0u, ml = any ? (unsigned)__double2loint(bm) : 0u;
-  const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
-  const bool c1 = any && mh == bh;
-  const unsigned blo = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
-  const bool c2 = c1 && ml == blo;
-  const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)bpos : 0xffffffffu);
-  const int pl = __ffs(__ballot_sync(0xffffffffu, c2 && bpos == bp)) - 1;
-  const double d = __hiloint2double((int)bh, (int)blo);
-  const int pa = __shfl_sync(0xffffffffu, ba, pl);
-  double pr = 0.0, pi = 0.0;
-#pragma unroll
-  for (int ra = 0; ra < RL; ++ra)
-    if (ra == pa) { pr = cr[ra]; pi = ci[ra]; }
-  pr = __shfl_sync(0xffffffffu, pr, pl);
-  pi = __shfl_sync(0xffffffffu, pi, pl);
-  const int p = pl + 32 * pa;
-  // multipliers of the rows that stay active (position > k after the exchange)
-  if (d != 0.0) {
-    const double y = __drcp_rn(d);
-    const bool d_ok = div_range_ok(d);
-#pragma unroll
-    for (int ra = 0; ra < RL; ++ra) {
-      const int row = l + 32 * ra;
-      int np = pos[ra];
-      if (row == p) np = k;
-      else if (act[ra] && np == k) np = bp;
-      if (act[ra] && np > k) {
-        const double xr = cr[ra], xi = ci[ra];
-        lbuf[buf * 32 * RL + row] = make_double2(div_by(__dadd_rn(__dmul_rn(xr, pr), __dmul_rn(xi, pi)), d, y, d_ok),
-                                                 div_by(__dsub_rn(__dmul_rn(xi, pr), __dmul_rn(xr, pi)), d, y, d_ok));
-      }
-    }
-  }
-  if (l == 0) {
-    pivd[buf] = d;
-    pivi[2 * buf] = p;
-    pivi[2 * buf + 1] = bp;
-  }
-}
-
-// b_ij -= l_i * u_j on one column (my RL rows): u = the pivot row's entry, from lane `plane`
-template <int RL>
-__device__ __forceinline__ void kk_update(double (&cr)[RL], double (&ci)[RL], const double2 (&lm)[RL],
-                                          const bool (&act)[RL], int pa, int plane) {
-  double ur = 0.0, ui = 0.0;
-#pragma unroll
-  for (int ra = 0; ra < RL; ++ra)
-    if (ra == pa) { ur = cr[ra]; ui = ci[ra]; }
-  ur = __shfl_sync(0xffffffffu, ur, plane);
-  ui = __shfl_sync(0xffffffffu, ui, plane);
-  // u = 0 (the pivot row is sparse until fill-in): every b_ij - l_i * 0 is b_ij up to the sign
-  // of a zero, and a zero's sign never reaches a pivot magnitude |b|^2, a nonzero sum or the
-  // product of the d_k — so X is bit-identical with the update skipped (warp-uniform branch)
-  if (ur == 0.0 && ui == 0.0) return;
-#pragma unroll
-  for (int ra = 0; ra < RL; ++ra) {
-    if (act[ra]) {
-      cr[ra] = __dsub_rn(cr[ra], __dsub_rn(__dmul_rn(lm[ra].x, ur), __dmul_rn(lm[ra].y, ui)));
-      ci[ra] = __dsub_rn(ci[ra], __dadd_rn(__dmul_rn(lm[ra].x, ui), __dmul_rn(lm[ra].y, ur)));
-    }
-  }
-}
-
-template <int RL, int CS>
-__global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
-                                                           const int32_t* __restrict__ ids, int trials,
-                                                           uint64_t seed, double* __restrict__ xout) {
-  extern __shared__ double2 kfill[];  // [n*n] fill buffer, then lbuf[2][32*RL], piv[2]
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  double2* lbuf = kfill + n * n;
-  double* pivd = reinterpret_cast<double*>(lbuf + 2 * 32 * RL);  // [2] d
-  int* pivi = reinterpret_cast<int*>(pivd + 2);                    // [2][2] (row p, position bp)
-  const double S32 = 0.8660254037844386;
-  const int64_t items = count * (int64_t)trials;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int64_t job = item / trials;
-    const int trial = (int)(item % trials);
-    const int32_t* a = mats + job * (int64_t)n * n;
-    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
-    __syncthreads();  // previous trial done with the shared buffers
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e / n, j = e - (e / n) * n;
-      double r = 0.0, s = 0.0;
-      if (a[e] != 0) {
-        const int ri = root_index(key, (uint64_t)i, (uint64_t)j);
-        r = ri == 0 ? 1.0 : -0.5;
-        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
-      }
-      kfill[e] = make_double2(r, s);
-    }
-    __syncthreads();
-    double re[CS][RL], im[CS][RL];  // [column slot][row slot]
-    int pos[RL];
-    bool act[RL];
-#pragma unroll
-    for (int ra = 0; ra < RL; ++ra) {
-      const int row = l + 32 * ra;
-      pos[ra] = row;
-      act[ra] = row < n;
-#pragma unroll
-      for (int s = 0; s < CS; ++s) {
-        const int col = w + 8 * s;
-        double2 v = make_double2(0.0, 0.0);
-        if (row < n && col < n) v = kfill[row * n + col];
-        re[s][ra] = v.x;
-        im[s][ra] = v.y;
-      }
-    }
-    if (w == 0) kk_pivot<RL>(0, 0, re[0], im[0], pos, act, l, lbuf, pivd, pivi);  // pivot of step 0
-    __syncthreads();
-    double x = 1.0;
-    bool done = false;
-#pragma unroll
-    for (int sk = 0; sk < CS; ++sk) {
-      for (int wk = 0; wk < 8; ++wk) {
-        const int k = 8 * sk + wk;
-        if (done || k >= n) break;
-        const int buf = k & 1;
-        const double d = pivd[buf];
-        const int p = pivi[2 * buf], bp = pivi[2 * buf + 1];
-        if (d == 0.0) { x = 0.0; done = true; break; }
-        x = __dmul_rn(x, d);
-        if (k + 1 == n) { done = true; break; }
-#pragma unroll
-        for (int ra = 0; ra < RL; ++ra) {
-          const int row = l + 32 * ra;
-          if (row == p) pos[ra] = k;
-          else if (act[ra] && pos[ra] == k) pos[ra] = bp;
-          act[ra] = act[ra] && pos[ra] > k;
-        }
-        const int pa = p >> 5, plane = p & 31;
-        double2 lm[RL];
-#pragma unroll
-        for (int ra = 0; ra < RL; ++ra)
-          lm[ra] = act[ra] ? lbuf[buf * 32 * RL + l + 32 * ra] : make_double2(0.0, 0.0);
-        // look-ahead: column k+1 first in its warp, then pivot k+1 (warp-uniform branches)
-        const int w1 = (wk + 1) & 7;
-        if (w == w1) {
-          if (wk < 7) {
-            kk_update<RL>(re[sk], im[sk], lm, act, pa, plane);
-            kk_pivot<RL>(k + 1, buf ^ 1, re[sk], im[sk], pos, act, l, lbuf, pivd, pivi);
-          } else if (sk + 1 < CS) {
-            kk_update<RL>(re[sk + 1], im[sk + 1], lm, act, pa, plane);
-            kk_pivot<RL>(k + 1, buf ^ 1, re[sk + 1], im[sk + 1], pos, act, l, lbuf, pivd, pivi);
-          }
-        }
-#pragma unroll
-        for (int s = 0; s < CS; ++s) {
-          if (w + 8 * s <= k) continue;                          // finished columns
-          if (w == w1 && s == (wk < 7 ? sk : sk + 1)) continue;  // column k+1: done above
-          kk_update<RL>(re[s], im[s], lm, act, pa, plane);
-        }
-        __syncthreads();
-      }
-    }
-    if (threadIdx.x == 0) xout[item] = x;
   }
 }
 
@@ -421,8 +162,10 @@ __global__ void __launch_bounds__(256, 1) kklll_cta_kernel(const int32_t* __rest
 // multipliers l_i go to a shared vector (one reciprocal per step + Markstein, div_by), and
 // the m x m trailing block is updated by all threads (thread = (row group, column): contiguous
 // 16-byte accesses, the multiplier a broadcast).  Same operations in the same order as the
-// oracle on every entry, so X is bit-identical; updates by a zero pivot-row entry are skipped
-// (see kk_update).
+// oracle on every entry, so X is bit-identical.  Updates by a zero pivot-row entry u = 0 are
+// skipped (the pivot row is sparse until fill-in): every b_ij - l_i * 0 is b_ij up to the sign
+// of a zero, and a zero's sign never reaches a pivot magnitude |b|^2, a nonzero sum or the
+// product of the d_k — so X is bit-identical with the update skipped.
 // pivot of column k (rows >= k): first row with maximal re^2 + im^2 — per lane ascending with a
 // strict >, then a (larger value, then smaller row) butterfly; lane 0 publishes it
 __device__ __forceinline__ void pivot_reduce(double bm, int bi, int lane, double& s_d, int& s_p) {
@@ -602,7 +345,7 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     TimingScope ts("kklll", st);
     count_launch();
     kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
-  } else if (!getenv("SPERM_KKLLL_CTA")) {
+  } else {
     // shared-memory-resident LU, one 256-thread CTA per trial, as many trials per SM as fit
     // (measured on the fullerene-96 jobs: 128 threads 1.37 s, 256 1.31 s, 512 1.97 s)
     // (128-thread CTAs below order SPERM_KKLLL_T128_MAX: more trials per SM, cheaper barriers)
@@ -627,35 +370,6 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     TimingScope ts("kklll", st);
     count_launch();
     kern<<<(unsigned)grid, nt, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
-  } else if (n <= 96) {
-    // A-B (SPERM_KKLLL_CTA=1): CTA-distributed registers: rows per lane RL = ceil(n/32), column
-    // slots per thread CS = ceil(n/8)
-    const int CSn = (n + 7) / 8;
-    auto kern = n <= 64 ? kklll_cta_kernel<2, 8> : CSn <= 9 ? kklll_cta_kernel<3, 9>
-                                             : CSn <= 10 ? kklll_cta_kernel<3, 10> : kklll_cta_kernel<3, 12>;
-    const int RLn = n <= 64 ? 2 : 3;
-    const size_t smem = sizeof(double2) * ((size_t)n * n + 2 * 32 * RLn) + 2 * sizeof(double) + 4 * sizeof(int);
-    SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
-    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
-    grid = std::max<int64_t>(1, std::min(grid, items));
-    TimingScope ts("kklll", st);
-    count_launch();
-    kern<<<(unsigned)grid, 256, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
-  } else {
-    const size_t per_warp = sizeof(double) * 2 * n * n;
-    int wpb = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp));
-    const size_t smem = per_warp * wpb;
-    SPERM_CUDA(cudaFuncSetAttribute(kklll_trial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_trial_kernel, wpb * 32, smem));
-    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
-    const int64_t need = (items + wpb - 1) / wpb;
-    if (grid > need) grid = need;
-    TimingScope ts("kklll", st);
-    count_launch();
-    kklll_trial_kernel<<<(unsigned)grid, wpb * 32, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   }
   cudaError_t le = cudaGetLastError();
   if (le == cudaSuccess) {

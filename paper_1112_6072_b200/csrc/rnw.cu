@@ -858,6 +858,12 @@ __global__ void reduce_mod_kernel(const unsigned long long* __restrict__ acc, in
   out[idx] = (uint32_t)(acc[idx] % (unsigned long long)c_p[idx % SPERM_KMAX]);
 }
 
+__global__ void fold_mod_kernel(unsigned long long* __restrict__ acc, int64_t rows) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * SPERM_KMAX) return;
+  acc[idx] %= (unsigned long long)c_p[idx % SPERM_KMAX];
+}
+
 // evaluation-order leaf ids, their plan keys, and per key: leaves, sum of k (primes) and sum
 // of k * mexp (Montgomery products per block value, summed over primes: the op model's input)
 __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order, const int2* __restrict__ meta,
@@ -1413,6 +1419,16 @@ extern "C" int sperm_reduce_mod(const uint64_t* d_acc, int64_t rows, uint32_t* d
   reduce_mod_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       (const unsigned long long*)d_acc, rows, d_out);
   SPERM_LAUNCH_CHECK("reduce_mod_kernel");
+  return SPERM_OK;
+}
+
+extern "C" int sperm_fold_mod(uint64_t* d_acc, int64_t rows, void* stream) {
+  if (rows < 0 || (rows > 0 && !d_acc)) return set_error(SPERM_ERR_ARG, "sperm_fold_mod: bad args");
+  if (rows == 0) return SPERM_OK;
+  const int64_t tot = rows * SPERM_KMAX;
+  count_launch();
+  fold_mod_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>((unsigned long long*)d_acc, rows);
+  SPERM_LAUNCH_CHECK("fold_mod_kernel");
   return SPERM_OK;
 }
 

@@ -235,6 +235,10 @@ def dynamic_chunks(order, chunk: int, store, key: str):
 
 _dynamic_calls = 0
 
+# leaves added to the accumulators between folds: each adds < 2^31 to its job row and to the
+# total row, so 2^32 leaves keep every uint64 entry below 2^63
+FOLD_EVERY = 1 << 32
+
 
 def allreduce_accumulators(acc, group=None):
     """Algorithm PH Step 4 across GPUs: one SUM all-reduce of the
@@ -254,7 +258,8 @@ def reconstruct(res, k: int):
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
               device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30,
-              assignment: str = "static", store=None, dynamic_chunk: int = 0) -> PHResult:
+              assignment: str = "static", store=None, dynamic_chunk: int = 0,
+              fold_every: int = FOLD_EVERY) -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
 
     With a torch.distributed `group` of world size G, every rank replicates the
@@ -262,7 +267,10 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     evaluates only the jobs assigned to it, and one all-reduce sums the residue accumulators.
     assignment="static": the LPT plan of sperm_schedule (S1); "dynamic": ranks claim chunks of
     the policy's job order from a shared counter in `store` (default: the process group's
-    store) as they finish — the paper's first-free-processor rule across GPUs."""
+    store) as they finish — the paper's first-free-processor rule across GPUs.
+    The uint64 accumulators gain < 2^31 per leaf, so they are folded mod p (sperm_fold_mod)
+    before more than `fold_every` leaves have been added since the last fold, and before the
+    all-reduce (so the sum over ranks stays below 2^64)."""
     import torch
     import torch.distributed as dist
     rank, world = (dist.get_rank(group), dist.get_world_size(group)) if group is not None else (0, 1)
@@ -333,6 +341,7 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
                     yield s, mine
 
     dynamic = assignment == "dynamic" and (world > 1 or store is not None)
+    since_fold = 0
     for s, sel in (dynamic_batches() if dynamic else static_batches()):
         idx = torch.tensor(sel, dtype=torch.int64, device=device)
         batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx),
@@ -341,6 +350,11 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             if lv.n > S.NMAX:
                 raise S.SpermError(S.ERR_ARG, f"leaf of order {lv.n} > {S.NMAX} (s >= 5 node)")
             stats["leaf_sets"] += 1
+            if since_fold + lv.count > fold_every:  # keep every accumulator below 2^63
+                S.sperm_fold_mod(acc, stream=rnw_stream)
+                stats["folds"] = stats.get("folds", 0) + 1
+                since_fold = 0
+            since_fold += lv.count
             t_r = time.perf_counter()
             rnw_stream.wait_stream(main)  # the leaves were written on the main stream
             for t in (lv.mats, lv.coef, lv.job):
@@ -356,6 +370,8 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             stats["rnw_host_s"] += time.perf_counter() - t_r
             leaves += lv.count
             terms += S.sperm_rnw_terms(lv.n, lv.count)
+    if world > 1:
+        S.sperm_fold_mod(acc, stream=rnw_stream)  # each rank's rows < 2^31: the G-rank sum fits
     main.wait_stream(rnw_stream)
     stats["t_loop_s"] = time.perf_counter() - t_loop
     allreduce_accumulators(acc, group)

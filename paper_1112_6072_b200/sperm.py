@@ -47,6 +47,7 @@ _SIGS = {
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
     "sperm_rnw_stats": (_I, [_P, _P, _P, _I]),
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
+    "sperm_fold_mod": (_I, [_P, _I64, _P]),
     "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "sperm_expand_stats": (_I, [_P, _P, _I]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
@@ -183,6 +184,15 @@ def sperm_reduce_mod(acc, stream=None):
     out = torch.empty((rows, KMAX), dtype=torch.int32, device=acc.device)
     _check(lib().sperm_reduce_mod(_ptr(acc), rows, _ptr(out), _stream(stream)))
     return out
+
+
+def sperm_fold_mod(acc, stream=None):
+    """acc[r][q] %= p_q in place (uint64 accumulators stored as int64)."""
+    import torch
+    if not (isinstance(acc, torch.Tensor) and acc.is_cuda and acc.dtype == torch.int64 and acc.is_contiguous()):
+        raise TypeError("expected a contiguous int64 CUDA tensor")
+    _check(lib().sperm_fold_mod(_ptr(acc), int(acc.shape[0]), _stream(stream)))
+    return acc
 
 
 def residues_to_ints_device(res, k, stream=None) -> List[int]:

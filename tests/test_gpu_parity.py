@@ -210,9 +210,9 @@ def test_kklll_bit_exact_trials():
             assert abs(float(est[j]) - e) <= 1e-12 * abs(e)
 
 
-@pytest.mark.parametrize("n", [33, 36, 39, 47, 64, 65, 77, 96, 100])
+@pytest.mark.parametrize("n", [25, 26, 27, 28, 29, 30, 31, 32, 33, 36, 39, 47, 64, 65, 77, 96, 100, 112])
 def test_kklll_bit_exact_large_orders(n):
-    """Shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
+    """Register kernel (n < 28, SPERM_KKLLL_SMEM_MIN) and shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
     threads), 128 (n < 48) and 256 threads (SPERM_KKLLL_T64_MAX / _T128_MAX move the bounds):
     every trial bit-identical to the oracle, including singular (zero) trials (24 trials:
     ~1e4-1e5 multiplier quotients per order through the reciprocal-based division)."""
@@ -310,6 +310,38 @@ def test_pipeline_dynamic_assignment_single_rank():
     assert r2.job_values == r1.job_values
 
 
+def test_pipeline_c60_l32_every_job():
+    """configs[2] as the bench runs it: C60, J >= 992 jobs, leaves of order <= 32 — every one of
+    the job values equals the oracle's (Python pre-expansion, per job by the C frontier DP)."""
+    from oracle.cfrontier import narrow_order, per_frontier_c
+    a = truncated_icosahedron()
+    r = pipeline.permanent(a, jobs_at_least=992, leaf_order=32)
+    assert r.value == golden("C60_truncated_icosahedron")
+    jobs = pre_expand(a, jobs_at_least=992)
+    assert r.num_jobs == len(jobs)
+    want = []
+    for c, m, k in jobs:
+        d = np.array(to_dense(m, k), dtype=np.int64)
+        want.append(c * per_frontier_c(d, narrow_order(d)))
+    assert r.job_values == want
+
+
+def test_pipeline_fold_every_leaf_set():
+    """The uint64 accumulators folded mod p (sperm_fold_mod) before every leaf set: the same
+    per-job values and total as without folding."""
+    a = truncated_icosahedron()
+    r1 = pipeline.permanent(a, jobs_at_least=128, leaf_order=20)
+    r2 = pipeline.permanent(a, jobs_at_least=128, leaf_order=20, fold_every=1)
+    assert r2.stats.get("folds", 0) >= 2
+    assert r1.value == r2.value == golden("C60_truncated_icosahedron")
+    assert r1.job_values == r2.job_values
+    acc = torch.tensor([[2**63 + 5] * 8, [123] * 8], dtype=torch.uint64).view(torch.int64).cuda()
+    P.sperm_fold_mod(acc)
+    got = acc.cpu().view(torch.uint64).numpy().astype(object)
+    for q in range(P.KMAX):
+        assert int(got[0, q]) == (2**63 + 5) % P.sperm_prime(q) and int(got[1, q]) == 123
+
+
 def test_pipeline_c60_leaf16():
     a = truncated_icosahedron()
     r = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
@@ -399,6 +431,60 @@ def test_rnw_many_primes_every_plan(wmax):
         res, k = P.sperm_permanent(dev(a[None]))
         assert int(k[0]) >= 4
         _plans_agree(a[None], [h_per(a)])
+
+
+def _forced(mats, plan_min):
+    os.environ["SPERM_RNW_PLAN_MIN"] = plan_min
+    try:
+        return gpu_per(mats)
+    finally:
+        os.environ.pop("SPERM_RNW_PLAN_MIN", None)
+
+
+@pytest.mark.parametrize("n", [27, 30, 33, 36, 40])
+def test_rnw_per_leaf_orders_27_to_40_every_fixed_width(n):
+    """Leaves of orders 27-40, one by one against the C frontier DP.  With a plan forced to few
+    low columns (SPERM_RNW_PLAN_MIN: plan 8 = B 1, plan 12 = B 2 with pairs; plan 6 = B 3) the
+    fixed rows n - 3B select the wide fixed-row tables: NFIX 24 (n - 3B <= 24), 32 and 40;
+    the default plan (B = 8) covers NFIX 4-16.  Signed weights on two of the leaves."""
+    from oracle.cfrontier import narrow_order, per_frontier_c
+    rng = np.random.default_rng(1000 + n)
+    mats = [random_3perm(n, rng) for _ in range(3)]
+    mats[1] = mats[1] * rng.integers(1, 4, size=(n, n))
+    mats[2] = mats[2] * rng.choice([-2, -1, 1, 3], size=(n, n))
+    mats = np.array(mats)
+    want = [per_frontier_c(m, narrow_order(m)) for m in mats]
+    assert gpu_per(mats) == want
+    for plan_min in ("6", "8", "12"):
+        assert _forced(mats, plan_min) == want, plan_min
+    if n <= 30:
+        assert _forced(mats, "0") == want  # the generic kernel
+
+
+def test_rnw_per_leaf_c60_l32_leaves():
+    """Order-32 leaves of configs[2] (C60 expanded to J >= 992 jobs; merged entries), one by one
+    against the frontier DP, under the default plan and forced narrow plans."""
+    from oracle.cfrontier import narrow_order, per_frontier_c
+    a = truncated_icosahedron()
+    sets = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=992)
+    s = [x for x in sets if x.n == 32][0]
+    idx = torch.arange(0, s.count, max(1, s.count // 12), device="cuda")[:12]
+    mats = s.mats.index_select(0, idx).cpu().numpy().astype(np.int64)
+    want = [per_frontier_c(m, narrow_order(m)) for m in mats]
+    assert gpu_per(mats) == want
+    for plan_min in ("4", "8", "12"):
+        assert _forced(mats, plan_min) == want, plan_min
+
+
+@pytest.mark.parametrize("n", [44, 48])
+def test_rnw_per_leaf_max_orders(n):
+    """The largest leaves (SPERM_NMAX = 48: 2^47 Gray-code terms), one 3-regular and one
+    weighted, against the frontier DP."""
+    from oracle.cfrontier import narrow_order, per_frontier_c
+    rng = np.random.default_rng(2000 + n)
+    mats = np.array([random_3perm(n, rng), random_3perm(n, rng) * rng.integers(1, 3, size=(n, n))])
+    want = [per_frontier_c(m, narrow_order(m)) for m in mats]
+    assert gpu_per(mats) == want
 
 
 def test_crt_device_matches_host():

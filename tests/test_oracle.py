@@ -178,6 +178,30 @@ def test_paper_t12_transcription():
     assert len(vals) == 159 and sum(vals) == total == int(_pins()["per_C100"])
 
 
+def test_c_frontier_pins():
+    """oracle/frontier.c: per(C100) = Table T12's Total in C (a few seconds), under
+    two row orders; = brute force on small signed matrices (zero rows/columns, n = 0..8); = the
+    Python DP on 3-regular n = 20; the closed forms per(J_n) = n!, per(J_n - I_n) = D_n."""
+    from oracle.cfrontier import narrow_order, per_frontier_c
+    from oracle.frontier import bfs_order
+    c100 = paper_graph("C100")
+    assert per_frontier_c(c100, bfs_order(c100)) == int(_pins()["per_C100"])
+    assert per_frontier_c(c100, narrow_order(c100)) == int(_pins()["per_C100"])
+    rng = np.random.default_rng(77)
+    for _ in range(60):
+        n = int(rng.integers(0, 9))
+        a = rng.integers(-3, 4, size=(n, n)) * (rng.random((n, n)) < 0.5)
+        order = rng.permutation(n)
+        assert per_frontier_c(a, order) == per_bruteforce(a)
+    for a in random_3perm_batch(3, 20, seed=5):
+        assert per_frontier_c(a, narrow_order(a)) == per_frontier(a)
+    for n in (1, 5, 9, 12):
+        j = np.ones((n, n), dtype=np.int64)
+        d = sum((-1) ** k * math.factorial(n) // math.factorial(k) for k in range(n + 1))
+        assert per_frontier_c(j) == math.factorial(n)
+        assert per_frontier_c(j - np.eye(n, dtype=np.int64)) == d
+
+
 @pytest.mark.slow
 def test_c60_two_constructions_agree():
     """Appendix C60 and the truncated icosahedron are the
