@@ -7,10 +7,15 @@ permutation matrices (half 0/1, half with nonzeros uniform in [1,7]); "direct ba
 R-NW, no expansion".  One step = the persistent R-NW kernels over all 256 x 2^23
 Gray-code terms in exact multi-prime arithmetic -> residues (then D2H + host CRT of the
 256 exact permanents, inside the e2e timing).
-Metric: Gray-code terms per second (whole job, all ranks).  Under torchrun each rank
-evaluates its own seeded batch of 256 (weak scaling, no data-path collective).
-The JSON line also carries `ph`: the whole path (expansion, KKLLL, LPT, R-NW, CRT) timed
-on configs[2], per(C60), with per-stage device times.
+Metric: Gray-code terms per second (whole job, all ranks).  With --gpus N > 1 the script
+re-launches itself under torch.distributed.run (one process per GPU, NCCL) unless WORLD_SIZE is
+already set; each rank evaluates its own seeded batch of 256 (weak scaling, no data-path
+collective) for `value`, and the line adds `strong_scaling`: configs[4] (the n = 96 spiral
+fullerene and random 3-regular matrix) through pipeline.permanent over the NCCL group — per(A)
+wall time on N GPUs (device events, max over ranks) per scheduling policy, against the same
+job on rank 0 alone, with the exact per(A) checked against the oracle's golden value.
+At N = 1 the line carries `ph` (configs[2], per(C60)), `configs4` (both n = 96 permanents,
+1 GPU), `ph_c100` (the paper's C100 case study) and the roofline / cpu_baseline blocks.
 """
 from __future__ import annotations
 
@@ -42,6 +47,9 @@ def parse():
     ap.add_argument("--no-ph", action="store_true", help="skip the whole-path per(C60) measurement")
     ap.add_argument("--ph-leaf", type=int, default=32, help="leaf order L of the per(C60) run")
     ap.add_argument("--no-c100", action="store_true", help="skip the per(C100) run (the paper's case study)")
+    ap.add_argument("--no-strong", action="store_true", help="skip the configs[4] runs (strong scaling at N > 1)")
+    ap.add_argument("--strong-jobs", type=int, default=160, help="configs[4]: PH jobs (jobs_at_least)")
+    ap.add_argument("--strong-leaf", type=int, default=16, help="configs[4]: leaf order L")
     return ap.parse_args()
 
 
@@ -94,13 +102,41 @@ def peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: start N ranks on this node (torch.distributed.run,
+    rendezvous on 127.0.0.1) running this script with the same arguments."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def device_index(local: int) -> int:
+    """LOCAL_RANK's GPU.  SPERM_BENCH_SHARE_DEVICE=1 maps every rank to GPU local % count (a
+    functional check of the N > 1 path on a one-GPU box with SPERM_BENCH_BACKEND=gloo; its
+    timings mean nothing); otherwise one GPU per rank, and too few GPUs is an error."""
+    import torch
+    cnt = torch.cuda.device_count()
+    if os.environ.get("SPERM_BENCH_SHARE_DEVICE") == "1":
+        return local % max(cnt, 1)
+    if local >= cnt:
+        raise RuntimeError(f"rank with LOCAL_RANK={local} but only {cnt} visible GPU(s)")
+    return local
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, max(world, args.gpus))
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -108,10 +144,15 @@ def main():
     import paper_1112_6072_b200 as P
     from workloads import random_3perm_batch
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    didx = device_index(local)
+    torch.cuda.set_device(didx)
+    dev = torch.device("cuda", didx)
+    backend = os.environ.get("SPERM_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     # each rank: its own seeded batch (rank 0 is exactly configs[1])
     h_np = random_3perm_batch(N_MATS, ORDER, seed=SEED + rank)
     h_mats = torch.tensor(h_np, dtype=torch.int32).pin_memory()
@@ -134,7 +175,7 @@ def main():
         vals = finish(*step(d_mats))
     # device-timed region: K steps, L2 flushed before each (outside the events)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(didx)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -171,7 +212,8 @@ def main():
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_total = sum(e2e_ms)
     if world > 1:
-        t = torch.tensor([total_ms, e2e_total, rnw_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms, e2e_total, rnw_ms], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, e2e_total, rnw_ms = [float(x) for x in t.cpu()]
     terms_step = P.sperm_rnw_terms(ORDER, N_MATS) * world
@@ -217,6 +259,13 @@ def main():
         "clocks": clocks,
         "check": {"per_first": str(vals[0]), "per_last": str(vals[-1])},
     }
+    if world > 1 and not args.no_strong:
+        out["strong_scaling"] = bench_strong(P, torch, dist, rank, world, dev, args.strong_jobs, args.strong_leaf)
+    if rank == 0 and world == 1 and not args.no_strong:
+        try:
+            out["configs4"] = bench_configs4(P, torch, args.strong_jobs, args.strong_leaf)
+        except Exception as e:
+            out["configs4"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_ph:
         out["ph"] = bench_ph(P, torch, leaf_order=args.ph_leaf)
     if rank == 0 and world == 1 and not args.no_ph:
@@ -235,6 +284,98 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def configs4_workloads():
+    """configs[4]: the seeded n = 96 spiral fullerene (isomer 0) and the n = 96 union of three
+    disjoint random permutation matrices (PCG64([2024, 96])), with their oracle golden values."""
+    import numpy as np
+    from workloads import random_3perm, random_fullerene
+    rng = np.random.default_rng(np.random.PCG64([2024, 96]))
+    return [("fullerene_n96_seed2024_iso0", random_fullerene(96, 2024, 0)[0]),
+            ("random3reg_n96_seed2024_96", random_3perm(96, rng))]
+
+
+def golden_value(name):
+    try:
+        for ln in open(os.path.join(ROOT, "tests", "golden", "oracle_values.txt")):
+            if ln.startswith(name + " "):
+                return int(ln.split()[1])
+    except OSError:
+        pass
+    return None
+
+
+def _timed_permanent(torch, pipeline, a, **kw):
+    """pipeline.permanent between two CUDA events on the current stream (device time of the
+    whole call, host gaps included) and a synchronize on both sides."""
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    r = pipeline.permanent(a, **kw)
+    e1.record(st)
+    torch.cuda.synchronize()
+    return r, e0.elapsed_time(e1) * 1e-3
+
+
+def bench_configs4(P, torch, jobs, leaf):
+    """configs[4] on one GPU: per(A) wall time of both n = 96 matrices (estimate-LPT order),
+    exact values against the oracle's (tests/golden/oracle_values.txt)."""
+    from paper_1112_6072_b200 import pipeline
+    out = {}
+    for name, a in configs4_workloads():
+        r, t = _timed_permanent(torch, pipeline, a, jobs_at_least=jobs, leaf_order=leaf)
+        g = golden_value(name)
+        out[name] = {"per": str(r.value), "matches_oracle_golden": (r.value == g) if g is not None else None,
+                     "wall_s_device": t, "jobs": r.num_jobs, "leaves": r.leaves, "terms": r.terms}
+    out["config"] = f"J >= {jobs} PH jobs, leaves of order <= {leaf}, estimate-LPT, 1 GPU"
+    return out
+
+
+def bench_strong(P, torch, dist, rank, world, dev, jobs, leaf):
+    """configs[4] strong scaling: each n = 96 matrix through pipeline.permanent on the whole
+    group (improved Step 3 across the GPUs, NCCL estimate / residue all-reduces), per policy:
+    estimate-LPT static (the paper's contribution, reading S1), estimate dynamic (chunks of the
+    estimate order claimed as ranks free up), size-LPT, natural and random order (static).
+    T_1 = the same job on rank 0 alone (group=None) while the others wait; T_N = device time of
+    the group run, max over ranks; efficiency = T_1 / (N T_N) (Tables 5-7's definition,
+    PAPER.md:736-790).  Every group run's per(A) is checked against the golden value."""
+    import torch.distributed as dist_
+    from paper_1112_6072_b200 import pipeline
+    pg = dist_.group.WORLD
+    policies = [("estimate", "static"), ("estimate", "dynamic"), ("size", "static"), ("natural", "static"),
+                ("random", "static")]
+    res = {"config": f"configs[4]: J >= {jobs} PH jobs, leaves of order <= {leaf}; {world} ranks",
+           "timing": "device time (CUDA events around the whole call on each rank), max over ranks",
+           "workloads": {}}
+    from workloads import dodecahedron
+    pipeline.permanent(dodecahedron(), jobs_at_least=8, leaf_order=12, group=pg)  # warm-up, all ranks
+    for name, a in configs4_workloads():
+        g = golden_value(name)
+        w = {"golden": str(g) if g is not None else None}
+        t1 = torch.zeros(1, dtype=torch.float64, device=dev)
+        dist.barrier()
+        if rank == 0:
+            r1, t = _timed_permanent(torch, pipeline, a, jobs_at_least=jobs, leaf_order=leaf)
+            t1[0] = t
+            w["per_1gpu"] = str(r1.value)
+            w["jobs"] = r1.num_jobs
+        dist.barrier()
+        pipeline._allreduce_sum(t1, pg)
+        w["T1_s"] = float(t1[0])
+        for pol, asg in policies:
+            dist.barrier()
+            r, t = _timed_permanent(torch, pipeline, a, jobs_at_least=jobs, leaf_order=leaf, policy=pol,
+                                    group=pg, assignment=asg)
+            tt = torch.tensor([t], dtype=torch.float64, device=dev if dist.get_backend(pg) == "nccl" else "cpu")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tn = float(tt[0])
+            w[f"{pol}_{asg}"] = {"TN_s": tn, "efficiency": w["T1_s"] / (world * tn) if tn else None,
+                                 "speedup": w["T1_s"] / tn if tn else None, "per": str(r.value),
+                                 "exact": (r.value == g) if g is not None else None}
+        res["workloads"][name] = w
+    return res
 
 
 def bench_expand(P, torch, jobs_at_least: int = 200000, reps: int = 3):

@@ -192,6 +192,12 @@ int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32
                  int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
                  int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
 
+/* sperm_nnz — number of nonzero entries of each node (device, asynchronous): d_out[m] =
+ * |{(i, j) : a_ij != 0}| of matrix m of d_mats [count][n][n].  The "size" scheduling key the
+ * load-balance comparison orders jobs by (the paper's alternatives to the estimate order:
+ * natural order, and the size regressors of PAPER.md:293-349).  Errors: SPERM_ERR_ARG. */
+int sperm_nnz(const int32_t* d_mats, int n, int64_t count, int64_t* d_out, void* stream);
+
 /* Cumulative algorithmic traffic of the completed sperm_expand calls since the last reset
  * (host): bytes = every parent read once + every child / early node written once (matrix,
  * coefficient, job id); nodes = parents processed.  For the HBM roofline of the expansion.
@@ -227,6 +233,16 @@ int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d
  *  h_loads [machines] double out (planned loads, may be NULL). */
 int sperm_schedule(const double* h_weights, int64_t count, int machines, int policy,
                    uint64_t seed, int32_t* h_machine, int32_t* h_order, double* h_loads);
+
+/* ---------------------------------------------------------------- statistics */
+/* sperm_kendall_tau — Kendall's rank correlation of (x_i, y_i), i < m, with the tie correction
+ * of Eq. (10) (Eqs. (7)-(9)): S = sum_{i<j} sign(x_j - x_i) sign(y_j - y_i),
+ * T / U = pairs tied in x / in y, tau = S / (sqrt(m(m-1)/2 - T) sqrt(m(m-1)/2 - U)); NaN if a
+ * ranking is constant.  The paper's measure of how well a key (estimate, permanent, size)
+ * ranks the measured job times (Tables 2-4).  Host, synchronous, O(m log m).
+ *  h_x, h_y  [m] double (host); h_tau out; h_counts [4] int64 out or NULL: S, T, U, m(m-1)/2.
+ * Errors: SPERM_ERR_ARG (m < 0, NULL, NaN input). */
+int sperm_kendall_tau(const double* h_x, const double* h_y, int64_t m, double* h_tau, int64_t* h_counts);
 
 /* ---------------------------------------------------------------- timing */
 /* Number of libsperm kernels launched (its own kernels; CUB scans/sorts it calls are not

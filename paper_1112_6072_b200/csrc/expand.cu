@@ -478,10 +478,35 @@ __global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
   }
 }
 
+// nonzeros of each node (one warp per node, coalesced 4-byte loads, warp-sum): the "size" key of
+// the load-balance comparison (the paper's |D| / S regressors, Tables 5-7's
+// alternatives to the estimate order)
+__global__ void nnz_kernel(const int32_t* __restrict__ mats, int n, int64_t count, int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= count) return;
+  const int32_t* m = mats + w * (int64_t)n * n;
+  int c = 0;
+  for (int e = lane; e < n * n; e += 32) c += m[e] != 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) out[w] = c;
+}
+
 }  // namespace
 }  // namespace sperm
 
 using namespace sperm;
+
+extern "C" int sperm_nnz(const int32_t* d_mats, int n, int64_t count, int64_t* d_out, void* stream) {
+  if (n < 0 || n > SPERM_EXPAND_NMAX || count < 0) return set_error(SPERM_ERR_ARG, "sperm_nnz: bad sizes");
+  if (count == 0) return SPERM_OK;
+  if (!d_out || (n > 0 && !d_mats)) return set_error(SPERM_ERR_ARG, "sperm_nnz: NULL pointer");
+  count_launch();
+  nnz_kernel<<<(unsigned)((count + 7) / 8), 256, 0, (cudaStream_t)stream>>>(d_mats, n, count, d_out);
+  const cudaError_t le = cudaGetLastError();
+  return le == cudaSuccess ? SPERM_OK : cuda_check(le, "nnz_kernel");
+}
 
 static std::mutex g_exp_mu;
 static double g_exp_bytes = 0.0, g_exp_nodes = 0.0;

@@ -1,5 +1,6 @@
 // host.cu — host-side parts of libsperm.so: errors, primes, CRT (Garner),
 // the improved Step 3 scheduler and the kernel timing registry.
+#include <cmath>
 #include <algorithm>
 #include <cstring>
 #include <atomic>
@@ -319,6 +320,70 @@ int sperm_schedule(const double* h_weights, int64_t count, int machines, int pol
   }
   if (h_loads)
     for (int m = 0; m < machines; ++m) h_loads[m] = loads[m];
+  return SPERM_OK;
+}
+
+// ------------------------------------------------------------------ Kendall tau
+// Kendall's rank correlation with the tie correction of Eq. (10), in
+// O(m log m): sort the pairs by (x, y); S = concordant - discordant pairs = P0 - T - U + W - 2 D
+// with P0 = m(m-1)/2 pairs, T / U = pairs tied in x / in y (Eqs. (8), (9)), W = pairs tied in
+// both, and D = discordant pairs = inversions of the y sequence (in (x, y) order), counted by
+// a bottom-up merge sort.  Every count is an exact int64.
+int sperm_kendall_tau(const double* h_x, const double* h_y, int64_t m, double* h_tau, int64_t* h_counts) {
+  if (m < 0 || (m > 0 && (!h_x || !h_y)) || !h_tau) return set_error(SPERM_ERR_ARG, "sperm_kendall_tau: bad arguments");
+  for (int64_t i = 0; i < m; ++i)
+    if (std::isnan(h_x[i]) || std::isnan(h_y[i])) return set_error(SPERM_ERR_ARG, "sperm_kendall_tau: NaN input");
+  std::vector<int64_t> idx(m);
+  for (int64_t i = 0; i < m; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+    return h_x[a] != h_x[b] ? h_x[a] < h_x[b] : h_y[a] < h_y[b];
+  });
+  const int64_t P0 = m * (m - 1) / 2;
+  int64_t T = 0, W = 0;
+  for (int64_t i = 0; i < m;) {  // runs of equal x, and within them runs of equal (x, y)
+    int64_t j = i;
+    while (j < m && h_x[idx[j]] == h_x[idx[i]]) ++j;
+    T += (j - i) * (j - i - 1) / 2;
+    for (int64_t a = i; a < j;) {
+      int64_t b = a;
+      while (b < j && h_y[idx[b]] == h_y[idx[a]]) ++b;
+      W += (b - a) * (b - a - 1) / 2;
+      a = b;
+    }
+    i = j;
+  }
+  std::vector<double> y(m), tmp(m);
+  for (int64_t i = 0; i < m; ++i) y[i] = h_y[idx[i]];
+  int64_t D = 0;  // strict inversions y[i] > y[j], i < j (equal y are not discordant)
+  for (int64_t w = 1; w < m; w *= 2) {
+    for (int64_t lo = 0; lo < m; lo += 2 * w) {
+      const int64_t mid = std::min(lo + w, m), hi = std::min(lo + 2 * w, m);
+      int64_t a = lo, b = mid, k = lo;
+      while (a < mid && b < hi) {
+        if (y[a] <= y[b]) tmp[k++] = y[a++];
+        else { D += mid - a; tmp[k++] = y[b++]; }
+      }
+      while (a < mid) tmp[k++] = y[a++];
+      while (b < hi) tmp[k++] = y[b++];
+    }
+    std::swap(y, tmp);
+  }
+  int64_t U = 0;  // y is now sorted: runs of equal y
+  for (int64_t i = 0; i < m;) {
+    int64_t j = i;
+    while (j < m && y[j] == y[i]) ++j;
+    U += (j - i) * (j - i - 1) / 2;
+    i = j;
+  }
+  const int64_t S = P0 - T - U + W - 2 * D;
+  const double den = std::sqrt((double)(P0 - T)) * std::sqrt((double)(P0 - U));
+  *h_tau = den > 0.0 ? (double)S / den : std::nan("");
+  if (h_counts) {
+    h_counts[0] = S;
+    h_counts[1] = T;
+    h_counts[2] = U;
+    h_counts[3] = P0;
+  }
   return SPERM_OK;
 }
 

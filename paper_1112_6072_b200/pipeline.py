@@ -51,10 +51,10 @@ class PHResult:
 
 
 def job_sizes(jobsets: List["NodeSet"], num_jobs: int) -> np.ndarray:
-    """Number of nonzero entries of every job (a size key for the scheduling study)."""
+    """Number of nonzero entries of every job (sperm_nnz; the "size" scheduling key)."""
     out = np.zeros(num_jobs, dtype=np.int64)
     for s in jobsets:
-        out[s.job.cpu().numpy()] = (s.mats != 0).sum(dim=(1, 2)).cpu().numpy()
+        out[s.job.cpu().numpy()] = S.sperm_nnz(s.mats).cpu().numpy()
     return out
 
 
@@ -210,13 +210,25 @@ def estimate_owner(job_ids, world: int):
     return job_ids % world
 
 
+def _allreduce_sum(t, group=None):
+    """SUM all-reduce of a CUDA tensor over `group`: in place over NCCL; a gloo group (the CPU
+    multi-process tests, or ranks sharing one device) stages it through host memory."""
+    import torch.distributed as dist
+    if group is None or dist.get_world_size(group) <= 1:
+        return t
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
 def gather_estimates(est_part, group=None):
     """Every rank's estimates from per-rank partial vectors (0.0 at the jobs other ranks own):
     one SUM all-reduce, exact since x + 0.0 = x for the nonnegative estimates."""
-    import torch.distributed as dist
-    if group is not None and dist.get_world_size(group) > 1:
-        dist.all_reduce(est_part, op=dist.ReduceOp.SUM, group=group)
-    return est_part
+    return _allreduce_sum(est_part, group)
 
 
 def dynamic_chunks(order, chunk: int, store, key: str):
@@ -244,10 +256,7 @@ def allreduce_accumulators(acc, group=None):
     """Algorithm PH Step 4 across GPUs: one SUM all-reduce of the
     [jobs + 1][8] residue accumulators (NCCL on GPUs).  Each rank added residues < 2^31
     per leaf, so the int64 (wrap-around) sum equals the exact uint64 sum."""
-    import torch.distributed as dist
-    if group is not None and dist.get_world_size(group) > 1:
-        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-    return acc
+    return _allreduce_sum(acc, group)
 
 
 def reconstruct(res, k: int):
@@ -268,7 +277,8 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     assignment="static": the LPT plan of sperm_schedule (S1); "dynamic": ranks claim chunks of
     the policy's job order from a shared counter in `store` (default: the process group's
     store) as they finish — the paper's first-free-processor rule across GPUs.
-    The uint64 accumulators gain < 2^31 per leaf, so they are folded mod p (sperm_fold_mod)
+    policy: "estimate" (KKLLL weights, the improved Step 3), "natural", "random", or "size"
+    (the job's nonzero count as the LPT weight).  The uint64 accumulators gain < 2^31 per leaf, so they are folded mod p (sperm_fold_mod)
     before more than `fold_every` leaves have been added since the last fold, and before the
     all-reduce (so the sum over ranks stays below 2^64)."""
     import torch
@@ -298,7 +308,11 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
         else:
             est_dev[ids.long()] = float("inf")
     est = gather_estimates(est_dev, group).cpu().numpy()
-    machine, order, _ = S.sperm_schedule(est, world, policy, seed=seed)
+    sizes = job_sizes(jobsets, num_jobs)
+    if policy == "size":  # LPT on the job's nonzero count instead of its estimate
+        machine, order, _ = S.sperm_schedule(sizes.astype(np.float64), world, "estimate", seed=seed)
+    else:
+        machine, order, _ = S.sperm_schedule(est, world, policy, seed=seed)
     acc = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
     job_cycles = torch.zeros(num_jobs, dtype=torch.int64, device=device) if measure_jobs else None
     pos = rank_positions(machine, order, rank)
@@ -381,4 +395,4 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
                     job_order_n={s.n: s.count for s in jobsets}, leaves=leaves, terms=terms,
                     estimates=est, machine=machine,
                     job_cycles=job_cycles.cpu().numpy() if measure_jobs else None,
-                    job_sizes=job_sizes(jobsets, num_jobs), stats=stats)
+                    job_sizes=sizes, stats=stats)

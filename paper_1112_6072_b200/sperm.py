@@ -50,8 +50,10 @@ _SIGS = {
     "sperm_fold_mod": (_I, [_P, _I64, _P]),
     "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "sperm_expand_stats": (_I, [_P, _P, _I]),
+    "sperm_nnz": (_I, [_P, _I, _I64, _P, _P]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
+    "sperm_kendall_tau": (_I, [_P, _P, _I64, _P, _P]),
     "sperm_launch_count": (_I64, [_I]),
     "sperm_timing_enable": (None, [_I]),
     "sperm_timing_reset": (None, []),
@@ -290,6 +292,16 @@ def sperm_expand_stats(reset: bool = False):
     return b.value, nn.value
 
 
+def sperm_nnz(mats, stream=None):
+    """Nonzeros of each matrix of mats [count, n, n] (int64 CUDA tensor [count])."""
+    import torch
+    mats = _dev(mats, torch.int32)
+    count, n = int(mats.shape[0]), int(mats.shape[1])
+    out = torch.empty((count,), dtype=torch.int64, device=mats.device)
+    _check(lib().sperm_nnz(_ptr(mats), n, count, _ptr(out), _stream(stream)))
+    return out
+
+
 # --------------------------------------------------------------------- estimator
 def sperm_estimate(mats, trials: int = 0, seed: int = 1, ids=None, keep_trials: bool = False, stream=None):
     """KKLLL estimates (fp64) of the 0/1 patterns of mats [count, n, n]."""
@@ -321,6 +333,28 @@ def sperm_schedule(weights, machines: int, policy: str = "estimate", seed: int =
                                 int(seed) & (2**64 - 1), machine.ctypes.data if count else None,
                                 order.ctypes.data if count else None, loads.ctypes.data))
     return machine, order, loads
+
+
+# --------------------------------------------------------------------- statistics
+def sperm_kendall_tau(x, y, return_counts: bool = False):
+    """Kendall tau with Eq. (10)'s tie correction (host C++).  With return_counts also
+    (S, T, U, m(m-1)/2)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
+    if x.shape != y.shape or x.ndim != 1:
+        raise ValueError("x and y must be 1-D of equal length")
+    tau = ctypes.c_double(0)
+    counts = np.zeros(4, dtype=np.int64)
+    _check(lib().sperm_kendall_tau(x.ctypes.data if len(x) else None, y.ctypes.data if len(y) else None, len(x),
+                                   ctypes.byref(tau), counts.ctypes.data))
+    return (tau.value, tuple(int(c) for c in counts)) if return_counts else tau.value
+
+
+def tau_z(tau: float, m: int) -> float:
+    """Normal-approximation z score of tau under independence: E = 0, var = 2(2m+5)/(9m(m-1))
+    (PAPER.md:406-409)."""
+    import math
+    return tau / math.sqrt(2.0 * (2 * m + 5) / (9.0 * m * (m - 1)))
 
 
 # --------------------------------------------------------------------- timing

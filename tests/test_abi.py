@@ -146,3 +146,27 @@ def test_bound_primes_sufficient_and_tight():
     # C100: per = 149364113290700 (Table T12) < 2^48 needs 2 primes; Bregman 6^(100/3) -> 3
     assert P.sperm_bound_primes(paper_graph("C100")) == 3
     assert P.sperm_bound_primes(truncated_icosahedron()) == 2
+
+
+def test_kendall_tau_matches_oracle_definition():
+    """sperm_kendall_tau (host C++, O(m log m)) = the O(m^2) definition of Eqs. (7)-(10)
+    (oracle/stats.py): S, T, U exactly and tau to the last bit of the same formula, on
+    random keys with heavy ties, all-distinct keys, constant keys and tiny inputs."""
+    import math
+    from oracle.stats import kendall_tau_b
+    rng = np.random.default_rng(8)
+    cases = [([], []), ([1.0], [2.0]), ([1.0, 1.0], [2.0, 3.0]), ([3.0, 1.0, 2.0], [1.0, 2.0, 3.0])]
+    for _ in range(60):
+        m = int(rng.integers(2, 300))
+        k = int(rng.integers(1, 12))
+        cases.append((list(rng.integers(0, k, size=m).astype(float)), list(rng.integers(0, k + 3, size=m).astype(float))))
+        cases.append((list(rng.random(m)), list(rng.random(m))))
+    for x, y in cases:
+        got, (s, t, u, p0) = S.sperm_kendall_tau(x, y, return_counts=True)
+        m = len(x)
+        if m < 2:
+            assert s == t == u == p0 == 0 and math.isnan(got)
+            continue
+        tau, s0, t0, u0 = kendall_tau_b(x, y)
+        assert (s, t, u, p0) == (s0, t0, u0, m * (m - 1) // 2)
+        assert (math.isnan(got) and math.isnan(tau)) or got == tau

@@ -331,7 +331,7 @@ def test_pipeline_fold_every_leaf_set():
     per-job values and total as without folding."""
     a = truncated_icosahedron()
     r1 = pipeline.permanent(a, jobs_at_least=128, leaf_order=20)
-    r2 = pipeline.permanent(a, jobs_at_least=128, leaf_order=20, fold_every=1)
+    r2 = pipeline.permanent(a, jobs_at_least=128, leaf_order=20, fold_every=1, leaf_budget_bytes=256 << 10)
     assert r2.stats.get("folds", 0) >= 2
     assert r1.value == r2.value == golden("C60_truncated_icosahedron")
     assert r1.job_values == r2.job_values
@@ -516,3 +516,75 @@ def test_rnw_prime_count_bregman_and_cap():
             assert int(r2[i, q]) == w % P.sperm_prime(q)
     with pytest.raises(P.SpermError):
         P.sperm_permanent(dev(mats), min_primes=3, max_primes=2)
+
+
+# ------------------------------------------------------------------ multi-rank pipeline
+def _ws2_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    sys_path_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import sys
+    if sys_path_root not in sys.path:
+        sys.path.insert(0, sys_path_root)
+    import paper_1112_6072_b200 as P_  # noqa: F401
+    from paper_1112_6072_b200 import pipeline as pl
+    from workloads import dodecahedron as dod, truncated_icosahedron as ti
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    res = {}
+    for name, a, J, L in (("C20", dod(), 30, 8), ("C60", ti(), 128, 18)):
+        for policy, asg in (("estimate", "static"), ("estimate", "dynamic"), ("size", "static"),
+                            ("natural", "static"), ("random", "static")):
+            r = pl.permanent(a, jobs_at_least=J, leaf_order=L, policy=policy, assignment=asg,
+                             group=dist.group.WORLD, dynamic_chunk=3)
+            res[f"{name}_{policy}_{asg}"] = (r.value, r.job_values, r.machine.tolist(), r.num_jobs)
+    import pickle
+    with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as f:
+        pickle.dump(res, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_pipeline_two_ranks_gloo_same_device(tmp_path):
+    """pipeline.permanent with a world-size-2 process group (two processes on cuda:0, gloo: the
+    collectives go through the host, so neither rank's kernels wait on the other's): sharded
+    KKLLL estimates + all-reduce, replicated LPT schedule, each rank evaluating only its jobs
+    (static) or claiming chunks from the store (dynamic), residue all-reduce + CRT.  Both ranks
+    must return the exact per(A) and every job value the single-rank run and the oracle give."""
+    import socket
+    import torch.multiprocessing as mp
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    mp.start_processes(_ws2_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    import pickle
+    rs = [pickle.load(open(tmp_path / f"r{r}.pkl", "rb")) for r in range(2)]
+    c20_jobs = [node_permanent(j) for j in pre_expand(dodecahedron(), jobs_at_least=30)]
+    single_c60 = pipeline.permanent(truncated_icosahedron(), jobs_at_least=128, leaf_order=18)
+    for key in rs[0]:
+        v0, jv0, mach0, nj = rs[0][key]
+        v1, jv1, mach1, _ = rs[1][key]
+        assert v0 == v1 and jv0 == jv1 and mach0 == mach1, key
+        if key.startswith("C20"):
+            assert v0 == 1392 and jv0 == c20_jobs, key
+        else:
+            assert v0 == golden("C60_truncated_icosahedron") and jv0 == single_c60.job_values, key
+        if key.endswith("static"):
+            assert set(mach0) == {0, 1}, key  # both ranks were dealt jobs
+
+
+@pytest.mark.parametrize("name", ["fullerene_n96_seed2024_iso0", "random3reg_n96_seed2024_96"])
+def test_pipeline_configs4_n96_vs_oracle(name):
+    """configs[4]: both n = 96 matrices through the whole path (the bench's strong-scaling
+    configuration, J >= 160, L = 16; and J >= 1000) against the C frontier DP's values."""
+    import numpy as np_
+    from workloads import random_fullerene
+    if name.startswith("fullerene"):
+        a = random_fullerene(96, 2024, 0)[0]
+    else:
+        a = random_3perm(96, np_.random.default_rng(np_.random.PCG64([2024, 96])))
+    want = golden(name)
+    for J in (160, 1000):
+        r = pipeline.permanent(a, jobs_at_least=J, leaf_order=16)
+        assert r.value == want, J
+        assert sum(r.job_values) == want

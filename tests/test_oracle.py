@@ -215,6 +215,30 @@ def test_c60_two_constructions_agree():
     assert 2 ** schrijver_lower_log2(60, 3) <= pa <= p
 
 
+# ---------------------------------------------------------------- Kendall tau
+def test_kendall_tau_oracle_pins():
+    """Eqs. (7)-(10): perfect agreement +1, reversal -1 (the paper's stated
+    limits); without ties S = P0 - 2 * inversions (brute-force inversion count); with ties the
+    tau-b of scipy.stats.kendalltau (a library routine)."""
+    from scipy.stats import kendalltau
+    from oracle.stats import kendall_tau_b
+    x = list(range(12))
+    assert abs(kendall_tau_b(x, x)[0] - 1.0) < 1e-15 and abs(kendall_tau_b(x, x[::-1])[0] + 1.0) < 1e-15
+    assert kendall_tau_b(x, x)[1:] == (66, 0, 0)
+    rng = np.random.default_rng(3)
+    for _ in range(30):
+        m = int(rng.integers(2, 40))
+        p = rng.permutation(m)
+        inv = sum(1 for i in range(m) for j in range(i + 1, m) if p[i] > p[j])
+        tau, s, t, u = kendall_tau_b(list(range(m)), list(p))
+        assert s == m * (m - 1) // 2 - 2 * inv and t == u == 0
+        xs = rng.integers(0, 5, size=m).astype(float)
+        ys = rng.integers(0, 4, size=m).astype(float)
+        tau, s, t, u = kendall_tau_b(list(xs), list(ys))
+        ref = kendalltau(xs, ys).statistic
+        assert (math.isnan(tau) and math.isnan(ref)) or abs(tau - ref) < 1e-12
+
+
 # ---------------------------------------------------------------- KKLLL
 def test_kklll_theorem1_exact_expectation():
     """E[X_A] = per(A) (Theorem 1) over all 3^nnz assignments."""

@@ -1,7 +1,7 @@
 """Writes tests/golden/oracle_values.txt: exact permanents of the workload graphs
 computed ONLY by oracle/ (frontier DP and H_per), never by the CUDA path.
 
-    python tools/make_golden.py [--fullerenes]
+    python tools/make_golden.py [--fullerenes] [--n96]
 
 Each line: <name> <value>   (name documents the workload recipe).
 """
@@ -43,6 +43,23 @@ def main():
                 vals[key] = str(per_frontier(g, bfs_order(g)))
                 print(key, vals[key], f"{time.time() - t:.1f}s", flush=True)
                 _write(vals)
+    if "--n96" in sys.argv:
+        # configs[4]: the spiral fullerene n=96 (isomer 0) and the random 3-regular n=96
+        # (PCG64([2024, 96])), by the C frontier DP (oracle/frontier.c; ~2 and ~4 CPU-minutes)
+        import numpy as np
+        from oracle.cfrontier import narrow_order, per_frontier_c
+        from workloads import random_3perm
+        g, _ = random_fullerene(96, 2024, 0)
+        rng = np.random.default_rng(np.random.PCG64([2024, 96]))
+        r = random_3perm(96, rng)
+        for key, m, order in (("fullerene_n96_seed2024_iso0", g, bfs_order(g)),
+                              ("random3reg_n96_seed2024_96", r, narrow_order(r))):
+            if key in vals:
+                continue
+            t = time.time()
+            vals[key] = str(per_frontier_c(m, order))
+            print(key, vals[key], f"{time.time() - t:.1f}s", flush=True)
+            _write(vals)
     _write(vals)
 
 
