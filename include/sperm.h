@@ -96,9 +96,13 @@ int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
  *             leaf contributes coef * per(leaf) (the scalars Eq. (2),
  *             PAPER.md:105-112, leaves on its children).
  *  d_order    [count] int32 evaluation order (device) or NULL (natural order):
- *             the persistent kernel's work queue hands out the leaves in this
- *             order (improved Step 3: non-increasing
- *             estimate).  Must be a permutation of 0..count-1.
+ *             leaves are grouped by their evaluation plan (one persistent grid
+ *             per group, the groups running concurrently, largest work first),
+ *             and each group's work queue hands out its leaves in this order
+ *             (stable grouping; improved Step 3: the pipeline
+ *             expands a rank's jobs in non-increasing-estimate order, so the
+ *             natural leaf order already follows it).  Must be a permutation
+ *             of 0..count-1.
  *  d_job      [count] int32 job id of each leaf (device) or NULL (every leaf
  *             belongs to job 0, so d_job_acc[0] accumulates the total).
  *  num_jobs   size of d_job_acc's first dimension (>= 1 when d_job_acc is set).
@@ -137,6 +141,17 @@ int sperm_permanent(const int32_t* d_mats, int n, int64_t count, const int64_t* 
                     const int32_t* d_order, const int32_t* d_job, int64_t num_jobs,
                     int min_primes, int max_primes, uint32_t* d_leaf_res, int32_t* d_leaf_k,
                     uint64_t* d_job_acc, uint64_t* d_leaf_cycles, void* stream);
+
+/* sperm_permanent_host — sperm_permanent on HOST buffers, synchronous: copies h_mats
+ * [count][n][n] int32 (host; pinned memory makes the copy asynchronous DMA) to the device,
+ * evaluates every matrix's exact permanent (R-NW mod the primes its bound needs, at least
+ * min_primes), reconstructs it on the device (sperm_crt_device) and copies back h_out
+ * [count][limbs + 1] uint32 (host): limbs little-endian magnitude words, then the sign (-1, 0,
+ * +1).  limbs >= (primes needed) + 1; limbs = SPERM_KMAX + 2 always suffices.  The public
+ * end-to-end call of the batched R-NW (configs[1] in bench.py's e2e figure).  Errors: those of
+ * sperm_permanent and sperm_crt_device; SPERM_ERR_ARG for bad sizes / NULL buffers. */
+int sperm_permanent_host(const int32_t* h_mats, int n, int64_t count, int min_primes, uint32_t* h_out,
+                         int limbs, void* stream);
 
 /* Number of Gray-code terms sperm_permanent evaluates for `count` leaves of
  * order n: count * 2^(n-1) (as double; exact for n <= 53). */

@@ -925,9 +925,12 @@ __global__ void rnw_spec_check_kernel(const int* __restrict__ hist, const int* _
 }
 
 // Small batches (count <= kSmallGroup): the keys kernel, the radix sort and the speculation check
-// in one single-CTA kernel — key histogram, exclusive scan, scatter of the leaf ids into their
-// groups (warp-aggregated cursors: the order inside a group is not kept, and nothing depends on it:
-// every leaf has its own accumulators), histogram store and the go flag.
+// in one single-CTA kernel — key histogram, exclusive scan, a stable scatter of the leaf ids into
+// their groups (so each group's work queue hands its leaves out in the caller's d_order, like the
+// stable radix sort of larger batches), histogram store and the go flag.  Stable scatter per
+// chunk of blockDim leaves: every warp's count per key (match_any), an exclusive scan of those
+// counts over the warps per key, then each leaf's slot = group cursor + warps before + lanes
+// before it with the same key.
 constexpr int kSmallGroup = 4096;
 constexpr int kSmallGroupThreads = 1024;
 __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
@@ -936,8 +939,9 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
     const int* __restrict__ err, KeyHist pred, int spec, int* __restrict__ go) {
   __shared__ int s_h[kNumKeys], s_hk[kNumKeys], s_cur[kNumKeys];
   __shared__ unsigned long long s_hx[kNumKeys];
+  __shared__ int s_wc[kSmallGroupThreads / 32][kNumKeys];  // per-warp key counts, then prefixes
   __shared__ int s_bad;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
     s_h[t] = s_hk[t] = 0;
     s_hx[t] = 0;
@@ -986,8 +990,9 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
     }
     if (lane == 0) s_bad = *err;
   }
-  __syncthreads();
   for (int base = 0; base < count; base += blockDim.x) {
+    for (int t = threadIdx.x; t < nwarps * kNumKeys; t += blockDim.x) s_wc[t / kNumKeys][t % kNumKeys] = 0;
+    __syncthreads();
     const int i = base + threadIdx.x;
     const bool live = i < count;
     int key = -1, leaf = 0;
@@ -998,11 +1003,20 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
       key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
     }
     const unsigned same = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(same) - 1;
-    int pos0 = 0;
-    if (live && lane == leader) pos0 = atomicAdd(&s_cur[key], __popc(same));
-    pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-    if (live) sorted[pos0 + __popc(same & ((1u << lane) - 1u))] = leaf;
+    if (live && lane == __ffs(same) - 1) s_wc[warp][key] = __popc(same);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kNumKeys; k += blockDim.x) {  // per key: exclusive prefix over the warps
+      int run = s_cur[k];
+      for (int w = 0; w < nwarps; ++w) {
+        const int c = s_wc[w][k];
+        s_wc[w][k] = run;
+        run += c;
+      }
+      s_cur[k] = run;
+    }
+    __syncthreads();
+    if (live) sorted[s_wc[warp][key] + __popc(same & ((1u << lane) - 1u))] = leaf;
+    __syncthreads();
   }
   for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
     hist[t] = s_h[t];
@@ -1029,12 +1043,15 @@ struct Launch {
   const int* go;                    // speculative launch: run only if *go != 0 (else NULL)
 };
 
-// A per-process pool of non-blocking streams and reusable events for the plan groups.
+// Non-blocking streams and reusable events for the plan groups, one pool per device (streams
+// and events belong to the device that was current when they were created).  Events are leased
+// per call (EventLease) and only returned once the call has enqueued every wait on them, so an
+// event is never re-recorded before a cudaStreamWaitEvent on its previous record was issued,
+// however many groups a call has or how many threads call concurrently.
 struct StreamPool {
   std::mutex mu;
   std::vector<cudaStream_t> streams;
-  std::vector<cudaEvent_t> events;
-  size_t next_event = 0;
+  std::vector<cudaEvent_t> free_events;
   cudaStream_t stream(int g) {
     std::lock_guard<std::mutex> lk(mu);
     while ((int)streams.size() <= g % 8) {
@@ -1044,20 +1061,42 @@ struct StreamPool {
     }
     return streams[g % 8];
   }
-  cudaEvent_t event() {  // round robin over 64 events (a call uses at most ~2 per group)
+  cudaEvent_t acquire() {
     std::lock_guard<std::mutex> lk(mu);
-    if (events.size() < 64) {
+    if (free_events.empty()) {
       cudaEvent_t e;
       cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      events.push_back(e);
       return e;
     }
-    return events[next_event++ % events.size()];
+    cudaEvent_t e = free_events.back();
+    free_events.pop_back();
+    return e;
+  }
+  void release(std::vector<cudaEvent_t>& evs) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_events.insert(free_events.end(), evs.begin(), evs.end());
+    evs.clear();
   }
 };
+struct EventLease {
+  StreamPool& pool;
+  std::vector<cudaEvent_t> evs;
+  explicit EventLease(StreamPool& p) : pool(p) {}
+  cudaEvent_t get() {
+    evs.push_back(pool.acquire());
+    return evs.back();
+  }
+  ~EventLease() { pool.release(evs); }
+};
 StreamPool& stream_pool() {
-  static StreamPool p;
-  return p;
+  static std::mutex m;
+  static std::map<int, std::unique_ptr<StreamPool>> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(m);
+  std::unique_ptr<StreamPool>& p = pools[dev];
+  if (!p) p.reset(new StreamPool);
+  return *p;
 }
 
 // Terms per lane 2^m: small enough that a group has 1-2x per_warp work items per resident warp
@@ -1505,8 +1544,8 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     std::vector<int> order;
   };
   thread_local Spec spec;
-  static const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables
-    const char* e = getenv("SPERM_SPECULATE");
+  const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables (read per call: the bench
+    const char* e = getenv("SPERM_SPECULATE");  // times both settings in one process)
     return !(e && e[0] == '0');
   }();
   int dev = 0;
@@ -1578,11 +1617,12 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   // The largest group runs on `st` itself, the others on pool streams 1..7 (stream 0 carries the
   // speculative path's read-back); joins: their completion events, waited on by `st` afterwards.
   std::vector<cudaEvent_t> joins;
+  StreamPool& pool = stream_pool();
+  EventLease lease(pool);  // returned at exit, after every wait on them has been enqueued
   auto launch_groups = [&](const int* hh, const std::vector<int>& order_keys, const int* go) -> int {
-    StreamPool& pool = stream_pool();
     cudaEvent_t fork = nullptr;
     if (order_keys.size() > 1) {
-      fork = pool.event();
+      fork = lease.get();
       SPERM_CUDA(cudaEventRecord(fork, st));
     }
     int64_t offs[kNumKeys];
@@ -1599,7 +1639,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
                (unsigned long long*)d_leaf_cycles, go};
       const int r = launch_key(key, NPg, L);
       if (gs != st) {
-        cudaEvent_t join = pool.event();
+        cudaEvent_t join = lease.get();
         SPERM_CUDA(cudaEventRecord(join, gs));
         joins.push_back(join);
       }
@@ -1617,8 +1657,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     }
     ts_rnw.reset(new TimingScope("rnw", st));
     // the read-back on pool stream 0, forked before the groups (`st` waits for it with the joins)
-    StreamPool& pool = stream_pool();
-    cudaEvent_t cf = pool.event();
+    cudaEvent_t cf = lease.get();
     cudaStream_t cs = pool.stream(0);
     SPERM_TRY(cudaEventRecord(cf, st));
     SPERM_TRY(cudaStreamWaitEvent(cs, cf, 0));
@@ -1703,4 +1742,47 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
 #undef SPERM_TRY
   if (le != cudaSuccess) return cuda_check(le, "rnw_finalize_kernel");
   return SPERM_OK;
+}
+
+// Host-buffer entry point: H2D of the matrices, sperm_permanent, device CRT, D2H of the exact
+// values — the whole batched R-NW as one synchronous call on host memory.
+extern "C" int sperm_permanent_host(const int32_t* h_mats, int n, int64_t count, int min_primes, uint32_t* h_out,
+                                    int limbs, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || n > SPERM_NMAX || count < 0 || limbs < min_primes + 1 || limbs > SPERM_KMAX + 2 ||
+      (count > 0 && ((n > 0 && !h_mats) || !h_out)))
+    return set_error(SPERM_ERR_ARG, "sperm_permanent_host: bad arguments");
+  if (count == 0) return SPERM_OK;
+  const size_t mat_bytes = sizeof(int32_t) * (size_t)n * n * count;
+  int32_t* d_mats = nullptr;
+  uint32_t* d_res = nullptr;
+  int32_t* d_k = nullptr;
+  uint32_t* d_out = nullptr;
+  auto release = [&]() {
+    cudaFreeAsync(d_mats, st);
+    cudaFreeAsync(d_res, st);
+    cudaFreeAsync(d_k, st);
+    cudaFreeAsync(d_out, st);
+  };
+  int rc = SPERM_OK;
+  cudaError_t e = cudaMallocAsync((void**)&d_mats, mat_bytes > 0 ? mat_bytes : 4, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&d_res, sizeof(uint32_t) * SPERM_KMAX * count, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&d_k, sizeof(int32_t) * count, st);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&d_out, sizeof(uint32_t) * (limbs + 1) * count, st);
+  if (e == cudaSuccess && mat_bytes) e = cudaMemcpyAsync(d_mats, h_mats, mat_bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) {
+    release();
+    return cuda_check(e, "sperm_permanent_host: allocation / H2D");
+  }
+  rc = sperm_permanent(d_mats, n, count, nullptr, nullptr, nullptr, 0, min_primes, 0, d_res, d_k, nullptr, nullptr,
+                       stream);
+  if (rc == SPERM_OK) rc = sperm_crt_device(d_res, count, SPERM_KMAX, d_k, 0, d_out, limbs, stream);
+  if (rc == SPERM_OK) {
+    e = cudaMemcpyAsync(h_out, d_out, sizeof(uint32_t) * (limbs + 1) * count, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_check(e, "sperm_permanent_host: D2H");
+  }
+  release();
+  e = cudaStreamSynchronize(st);
+  if (rc == SPERM_OK && e != cudaSuccess) rc = cuda_check(e, "sperm_permanent_host: synchronize");
+  return rc;
 }

@@ -44,6 +44,7 @@ _SIGS = {
     "sperm_crt_device": (_I, [_P, _I64, _I, _P, _I, _P, _I, _P]),
     "sperm_bound_primes": (_I, [_P, _I, _P]),
     "sperm_permanent": (_I, [_P, _I, _I64, _P, _P, _P, _I64, _I, _I, _P, _P, _P, _P, _P]),
+    "sperm_permanent_host": (_I, [_P, _I, _I64, _I, _P, _I, _P]),
     "sperm_rnw_terms": (ctypes.c_double, [_I, _I64]),
     "sperm_rnw_stats": (_I, [_P, _P, _P, _I]),
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
@@ -166,6 +167,29 @@ def sperm_permanent(mats, coef=None, order=None, job=None, num_jobs: int = 0, mi
                                  int(min_primes), int(max_primes), _ptr(leaf_res), _ptr(leaf_k), _ptr(job_acc),
                                  _ptr(leaf_cycles), _stream(stream)))
     return leaf_res, leaf_k
+
+
+def sperm_permanent_host(h_mats, min_primes: int = 1, out=None, stream=None) -> List[int]:
+    """Exact permanents of a HOST batch [count, n, n] int32 (numpy, ideally pinned memory via a
+    torch CPU tensor's numpy view): one synchronous C call does H2D, R-NW, device CRT and D2H;
+    the returned words are marshalled to Python ints.  `out` (uint32 [count, KMAX + 3]) may be
+    passed to reuse a (pinned) result buffer."""
+    a = np.asarray(h_mats)
+    if a.dtype != np.int32 or not a.flags.c_contiguous or a.ndim != 3:
+        raise TypeError("expected a C-contiguous int32 array [count, n, n]")
+    count, n = int(a.shape[0]), int(a.shape[1])
+    limbs = KMAX + 2
+    if out is None:
+        out = np.empty((count, limbs + 1), dtype=np.uint32)
+    _check(lib().sperm_permanent_host(a.ctypes.data if a.size else None, n, count, int(min_primes),
+                                      out.ctypes.data if count else None, limbs, _stream(stream)))
+    mag, sign = out[:, :limbs], out[:, limbs].view(np.int32)
+    small = (~mag[:, 2:].any(axis=1)).tolist()
+    lo = (mag[:, 0].astype(np.uint64) | (mag[:, 1].astype(np.uint64) << np.uint64(32))).tolist()
+    buf = np.ascontiguousarray(mag).tobytes()
+    w = 4 * limbs
+    return [s_ * (v if sm else int.from_bytes(buf[r * w:(r + 1) * w], "little"))
+            for r, (s_, v, sm) in enumerate(zip(sign.tolist(), lo, small))]
 
 
 def sperm_rnw_terms(n: int, count: int) -> float:

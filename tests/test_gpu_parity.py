@@ -588,3 +588,15 @@ def test_pipeline_configs4_n96_vs_oracle(name):
         r = pipeline.permanent(a, jobs_at_least=J, leaf_order=16)
         assert r.value == want, J
         assert sum(r.job_values) == want
+
+
+def test_permanent_host_buffers():
+    """sperm_permanent_host (host buffers: H2D, R-NW, device CRT, D2H in one call) on configs[1]'s
+    first 16 + last 16 matrices and a signed ragged case, against the oracle."""
+    mats = random_3perm_batch(256, 24, seed=2024)
+    sel = np.concatenate([mats[:16], mats[-16:]]).astype(np.int32)
+    assert P.sperm_permanent_host(np.ascontiguousarray(sel)) == [h_per(m) for m in sel]
+    rng = np.random.default_rng(17)
+    b = (rng.integers(-5, 6, size=(9, 11, 11)) * (rng.random((9, 11, 11)) < 0.4)).astype(np.int32)
+    assert P.sperm_permanent_host(b, min_primes=3) == [per_ryser_nw_gray(m) for m in b]
+    assert P.sperm_permanent_host(np.zeros((0, 5, 5), dtype=np.int32)) == []
