@@ -438,16 +438,35 @@ def bench_c100(P, torch, leaf_order: int = 15, jobs_at_least: int = 159):
     P.sperm_rnw_stats(reset=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r = pipeline.permanent(paper_graph("C100"), jobs_at_least=jobs_at_least, leaf_order=leaf_order)
+    r = pipeline.permanent(paper_graph("C100"), jobs_at_least=jobs_at_least, leaf_order=leaf_order,
+                           measure_jobs=True)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
     terms = P.sperm_rnw_stats(reset=True)[0]
     P.sperm_timing_enable(False)
+    # the paper's load-balance study on this run's measured job costs T_i (SM cycles of each job's
+    # R-NW leaves): Kendall tau (Eq. 10, Table 3) and Tables 5-7's efficiencies of Step 3 at m
+    # processors in natural / exact-time / estimated order (LS replayed with the actual costs)
+    import numpy as np
+    T = r.job_cycles.astype(np.float64)
+    est = r.estimates
+    tau_est = P.sperm_kendall_tau(T, est)
+    tau_size = P.sperm_kendall_tau(T, r.job_sizes.astype(np.float64))
+    orders = {"natural": np.arange(len(T)), "exact": np.argsort(-T, kind="stable"),
+              "estimated": np.argsort(-est, kind="stable")}
+    eff = {str(m): {k: P.replay_efficiency(T, o, m) for k, o in orders.items()} for m in (8, 16, 32)}
     return {"workload": f"per(C100), PAPER.md appendix graph; J>={jobs_at_least}, leaves of order <= {leaf_order}",
             "per": str(r.value), "paper_table_T12_total": str(pin), "matches_paper": r.value == pin,
             "wall_s": wall, "jobs": r.num_jobs, "leaves": r.leaves, "terms": terms,
-            "stage_ms": stages, "stage_note": "device time per stage (library CUDA-event timers, one stream)", "paper_T1_s": 118413.21, "paper_T32_s": 3796.85}
+            "stage_ms": stages, "stage_note": "device time per stage (library CUDA-event timers, one stream); "
+                                              "per-job cycle counters on (measure_jobs)",
+            "kendall_tau_T_estimate": tau_est, "kendall_tau_T_size": tau_size,
+            "tau_z_estimate": P.tau_z(tau_est, len(T)),
+            "paper_tau_T_AP_table3": 0.4919, "paper_tau_T_P_table3": 0.5334,
+            "replay_efficiency": eff,
+            "paper_efficiency_32": {"natural": 0.8434, "exact": 0.9746, "estimated": 0.9461},
+            "paper_T1_s": 118413.21, "paper_T32_s": 3796.85}
 
 
 def bench_ph(P, torch, leaf_order: int = 32, jobs_at_least: int = 992):

@@ -249,6 +249,16 @@ int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d
 int sperm_schedule(const double* h_weights, int64_t count, int machines, int policy,
                    uint64_t seed, int32_t* h_machine, int32_t* h_order, double* h_loads);
 
+/* sperm_list_schedule — Algorithm LS with the jobs' ACTUAL costs: jobs in
+ * the order h_order (a permutation of 0..count-1), each to the machine with the least
+ * accumulated cost so far (ties: lowest id).  This is Step 3 of Algorithm PH as it runs ("the
+ * currently least loaded processor") replayed with measured job times,
+ * for the natural / exact-time / estimated orders of Tables 5-7.
+ *  h_cost [count] double (host); h_machine [count] int32 out or NULL; h_loads [machines] out.
+ * Errors: SPERM_ERR_ARG. */
+int sperm_list_schedule(const double* h_cost, const int32_t* h_order, int64_t count, int machines,
+                        int32_t* h_machine, double* h_loads);
+
 /* ---------------------------------------------------------------- statistics */
 /* sperm_kendall_tau — Kendall's rank correlation of (x_i, y_i), i < m, with the tie correction
  * of Eq. (10) (Eqs. (7)-(9)): S = sum_{i<j} sign(x_j - x_i) sign(y_j - y_i),

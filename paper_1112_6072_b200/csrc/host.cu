@@ -323,6 +323,30 @@ int sperm_schedule(const double* h_weights, int64_t count, int machines, int pol
   return SPERM_OK;
 }
 
+// Algorithm LS replayed with the jobs' actual costs: jobs taken in the given
+// order, each to the machine whose accumulated cost is currently least (ties: lowest id) — Step 3
+// of Algorithm PH as it runs ("the currently least loaded processor")
+// when the job costs are known afterwards (Tables 5-7's natural / exact / estimated orders).
+int sperm_list_schedule(const double* h_cost, const int32_t* h_order, int64_t count, int machines,
+                        int32_t* h_machine, double* h_loads) {
+  if (count < 0 || machines < 1 || (count > 0 && (!h_cost || !h_order)) || !h_loads)
+    return set_error(SPERM_ERR_ARG, "sperm_list_schedule: bad arguments");
+  std::vector<double> loads(machines, 0.0);
+  std::vector<char> seen(count, 0);
+  for (int64_t r = 0; r < count; ++r) {
+    const int32_t j = h_order[r];
+    if (j < 0 || j >= count || seen[j]) return set_error(SPERM_ERR_ARG, "sperm_list_schedule: order is not a permutation");
+    seen[j] = 1;
+    int best = 0;
+    for (int m = 1; m < machines; ++m)
+      if (loads[m] < loads[best]) best = m;
+    loads[best] += h_cost[j];
+    if (h_machine) h_machine[j] = best;
+  }
+  for (int m = 0; m < machines; ++m) h_loads[m] = loads[m];
+  return SPERM_OK;
+}
+
 // ------------------------------------------------------------------ Kendall tau
 // Kendall's rank correlation with the tie correction of Eq. (10), in
 // O(m log m): sort the pairs by (x, y); S = concordant - discordant pairs = P0 - T - U + W - 2 D

@@ -55,6 +55,7 @@ _SIGS = {
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_kendall_tau": (_I, [_P, _P, _I64, _P, _P]),
+    "sperm_list_schedule": (_I, [_P, _P, _I64, _I, _P, _P]),
     "sperm_launch_count": (_I64, [_I]),
     "sperm_timing_enable": (None, [_I]),
     "sperm_timing_reset": (None, []),
@@ -357,6 +358,26 @@ def sperm_schedule(weights, machines: int, policy: str = "estimate", seed: int =
                                 int(seed) & (2**64 - 1), machine.ctypes.data if count else None,
                                 order.ctypes.data if count else None, loads.ctypes.data))
     return machine, order, loads
+
+
+def sperm_list_schedule(cost, order, machines: int):
+    """Algorithm LS replayed with actual costs: (machine[count], loads[machines])."""
+    c = np.ascontiguousarray(np.asarray(cost, dtype=np.float64))
+    o = np.ascontiguousarray(np.asarray(order, dtype=np.int32))
+    count = c.shape[0]
+    machine = np.zeros(count, dtype=np.int32)
+    loads = np.zeros(machines, dtype=np.float64)
+    _check(lib().sperm_list_schedule(c.ctypes.data if count else None, o.ctypes.data if count else None, count,
+                                     int(machines), machine.ctypes.data if count else None, loads.ctypes.data))
+    return machine, loads
+
+
+def replay_efficiency(cost, order, machines: int) -> float:
+    """Parallel efficiency sum(T) / (m * makespan) of LS in `order` with actual costs T
+    (Tables 5-7's efficiency)."""
+    _, loads = sperm_list_schedule(cost, order, machines)
+    mk = loads.max()
+    return float(np.sum(cost) / (machines * mk)) if mk > 0 else 1.0
 
 
 # --------------------------------------------------------------------- statistics

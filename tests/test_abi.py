@@ -170,3 +170,20 @@ def test_kendall_tau_matches_oracle_definition():
         tau, s0, t0, u0 = kendall_tau_b(x, y)
         assert (s, t, u, p0) == (s0, t0, u0, m * (m - 1) // 2)
         assert (math.isnan(got) and math.isnan(tau)) or got == tau
+
+
+def test_list_schedule_matches_oracle_ls():
+    """sperm_list_schedule = oracle.schedule.ls (Algorithm LS) on random
+    costs and orders, ties included; efficiency = sum / (m * makespan)."""
+    rng = np.random.default_rng(21)
+    for _ in range(40):
+        cnt = int(rng.integers(1, 60))
+        m = int(rng.integers(1, 9))
+        cost = rng.integers(1, 6, size=cnt).astype(float)
+        order = rng.permutation(cnt)
+        mach, loads = S.sperm_list_schedule(cost, order, m)
+        om, ol = ls(list(cost), list(order), m)
+        assert list(mach) == list(om) and np.allclose(loads, ol)
+        assert abs(S.replay_efficiency(cost, order, m) - cost.sum() / (m * max(ol))) < 1e-12
+    with pytest.raises(S.SpermError):
+        S.sperm_list_schedule([1.0, 2.0], [0, 0], 2)
