@@ -259,6 +259,17 @@ int sperm_schedule(const double* h_weights, int64_t count, int machines, int pol
 int sperm_list_schedule(const double* h_cost, const int32_t* h_order, int64_t count, int machines,
                         int32_t* h_machine, double* h_loads);
 
+/* sperm_interpolate_mod — the polynomial P of degree < npts through the points (x_j, v_j),
+ * modulo each of the first k CRT primes (host, synchronous): h_values [npts][stride] uint32 with
+ * v_j mod p_q at column q < k (e.g. the residue rows of sperm_permanent), h_x [npts] distinct
+ * integer points, h_coef [npts][coef_stride] out: coefficient of x^t mod p_q at row t, column q.
+ * Newton divided differences mod p.  With the values of per(xI - A) at n + 1 points this gives
+ * the permanental polynomial's coefficients (Eq. (11)) modulo the primes;
+ * sperm_crt_batch then recovers them exactly when prod p_q > 2 max |coefficient|.
+ * Errors: SPERM_ERR_ARG (bad sizes, points not distinct mod some p_q). */
+int sperm_interpolate_mod(const uint32_t* h_values, int stride, const int64_t* h_x, int npts, int k,
+                          uint32_t* h_coef, int coef_stride);
+
 /* ---------------------------------------------------------------- statistics */
 /* sperm_kendall_tau — Kendall's rank correlation of (x_i, y_i), i < m, with the tie correction
  * of Eq. (10) (Eqs. (7)-(9)): S = sum_{i<j} sign(x_j - x_i) sign(y_j - y_i),

@@ -103,3 +103,52 @@ def per_dense_small(a) -> int:
 
 def transpose(a: Sequence[Sequence[int]]) -> List[List[int]]:
     return [list(r) for r in zip(*a)] if len(a) else []
+
+
+def permanental_polynomial(a) -> list:
+    """Coefficients [c_0..c_n] of per(xI - A) (Eq. (11)) by Eq. (1) itself:
+    every permutation sigma contributes prod_i (x [sigma(i) = i] - a_{i sigma(i)}), a polynomial
+    in x multiplied out term by term.  Brute force (n <= 8)."""
+    from itertools import permutations
+    a = [[int(v) for v in row] for row in a]
+    n = len(a)
+    total = [0] * (n + 1)
+    for sigma in permutations(range(n)):
+        poly = [1]  # coefficients of the running product
+        for i in range(n):
+            j = sigma[i]
+            f = [-a[i][j], 1 if i == j else 0]  # x [i == j] - a_ij
+            nxt = [0] * (len(poly) + 1)
+            for d, c in enumerate(poly):
+                nxt[d] += c * f[0]
+                nxt[d + 1] += c * f[1]
+            poly = nxt
+        for d, c in enumerate(poly):
+            total[d] += c
+    return total
+
+
+def polynomial_from_values(xs, vs) -> list:
+    """Exact coefficients of the polynomial of degree < len(xs) through (xs[j], vs[j]), by
+    Lagrange's formula in rational arithmetic (fractions.Fraction)."""
+    from fractions import Fraction
+    m = len(xs)
+    coef = [Fraction(0)] * m
+    for j in range(m):
+        num = [Fraction(1)]  # prod_{i != j} (x - x_i)
+        den = Fraction(1)
+        for i in range(m):
+            if i == j:
+                continue
+            num = [Fraction(0)] + num
+            for d in range(len(num) - 1):
+                num[d] -= xs[i] * num[d + 1]
+            den *= xs[j] - xs[i]
+        for d in range(m):
+            coef[d] += vs[j] * num[d] / den
+    out = []
+    for c in coef:
+        if c.denominator != 1:
+            raise ArithmeticError("non-integer coefficient")
+        out.append(int(c))
+    return out

@@ -347,6 +347,59 @@ int sperm_list_schedule(const double* h_cost, const int32_t* h_order, int64_t co
   return SPERM_OK;
 }
 
+// ------------------------------------------------------------------ interpolation
+// Coefficients of the polynomial P of degree < npts through (x_j, P(x_j) mod p_q), modulo each of
+// the first k CRT primes: Newton divided differences, then the Newton form expanded into the
+// monomial basis (Horner on polynomials), all in exact uint64 arithmetic mod p.  Used for the
+// permanental polynomial per(xI - A) (Eq. (11)) from its values at npts points.
+static uint64_t powmod(uint64_t b, uint64_t e, uint64_t p) {
+  uint64_t r = 1;
+  b %= p;
+  while (e) {
+    if (e & 1) r = r * b % p;
+    b = b * b % p;
+    e >>= 1;
+  }
+  return r;
+}
+
+int sperm_interpolate_mod(const uint32_t* h_values, int stride, const int64_t* h_x, int npts, int k,
+                          uint32_t* h_coef, int coef_stride) {
+  if (npts < 1 || k < 1 || k > SPERM_KMAX || stride < k || coef_stride < k || !h_values || !h_x || !h_coef)
+    return set_error(SPERM_ERR_ARG, "sperm_interpolate_mod: bad arguments");
+  for (int q = 0; q < k; ++q) {
+    const uint64_t p = kPrimes[q];
+    std::vector<uint64_t> xs(npts), d(npts);
+    for (int j = 0; j < npts; ++j) {
+      const int64_t xm = h_x[j] % (int64_t)p;
+      xs[j] = (uint64_t)(xm < 0 ? xm + (int64_t)p : xm);
+      d[j] = h_values[(size_t)j * stride + q] % p;
+    }
+    for (int j = 0; j < npts; ++j)
+      for (int i = 0; i < j; ++i)
+        if (xs[i] == xs[j]) return set_error(SPERM_ERR_ARG, "sperm_interpolate_mod: points not distinct mod p");
+    // divided differences: d[j] = f[x_0..x_j]
+    for (int lvl = 1; lvl < npts; ++lvl)
+      for (int j = npts - 1; j >= lvl; --j) {
+        const uint64_t num = (d[j] + p - d[j - 1]) % p;
+        const uint64_t den = (xs[j] + p - xs[j - lvl]) % p;
+        d[j] = num * powmod(den, p - 2, p) % p;
+      }
+    // P = d0 + (x - x0)(d1 + (x - x1)(d2 + ...)): Horner from the innermost term
+    std::vector<uint64_t> c(npts, 0);
+    c[0] = d[npts - 1];
+    int deg = 0;
+    for (int j = npts - 2; j >= 0; --j) {
+      // c := c * (x - x_j) + d[j]
+      ++deg;
+      for (int t = deg; t >= 1; --t) c[t] = (c[t - 1] + (p - xs[j]) * c[t] % p) % p;
+      c[0] = ((p - xs[j]) * c[0] % p + d[j]) % p;
+    }
+    for (int t = 0; t < npts; ++t) h_coef[(size_t)t * coef_stride + q] = (uint32_t)c[t];
+  }
+  return SPERM_OK;
+}
+
 // ------------------------------------------------------------------ Kendall tau
 // Kendall's rank correlation with the tie correction of Eq. (10), in
 // O(m log m): sort the pairs by (x, y); S = concordant - discordant pairs = P0 - T - U + W - 2 D

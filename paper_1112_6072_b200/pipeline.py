@@ -396,3 +396,35 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
                     estimates=est, machine=machine,
                     job_cycles=job_cycles.cpu().numpy() if measure_jobs else None,
                     job_sizes=sizes, stats=stats)
+
+
+def permanental_polynomial(a, device="cuda"):
+    """The permanental polynomial P(x) = per(xI - A) = sum_t c_t x^t (Eq. (11)),
+    exactly: returns [c_0, ..., c_n] as Python ints.
+
+    The n + 1 values P(x_j), x_j = j - floor(n/2), are evaluated in ONE batched sperm_permanent
+    call (R-NW of every x_j I - A) modulo the k primes the coefficients need — sum_t |c_t| <=
+    per(I + |A|) (every term of per(xI - A) expands into terms of per(|x| I + |A|) at |x| = 1),
+    whose bound sperm_bound_primes gives — then interpolated modulo each prime
+    (sperm_interpolate_mod, Newton) and reconstructed by CRT (sperm_crt_batch).  The paper
+    evaluates P at the (n+1)-th roots of unity in complex floating point (PAPER.md:533-546);
+    integer points and modular arithmetic make every coefficient exact.  Direct R-NW limits n to
+    SPERM_NMAX (48): through the expansion, merged entries of x I - A grow like |x|^depth
+    (NEXT-3), so larger graphs are out of this function's reach."""
+    import torch
+    a = np.asarray(a, dtype=np.int64)
+    n = a.shape[0]
+    if a.ndim != 2 or a.shape[1] != n:
+        raise ValueError("square matrix expected")
+    if n > S.NMAX:
+        raise ValueError(f"permanental_polynomial: n = {n} > {S.NMAX} (direct R-NW only)")
+    if n == 0:
+        return [1]
+    k = S.sperm_bound_primes(np.abs(a) + np.eye(n, dtype=np.int64))
+    xs = np.arange(n + 1, dtype=np.int64) - n // 2
+    mats = xs[:, None, None] * np.eye(n, dtype=np.int64)[None] - a[None]
+    if np.abs(mats).max() >= 2**31:
+        raise ValueError("entries must fit int32")
+    res, _ = S.sperm_permanent(torch.tensor(mats, dtype=torch.int32, device=device), min_primes=k, max_primes=k)
+    coef = S.sperm_interpolate_mod(res.cpu().numpy().view(np.uint32), xs, k)
+    return S.residues_to_ints(coef, k)

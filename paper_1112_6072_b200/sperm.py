@@ -56,6 +56,7 @@ _SIGS = {
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_kendall_tau": (_I, [_P, _P, _I64, _P, _P]),
     "sperm_list_schedule": (_I, [_P, _P, _I64, _I, _P, _P]),
+    "sperm_interpolate_mod": (_I, [_P, _I, _P, _I, _I, _P, _I]),
     "sperm_launch_count": (_I64, [_I]),
     "sperm_timing_enable": (None, [_I]),
     "sperm_timing_reset": (None, []),
@@ -358,6 +359,18 @@ def sperm_schedule(weights, machines: int, policy: str = "estimate", seed: int =
                                 int(seed) & (2**64 - 1), machine.ctypes.data if count else None,
                                 order.ctypes.data if count else None, loads.ctypes.data))
     return machine, order, loads
+
+
+def sperm_interpolate_mod(values, xs, k: int):
+    """Coefficients (mod the first k primes) of the polynomial through (xs[j], values[j] mod p_q):
+    values uint32 [npts, >= k]; returns uint32 [npts, KMAX] (row t = coefficient of x^t)."""
+    v = np.ascontiguousarray(np.asarray(values).view(np.uint32) if np.asarray(values).dtype == np.int32
+                             else np.asarray(values, dtype=np.uint32))
+    x = np.ascontiguousarray(np.asarray(xs, dtype=np.int64))
+    npts = x.shape[0]
+    out = np.zeros((npts, KMAX), dtype=np.uint32)
+    _check(lib().sperm_interpolate_mod(v.ctypes.data, v.shape[1], x.ctypes.data, npts, int(k), out.ctypes.data, KMAX))
+    return out
 
 
 def sperm_list_schedule(cost, order, machines: int):

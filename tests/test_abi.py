@@ -187,3 +187,24 @@ def test_list_schedule_matches_oracle_ls():
         assert abs(S.replay_efficiency(cost, order, m) - cost.sum() / (m * max(ol))) < 1e-12
     with pytest.raises(S.SpermError):
         S.sperm_list_schedule([1.0, 2.0], [0, 0], 2)
+
+
+def test_interpolate_mod_matches_exact_lagrange():
+    """sperm_interpolate_mod (Newton mod p, host C++) + sperm_crt = exact rational Lagrange
+    (oracle.permanent.polynomial_from_values) on random integer polynomials, points spread
+    around 0 and arbitrary distinct points."""
+    from oracle.permanent import polynomial_from_values
+    rng = np.random.default_rng(19)
+    for _ in range(25):
+        deg = int(rng.integers(0, 30))
+        coef = [int(c) for c in rng.integers(-10**12, 10**12, size=deg + 1)]
+        xs = list(range(-(deg // 2), deg + 1 - deg // 2)) if rng.random() < 0.5 else \
+            [int(v) for v in rng.choice(np.arange(-200, 200), size=deg + 1, replace=False)]
+        vals = [sum(c * x ** t for t, c in enumerate(coef)) for x in xs]
+        assert polynomial_from_values(xs, vals) == coef
+        k = 3
+        res = np.array([[v % S.sperm_prime(q) for q in range(S.KMAX)] for v in vals], dtype=np.uint64).astype(np.uint32)
+        got = S.residues_to_ints(S.sperm_interpolate_mod(res, xs, k), k)
+        assert got == coef
+    with pytest.raises(S.SpermError):
+        S.sperm_interpolate_mod(np.zeros((2, 8), dtype=np.uint32), [3, 3], 2)

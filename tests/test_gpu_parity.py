@@ -600,3 +600,29 @@ def test_permanent_host_buffers():
     b = (rng.integers(-5, 6, size=(9, 11, 11)) * (rng.random((9, 11, 11)) < 0.4)).astype(np.int32)
     assert P.sperm_permanent_host(b, min_primes=3) == [per_ryser_nw_gray(m) for m in b]
     assert P.sperm_permanent_host(np.zeros((0, 5, 5), dtype=np.int32)) == []
+
+
+# ------------------------------------------------------------------ NEXT-3: case study 3 and Eq. (11)
+def test_permanental_polynomial_c20_and_small():
+    """pipeline.permanental_polynomial (R-NW at n + 1 points in one batched call, modular
+    interpolation, CRT) = the oracle's polynomial of C20 (frontier values + exact Lagrange) and
+    the brute-force expansion of Eq. (11) on random signed matrices n <= 7."""
+    from test_oracle import c20_polynomial
+    from oracle.permanent import permanental_polynomial as oracle_poly
+    assert pipeline.permanental_polynomial(dodecahedron()) == c20_polynomial()
+    rng = np.random.default_rng(23)
+    for _ in range(12):
+        n = int(rng.integers(1, 8))
+        a = rng.integers(-4, 5, size=(n, n)) * (rng.random((n, n)) < 0.6)
+        assert pipeline.permanental_polynomial(a) == oracle_poly(a)
+
+
+def test_case_study3_c60_i_plus_a():
+    """Case study 3 (Table 4): per(I + A) of C60 — the 4-regular matrix of the
+    permanental-polynomial study — through the whole path, against the C frontier DP."""
+    from oracle.cfrontier import per_frontier_c
+    from oracle.frontier import bfs_order
+    a = truncated_icosahedron() + np.eye(60, dtype=np.int64)
+    want = per_frontier_c(a, bfs_order(truncated_icosahedron()))
+    r = pipeline.permanent(a, jobs_at_least=123, leaf_order=24)
+    assert r.value == want

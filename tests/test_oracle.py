@@ -334,3 +334,42 @@ def test_crt_roundtrip():
         if abs(x) >= M // 2:
             continue
         assert crt([x % p for p in primes], primes) == x
+
+
+# ---------------------------------------------------------------- permanental polynomial
+def test_permanental_polynomial_oracle_pins():
+    """Eq. (11) (PAPER.md:519-531), P(x) = per(xI - A):
+      * K_n (A = J - I): c_k = (-1)^(n-k) C(n, k) D_(n-k) (fixed points take x, the rest derange);
+      * Lagrange through brute-force values = the brute-force expansion (random signed, n <= 6);
+      * C20 (frontier DP values at 21 points): c_20 = 1, c_19 = -trace = 0, c_18 = |E| = 30,
+        c_17 = -2 * triangles = 0, c_0 = per(A) = 1392, sum |c_t| = per(I + A)."""
+    from oracle.cfrontier import per_frontier_c
+    from oracle.permanent import permanental_polynomial, polynomial_from_values
+    D = [1, 0]
+    for m in range(2, 9):
+        D.append((m - 1) * (D[m - 1] + D[m - 2]))
+    for n in range(1, 7):
+        a = np.ones((n, n), dtype=np.int64) - np.eye(n, dtype=np.int64)
+        want = [(-1) ** (n - k) * math.comb(n, k) * D[n - k] for k in range(n + 1)]
+        assert permanental_polynomial(a) == want
+    rng = np.random.default_rng(41)
+    for _ in range(20):
+        n = int(rng.integers(1, 7))
+        a = rng.integers(-3, 4, size=(n, n)) * (rng.random((n, n)) < 0.6)
+        xs = list(range(-(n // 2), n + 1 - n // 2))
+        vs = [per_bruteforce(x * np.eye(n, dtype=np.int64) - a) for x in xs]
+        assert polynomial_from_values(xs, vs) == permanental_polynomial(a)
+    c = c20_polynomial()
+    assert c[20] == 1 and c[19] == 0 and c[18] == 30 and c[17] == 0 and c[0] == 1392
+    ipa = per_frontier_c(dodecahedron() + np.eye(20, dtype=np.int64))
+    assert sum(abs(v) for v in c) == ipa
+    assert all((v >= 0) == ((20 - t) % 2 == 0) or v == 0 for t, v in enumerate(c))  # alternating signs
+
+
+def c20_polynomial():
+    """Oracle permanental polynomial of C20: frontier-DP values at x = -10..10, exact Lagrange."""
+    from oracle.cfrontier import per_frontier_c
+    from oracle.permanent import polynomial_from_values
+    a = dodecahedron().astype(np.int64)
+    xs = list(range(-10, 11))
+    return polynomial_from_values(xs, [per_frontier_c(x * np.eye(20, dtype=np.int64) - a) for x in xs])
