@@ -393,6 +393,9 @@ def bench_strong(P, torch, dist, rank, world, dev, jobs, leaf):
             w[f"{pol}_{asg}"] = {"TN_s": tn, "efficiency": w["T1_s"] / (world * tn) if tn else None,
                                  "speedup": w["T1_s"] / tn if tn else None, "per": str(r.value),
                                  "exact": (r.value == g) if g is not None else None}
+            if asg == "dynamic":  # rank 0's claims on the box-wide device queue (CUDA IPC counter)
+                c = r.stats.get("claims", 0)
+                w[f"{pol}_{asg}"]["queue"] = {"claims_rank0": c, "us_per_claim": 1e6 * r.stats.get("claim_s", 0.0) / max(c, 1)}
         res["workloads"][name] = w
     return res
 

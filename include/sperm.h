@@ -270,6 +270,28 @@ int sperm_list_schedule(const double* h_cost, const int32_t* h_order, int64_t co
 int sperm_interpolate_mod(const uint32_t* h_values, int stride, const int64_t* h_x, int npts, int k,
                           uint32_t* h_coef, int coef_stride);
 
+/* ---------------------------------------------------------------- box-wide queue */
+/* A dynamic work queue shared by the GPUs of one node: the improved Step 3's "currently least
+ * loaded processor" across GPUs — every rank claims the next chunk of
+ * the shared (estimate) job order when it runs out of work.  The counter lives in rank 0's device
+ * memory; peers map it through CUDA IPC and claim with a system-scope atomicAdd over
+ * NVLink / NVSwitch.
+ *  sperm_queue_create  (rank 0) allocates a zeroed uint64 counter on the current device; writes
+ *                      its IPC handle (SPERM_QUEUE_HANDLE_BYTES bytes) to h_handle, which the
+ *                      caller sends to the peers (e.g. through the process group's store).
+ *  sperm_queue_open    (peers) maps the counter from the handle (another process; same or
+ *                      another device of the node).
+ *  sperm_queue_claim   start = atomicAdd(counter, chunk) (a one-thread kernel on `stream`),
+ *                      through the caller's 8-byte DEVICE scratch d_scratch (on the current
+ *                      device); synchronous: *h_start receives the claimed range's first index.
+ *  sperm_queue_close   owner != 0: frees the counter (after every peer closed it); else unmaps.
+ * Errors: SPERM_ERR_ARG, SPERM_ERR_CUDA. */
+#define SPERM_QUEUE_HANDLE_BYTES 64
+int sperm_queue_create(void** d_counter, void* h_handle);
+int sperm_queue_open(const void* h_handle, void** d_counter);
+int sperm_queue_claim(void* d_counter, int64_t chunk, void* d_scratch, int64_t* h_start, void* stream);
+int sperm_queue_close(void* d_counter, int owner);
+
 /* ---------------------------------------------------------------- statistics */
 /* sperm_kendall_tau — Kendall's rank correlation of (x_i, y_i), i < m, with the tie correction
  * of Eq. (10) (Eqs. (7)-(9)): S = sum_{i<j} sign(x_j - x_i) sign(y_j - y_i),

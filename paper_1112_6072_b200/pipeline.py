@@ -231,18 +231,56 @@ def gather_estimates(est_part, group=None):
     return _allreduce_sum(est_part, group)
 
 
-def dynamic_chunks(order, chunk: int, store, key: str):
+def dynamic_chunks(order, chunk: int, claim):
     """The paper's dynamic Step 3 across ranks (each job goes to the
     first free processor, in estimate order): every rank repeatedly claims the next `chunk` jobs
-    of the shared order from one atomic counter in the torch.distributed store (store.add), so a
-    rank that finishes early takes more.  Yields the claimed job ids; over all ranks every job is
-    claimed exactly once."""
+    of the shared order — claim(chunk) returns the first index of a fresh range of the shared
+    counter — so a rank that finishes early takes more.  Yields the claimed job ids; over all
+    ranks every job is claimed exactly once."""
     order = np.asarray(order)
     while True:
-        start = int(store.add(key, chunk)) - chunk
+        start = int(claim(chunk))
         if start >= len(order):
             return
         yield order[start:start + chunk]
+
+
+def store_claimer(store, key: str):
+    """claim() through the torch.distributed store's atomic add (a host TCP round trip)."""
+    return lambda chunk: int(store.add(key, chunk)) - chunk
+
+
+class DeviceClaimer:
+    """claim() through the box-wide device queue (sperm_queue_*): rank 0 creates the counter in
+    its HBM and publishes the IPC handle in the store; the other ranks map it and claim with a
+    system-scope atomicAdd over NVLink.  close() unmaps (peers) / frees (owner, after a barrier)."""
+
+    def __init__(self, store, key: str, rank: int, group=None):
+        self.group, self.rank = group, rank
+        if rank == 0:
+            self.q = S.DeviceQueue()
+            store.set(key, self.q.handle)
+        else:
+            self.q = S.DeviceQueue(handle=store.get(key))
+        self.claims = 0
+        self.claim_s = 0.0
+
+    def __call__(self, chunk: int) -> int:
+        import time
+        t0 = time.perf_counter()
+        v = self.q.claim(chunk)
+        self.claim_s += time.perf_counter() - t0
+        self.claims += 1
+        return v
+
+    def close(self):
+        import torch.distributed as dist
+        if self.rank != 0:
+            self.q.close()
+        if self.group is not None and dist.get_world_size(self.group) > 1:
+            dist.barrier(group=self.group)  # every peer has unmapped the counter
+        if self.rank == 0:
+            self.q.close()
 
 
 _dynamic_calls = 0
@@ -268,15 +306,17 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
               device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30,
               assignment: str = "static", store=None, dynamic_chunk: int = 0,
-              fold_every: int = FOLD_EVERY) -> PHResult:
+              fold_every: int = FOLD_EVERY, queue: str = "device") -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
 
     With a torch.distributed `group` of world size G, every rank replicates the
     (cheap, deterministic) pre-expansion and scheduling, estimates its share of the jobs,
     evaluates only the jobs assigned to it, and one all-reduce sums the residue accumulators.
     assignment="static": the LPT plan of sperm_schedule (S1); "dynamic": ranks claim chunks of
-    the policy's job order from a shared counter in `store` (default: the process group's
-    store) as they finish — the paper's first-free-processor rule across GPUs.
+    the policy's job order from one shared counter as they finish — the paper's first-free-
+    processor rule across GPUs; queue="device": the counter is in rank 0's HBM, claimed with
+    system-scope atomics through CUDA IPC (sperm_queue_*; the IPC handle travels through
+    `store`, default the process group's store); queue="store": the store's own atomic add.
     policy: "estimate" (KKLLL weights, the improved Step 3), "natural", "random", or "size"
     (the job's nonzero count as the LPT weight).  The uint64 accumulators gain < 2^31 per leaf, so they are folded mod p (sperm_fold_mod)
     before more than `fold_every` leaves have been added since the last fold, and before the
@@ -341,13 +381,18 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             for b0 in range(0, len(sel), batch_jobs):
                 yield s, sel[b0:b0 + batch_jobs]
 
+    claimer = None
+
     def dynamic_batches():
+        nonlocal claimer
         global _dynamic_calls
         _dynamic_calls += 1
         st = store if store is not None else dist.distributed_c10d._get_default_store()
+        key = f"sperm_dynamic_{_dynamic_calls}"
+        claimer = DeviceClaimer(st, key, rank, group) if queue == "device" else store_claimer(st, key)
         starts = np.cumsum([0] + [s.count for s in jobsets])  # job ids are numbered set by set
         chunk = dynamic_chunk or max(1, num_jobs // (16 * world))
-        for jobs in dynamic_chunks(order, chunk, st, f"sperm_dynamic_{_dynamic_calls}"):
+        for jobs in dynamic_chunks(order, chunk, claimer):
             which = np.searchsorted(starts, jobs, side="right") - 1
             for si, s in enumerate(jobsets):
                 mine = jobs[which == si] - starts[si]
@@ -384,6 +429,9 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
             stats["rnw_host_s"] += time.perf_counter() - t_r
             leaves += lv.count
             terms += S.sperm_rnw_terms(lv.n, lv.count)
+    if isinstance(claimer, DeviceClaimer):
+        stats["claims"], stats["claim_s"] = claimer.claims, claimer.claim_s
+        claimer.close()
     if world > 1:
         S.sperm_fold_mod(acc, stream=rnw_stream)  # each rank's rows < 2^31: the G-rank sum fits
     main.wait_stream(rnw_stream)

@@ -57,6 +57,10 @@ _SIGS = {
     "sperm_kendall_tau": (_I, [_P, _P, _I64, _P, _P]),
     "sperm_list_schedule": (_I, [_P, _P, _I64, _I, _P, _P]),
     "sperm_interpolate_mod": (_I, [_P, _I, _P, _I, _I, _P, _I]),
+    "sperm_queue_create": (_I, [_P, _P]),
+    "sperm_queue_open": (_I, [_P, _P]),
+    "sperm_queue_claim": (_I, [_P, _I64, _P, _P, _P]),
+    "sperm_queue_close": (_I, [_P, _I]),
     "sperm_launch_count": (_I64, [_I]),
     "sperm_timing_enable": (None, [_I]),
     "sperm_timing_reset": (None, []),
@@ -391,6 +395,39 @@ def replay_efficiency(cost, order, machines: int) -> float:
     _, loads = sperm_list_schedule(cost, order, machines)
     mk = loads.max()
     return float(np.sum(cost) / (machines * mk)) if mk > 0 else 1.0
+
+
+# --------------------------------------------------------------------- box-wide queue
+QUEUE_HANDLE_BYTES = 64
+
+
+class DeviceQueue:
+    """The box-wide dynamic queue (sperm_queue_*): a uint64 counter in rank 0's device memory,
+    mapped by the other ranks through CUDA IPC; claim(chunk) -> first index of the claimed range."""
+
+    def __init__(self, handle: Optional[bytes] = None):
+        import torch
+        self.ptr = ctypes.c_void_p(0)
+        self.owner = handle is None
+        if self.owner:
+            buf = ctypes.create_string_buffer(QUEUE_HANDLE_BYTES)
+            _check(lib().sperm_queue_create(ctypes.byref(self.ptr), buf))
+            self.handle = buf.raw
+        else:
+            buf = ctypes.create_string_buffer(bytes(handle), QUEUE_HANDLE_BYTES)
+            _check(lib().sperm_queue_open(buf, ctypes.byref(self.ptr)))
+            self.handle = bytes(handle)
+        self.scratch = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def claim(self, chunk: int, stream=None) -> int:
+        start = ctypes.c_int64(0)
+        _check(lib().sperm_queue_claim(self.ptr, int(chunk), _ptr(self.scratch), ctypes.byref(start), _stream(stream)))
+        return start.value
+
+    def close(self):
+        if self.ptr:
+            _check(lib().sperm_queue_close(self.ptr, 1 if self.owner else 0))
+            self.ptr = ctypes.c_void_p(0)
 
 
 # --------------------------------------------------------------------- statistics

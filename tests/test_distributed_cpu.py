@@ -108,7 +108,7 @@ def _dyn_worker(rank, world, port, q):
         order = np.argsort(-np.array([abs(v) for v in vals]), kind="stable")  # any shared order
         store = dist.distributed_c10d._get_default_store()
         mine = []
-        for chunk in pipeline.dynamic_chunks(order, 3, store, "test_dynamic"):
+        for chunk in pipeline.dynamic_chunks(order, 3, pipeline.store_claimer(store, "test_dynamic")):
             mine.extend(int(j) for j in chunk)
             time.sleep(0.002 * (rank + 1))  # ranks of different speed: the faster claims more
         k = P.sperm_bound_primes(dodecahedron())

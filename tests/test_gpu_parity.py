@@ -308,6 +308,10 @@ def test_pipeline_dynamic_assignment_single_rank():
     r2 = pipeline.permanent(a, jobs_at_least=128, leaf_order=18, assignment="dynamic", store=store, dynamic_chunk=5)
     assert r2.value == r1.value == golden("C60_truncated_icosahedron")
     assert r2.job_values == r1.job_values
+    assert r2.stats["claims"] == -(-r1.num_jobs // 5) + 1  # device queue: every chunk + the empty claim
+    r3 = pipeline.permanent(a, jobs_at_least=128, leaf_order=18, assignment="dynamic", store=store, dynamic_chunk=7,
+                            queue="store")
+    assert r3.job_values == r1.job_values
 
 
 def test_pipeline_c60_l32_every_job():
@@ -532,11 +536,13 @@ def _ws2_worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     res = {}
     for name, a, J, L in (("C20", dod(), 30, 8), ("C60", ti(), 128, 18)):
-        for policy, asg in (("estimate", "static"), ("estimate", "dynamic"), ("size", "static"),
-                            ("natural", "static"), ("random", "static")):
+        for policy, asg, q in (("estimate", "static", "device"), ("estimate", "dynamic", "device"),
+                               ("estimate", "dynamic", "store"), ("size", "static", "device"),
+                               ("natural", "static", "device"), ("random", "static", "device")):
             r = pl.permanent(a, jobs_at_least=J, leaf_order=L, policy=policy, assignment=asg,
-                             group=dist.group.WORLD, dynamic_chunk=3)
-            res[f"{name}_{policy}_{asg}"] = (r.value, r.job_values, r.machine.tolist(), r.num_jobs)
+                             group=dist.group.WORLD, dynamic_chunk=3, queue=q)
+            res[f"{name}_{policy}_{asg}_{q}"] = (r.value, r.job_values, r.machine.tolist(), r.num_jobs,
+                                                 r.stats.get("claims", 0))
     import pickle
     with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as f:
         pickle.dump(res, f)
@@ -562,8 +568,12 @@ def test_pipeline_two_ranks_gloo_same_device(tmp_path):
     c20_jobs = [node_permanent(j) for j in pre_expand(dodecahedron(), jobs_at_least=30)]
     single_c60 = pipeline.permanent(truncated_icosahedron(), jobs_at_least=128, leaf_order=18)
     for key in rs[0]:
-        v0, jv0, mach0, nj = rs[0][key]
-        v1, jv1, mach1, _ = rs[1][key]
+        v0, jv0, mach0, nj, c0 = rs[0][key]
+        v1, jv1, mach1, _, c1 = rs[1][key]
+        if "dynamic_device" in key:  # IPC-mapped counter: every chunk claimed once over both ranks
+            assert c0 + c1 == -(-nj // 3) + 2, key
+        if key.endswith("static_device"):
+            key = key[:-len("_device")]
         assert v0 == v1 and jv0 == jv1 and mach0 == mach1, key
         if key.startswith("C20"):
             assert v0 == 1392 and jv0 == c20_jobs, key
