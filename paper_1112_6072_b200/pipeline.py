@@ -302,7 +302,67 @@ def reconstruct(res, k: int):
     return [S.sperm_crt(res[j], k) for j in range(res.shape[0] - 1)], S.sperm_crt(res[-1], k)
 
 
-def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 20, trials: int = 0,
+def _eval_jobs(jobsets, jobs, L, num_jobs, k_total, nonneg, device, acc):
+    """Expand the given job ids to leaves of order <= L and evaluate them (R-NW) into `acc`."""
+    import torch
+    starts = np.cumsum([0] + [s.count for s in jobsets])
+    jobs = np.asarray(jobs)
+    which = np.searchsorted(starts, jobs, side="right") - 1
+    for si, s in enumerate(jobsets):
+        mine = jobs[which == si] - starts[si]
+        if not len(mine):
+            continue
+        idx = torch.tensor(mine, dtype=torch.int64, device=device)
+        batch = NodeSet(s.n, s.mats.index_select(0, idx), s.coef.index_select(0, idx), s.job.index_select(0, idx))
+        for lv in iter_leaves(batch, L):
+            if lv.n > S.NMAX:
+                return False
+            S.sperm_permanent(lv.mats, coef=lv.coef, job=lv.job, num_jobs=num_jobs, min_primes=k_total,
+                              max_primes=k_total if nonneg else 0, job_acc=acc)
+    return True
+
+
+def choose_leaf_order(jobsets, order, num_jobs, k_total, nonneg, device, sample_frac: float = 0.01,
+                      start: int = 16, lo: int = 8, hi: int = 32):
+    """Reading R5's leaf order L chosen per workload by measurement (NEXT-1): the jobs at evenly
+    spaced positions of the estimate order (about `sample_frac` of them, at least 2) are expanded
+    to leaves of order <= L and evaluated, timed with CUDA events, for L = start and then one
+    step at a time in the direction that got faster (hill climbing) until it stops improving.
+    H_per's own rule stops at order 2 and never reaches s >= 5 on 3-regular
+    inputs; the balance between the expansion's node count and the R-NW's 2^(L-1)
+    terms per leaf is machine-dependent, so it is measured.  Returns (L, {L: seconds})."""
+    import torch
+    order = np.asarray(order)
+    m = max(2, int(round(sample_frac * len(order))))
+    pick = order[np.linspace(0, len(order) - 1, num=min(m, len(order))).round().astype(int)]
+    scratch = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
+    times = {}
+
+    def t_of(L):
+        if L not in times:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            ok = _eval_jobs(jobsets, pick, L, num_jobs, k_total, nonneg, device, scratch)
+            e1.record()
+            torch.cuda.synchronize()
+            times[L] = e0.elapsed_time(e1) * 1e-3 if ok else float("inf")
+        return times[L]
+
+    L = max(lo, min(hi, start))
+    best = t_of(L)
+    for step in (-1, 1):
+        moved = False
+        while lo <= L + step <= hi and t_of(L + step) < best:
+            L += step
+            best = times[L]
+            moved = True
+        if moved:
+            break
+    return L, {str(k): v for k, v in sorted(times.items())}
+
+
+def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order=20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
               device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30,
               assignment: str = "static", store=None, dynamic_chunk: int = 0,
@@ -317,6 +377,7 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     processor rule across GPUs; queue="device": the counter is in rank 0's HBM, claimed with
     system-scope atomics through CUDA IPC (sperm_queue_*; the IPC handle travels through
     `store`, default the process group's store); queue="store": the store's own atomic add.
+    leaf_order: L of reading R5, or "auto" (choose_leaf_order: measured on a sample of the jobs).
     policy: "estimate" (KKLLL weights, the improved Step 3), "natural", "random", or "size"
     (the job's nonzero count as the LPT weight).  The uint64 accumulators gain < 2^31 per leaf, so they are folded mod p (sperm_fold_mod)
     before more than `fold_every` leaves have been added since the last fold, and before the
@@ -356,10 +417,20 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order: int = 2
     acc = torch.zeros((num_jobs + 1, S.KMAX), dtype=torch.int64, device=device)
     job_cycles = torch.zeros(num_jobs, dtype=torch.int64, device=device) if measure_jobs else None
     pos = rank_positions(machine, order, rank)
+    if leaf_order == "auto":
+        leaf_order, stats_auto = choose_leaf_order(jobsets, order, num_jobs, k_total, nonneg, device)
+        if world > 1:  # every rank uses rank 0's choice
+            box = [leaf_order]
+            dist.broadcast_object_list(box, src=0, group=group)
+            leaf_order = int(box[0])
+    else:
+        stats_auto = None
     leaves = 0
     terms = 0.0
     import time
-    stats = {"rnw_calls": 0, "rnw_host_s": 0.0, "leaf_sets": 0, "t_loop_s": 0.0}
+    stats = {"rnw_calls": 0, "rnw_host_s": 0.0, "leaf_sets": 0, "t_loop_s": 0.0, "leaf_order": leaf_order}
+    if stats_auto is not None:
+        stats["leaf_order_auto"] = stats_auto
     t_loop = time.perf_counter()
     # Every stage runs on the caller's stream.  SPERM_PIPELINE_OVERLAP=1 puts the R-NW batches on
     # a stream of their own instead, so that the next chunk's expansion could overlap them; the

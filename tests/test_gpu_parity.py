@@ -636,3 +636,15 @@ def test_case_study3_c60_i_plus_a():
     want = per_frontier_c(a, bfs_order(truncated_icosahedron()))
     r = pipeline.permanent(a, jobs_at_least=123, leaf_order=24)
     assert r.value == want
+
+
+def test_pipeline_auto_leaf_order():
+    """leaf_order="auto" (NEXT-1): L measured on a sample of the jobs; the value and every job
+    value are those of a fixed-L run, and the choice is one of the timed candidates."""
+    a = truncated_icosahedron()
+    r = pipeline.permanent(a, jobs_at_least=128, leaf_order="auto")
+    r0 = pipeline.permanent(a, jobs_at_least=128, leaf_order=18)
+    assert r.value == golden("C60_truncated_icosahedron") and r.job_values == r0.job_values
+    times = r.stats["leaf_order_auto"]
+    L = r.stats["leaf_order"]
+    assert str(L) in times and times[str(L)] == min(times.values())
