@@ -81,6 +81,23 @@ __host__ __device__ constexpr int tree_min_blocks(int B, int nfix, int gf) {
                  : (3 * B + nfix <= 20 ? 3 : 2);
 }
 constexpr int kMaxLow = 8;  // low columns picked per leaf
+// Tree-kernel block loop variants (A-B builds, tools/build_variant.py): a flip of a high column
+// touches few rows of a sparse leaf; kSparseW adds its column only to the touched row-sum groups,
+// kSparseE recomputes only the touched low columns' E_c and fixed-row groups (warp-uniform masks).
+// Measured on configs[1]: sparse W 0.164 vs 0.160 ms (predicated, no fewer issue slots), sparse E
+// 0.159 (neutral); both off by default.
+#ifndef SPERM_RNW_SPARSE_W
+#define SPERM_RNW_SPARSE_W 0
+#endif
+#ifndef SPERM_RNW_SPARSE_E
+#define SPERM_RNW_SPARSE_E 0
+#endif
+#ifndef SPERM_RNW_BLOCK_UNROLL  // measured (configs[1] kernel ms/step): 1: 0.160, 2: 0.151, 3: 0.150,
+#define SPERM_RNW_BLOCK_UNROLL 4  // 4: 0.146, 8: 0.151 (more independent chains in flight per warp)
+#endif
+constexpr bool kSparseW = SPERM_RNW_SPARSE_W != 0;
+constexpr bool kSparseE = SPERM_RNW_SPARSE_E != 0;
+constexpr int kBlockUnroll = SPERM_RNW_BLOCK_UNROLL;
 
 // the CRT primes (kPrimes, common.cuh) and p^-1 mod 2^32
 __constant__ int32_t c_p[SPERM_KMAX] = {2147483647, 2147483629, 2147483587, 2147483579,
@@ -590,9 +607,9 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_generic_kernel(
 
 // ============================================================================ tree kernel
 // shared memory per warp (words): colpos[nh][S4] | colneg[nh][S4] (bank-shifted) | w0[S4] |
-// delta[NS]
+// delta[NS] | mask[nh]
 struct TreeSmem {
-  int S4, nh, pos, neg, w0, delta, words;
+  int S4, nh, pos, neg, w0, delta, mask, words;
 };
 __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
   TreeSmem t;
@@ -602,7 +619,8 @@ __host__ __device__ inline TreeSmem tree_smem(int NRT, int NS, int n, int B) {
   t.neg = ((t.nh * t.S4 + 31) / 32) * 32 + 16;
   t.w0 = ((t.neg + t.nh * t.S4 + 3) / 4) * 4;
   t.delta = t.w0 + t.S4;
-  t.words = ((t.delta + NS + 3) / 4) * 4;
+  t.mask = t.delta + NS;
+  t.words = ((t.mask + t.nh + 3) / 4) * 4;
   return t;
 }
 
@@ -667,6 +685,15 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         const int row = pr[s];
         sm[L.delta + s] = row >= 0 ? 2 * a[row * n + pc[s / KS]] : 0;
       }
+      __syncwarp();
+      // what a flip of high column h touches (sparse leaves: a column has few rows): bit v < 16 =
+      // row-sum group W[4v..4v+3], bit 16 + c = low column c's slot rows, bit 24 = a fixed row
+      for (int h = lane; h < L.nh; h += 32) {
+        uint32_t mk = 0;
+        for (int r = 0; r < NRT; ++r)
+          if (sm[L.pos + h * S4 + r] != 0) mk |= (1u << (r >> 2)) | (r < NS ? 1u << (16 + r / KS) : 1u << 24);
+        sm[L.mask + h] = (int32_t)mk;
+      }
       emode = pr[kPermGend];
       __syncwarp();
       cur_leaf = leaf;
@@ -695,33 +722,43 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     // the block loop, instantiated for the leaf's prime count K = 1, 2, 3 (straight-line prime
     // loops) and for K = SPERM_KMAX with a runtime bound; the E mode is tested once per block.
     // (measured: configs[1] kernel 0.235 -> 0.186 ms/step, order-15 leaves 34 -> 26 ms / 4M)
+    // E_c and the fixed-row group products persist across blocks: a block recomputes only what
+    // the flipped high column touches (its warp-uniform mask; the first block computes all)
+    constexpr int NP2 = (B + 1) / 2, NP4 = (B + 3) / 4;
+    int32_t E[B], FG[NGF];
     auto blocks = [&](auto kc) {
       constexpr int K = decltype(kc)::value;
+#pragma unroll kBlockUnroll
       for (uint32_t ob = 0; ob < nblk; ++ob) {
-        if (ob) {  // flip high Gray bit B + hh (warp-uniform column)
+        uint32_t mk = 0xffffffffu;
+        if (ob) {  // flip high Gray bit B + hh (warp-uniform column): only the touched row groups
           const int hh = __ffs(ob) - 1;
+          mk = (uint32_t)sm[L.mask + hh];
           const bool add = !(((O0 + ob) >> (hh + 1)) & 1ull);
           const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
 #pragma unroll
           for (int v = 0; v < S4 / 4; ++v) {
-            const int4 d = col[v];
-            W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
+            if (!(kSparseW) || (mk & (1u << v))) {
+              const int4 d = col[v];
+              W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
+            }
           }
         }
         // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1); exact products
         // of pairs and quads of the E_c (used when the leaf's E mode says they fit int32;
         // wrapped otherwise and then unused)
-        constexpr int NP2 = (B + 1) / 2, NP4 = (B + 3) / 4;
-        int32_t E[B], P2[NP2], P4[NP4];
+        int32_t P2[NP2], P4[NP4];
 #pragma unroll
         for (int c = 0; c < B; ++c) {
-          int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
+          if (!(kSparseE) || (mk & (1u << (16 + c)))) {
+            int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
 #pragma unroll
-          for (int s = 1; s < KS; ++s) {
-            x0 *= W[c * KS + s];
-            x1 *= W[c * KS + s] + D[c * KS + s];
+            for (int s = 1; s < KS; ++s) {
+              x0 *= W[c * KS + s];
+              x1 *= W[c * KS + s] + D[c * KS + s];
+            }
+            E[c] = x0 - x1;
           }
-          E[c] = x0 - x1;
         }
 #pragma unroll
         for (int j = 0; j < NP2; ++j)
@@ -729,13 +766,14 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
 #pragma unroll
         for (int j = 0; j < NP4; ++j)
           P4[j] = 2 * j + 1 < NP2 ? (int32_t)((uint32_t)P2[2 * j] * (uint32_t)P2[2 * j + 1]) : P2[2 * j];
-        int32_t FG[NGF];
+        if (!(kSparseE) || (mk & (1u << 24))) {
 #pragma unroll
-        for (int g = 0; g < NGF; ++g) {
-          int32_t x = W[NS + g * GF];
+          for (int g = 0; g < NGF; ++g) {
+            int32_t x = W[NS + g * GF];
 #pragma unroll
-          for (int r = 1; r < GF; ++r) x *= W[NS + g * GF + r];
-          FG[g] = x;
+            for (int r = 1; r < GF; ++r) x *= W[NS + g * GF + r];
+            FG[g] = x;
+          }
         }
         // the sign (-1)^{|high Gray bits|} rides on the first factor (prime-independent): the
         // Montgomery chain then yields a residue of the signed block value, congruent mod p
@@ -1544,9 +1582,9 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     std::vector<int> order;
   };
   thread_local Spec spec;
-  const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables (read per call: the bench
-    const char* e = getenv("SPERM_SPECULATE");  // times both settings in one process)
-    return !(e && e[0] == '0');
+  const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=1 enables (read per call: the bench
+    const char* e = getenv("SPERM_SPECULATE");  // times both settings in one process); measured
+    return e && e[0] == '1';  // slower in round 2 (configs[1] 0.203 vs 0.195 ms/step), so off
   }();
   int dev = 0;
   SPERM_TRY(cudaGetDevice(&dev));

@@ -15,7 +15,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsperm.so")
+# SPERM_LIB: an alternative in-tree build of the library (A-B variants, tools/build_variant.py)
+LIB_PATH = os.environ.get("SPERM_LIB") or os.path.join(_HERE, "libsperm.so")
 
 KMAX = 8
 NMAX = 48

@@ -367,7 +367,15 @@ def _plans_agree(mats, want):
 def test_rnw_speculative_groups_repeat_and_change():
     """Same-shape calls launch the previous call's plan groups before the histogram read-back
     (csrc/rnw.cu rnw_spec_check_kernel): repeats, same-shape batches with other contents and other
-    plan histograms must all stay exact."""
+    plan histograms must all stay exact.  (Speculation is off by default; SPERM_SPECULATE=1.)"""
+    os.environ["SPERM_SPECULATE"] = "1"
+    try:
+        _speculative_cases()
+    finally:
+        os.environ.pop("SPERM_SPECULATE", None)
+
+
+def _speculative_cases():
     a = random_3perm_batch(16, 20, seed=11)
     a2 = random_3perm_batch(16, 20, seed=12)
     rng = np.random.default_rng(7)
