@@ -54,30 +54,57 @@ def parse():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML (pynvml, in-process: no
+    nvidia-smi processes competing with the host launch path) every 2 ms of the timed region,
+    plus one sample at start and stop; falls back to nvidia-smi if NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvml"
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            self.source = "nvidia-smi"
+
+    def _sample(self):
+        if self.nv is not None:
+            nv = self.nv
+            sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.rows.append((float(sm), float(self.max_mhz),
+                              [name for name, attr in self.REASONS if bits & getattr(nv, attr)]))
+        else:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+            r = [x.strip() for x in out.strip().split(",")]
+            if len(r) >= 6:
+                self.rows.append((float(r[0]), float(r[1]), [self.REASONS[i][0] for i in range(4)
+                                                             if "Active" in r[2 + i] and "Not" not in r[2 + i]]))
 
     def start(self):
+        self._sample()
+
         def run():
-            while not self._stop.is_set():
+            while not self._stop.wait(0.002 if self.nv is not None else 0.2):
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    self._sample()
                 except Exception:
                     pass
-                self._stop.wait(0.2)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -85,13 +112,14 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
-                          and "Not" not in r[2 + i]})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        try:
+            self._sample()
+        except Exception:
+            pass
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(r[1] for r in self.rows) if sm else None,
+                "reasons": sorted({x for r in self.rows for x in r[2]}), "samples": len(self.rows),
+                "source": self.source}
 
 
 def peaks():
@@ -194,15 +222,14 @@ def main():
     st_terms, st_fma, st_alu = P.sperm_rnw_stats(reset=True)
     launches = P.sperm_launch_count(reset=True)
     P.sperm_timing_enable(False)
-    clocks = sampler.stop()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     vals = finish(res, k)
-    # the same K steps with the speculative plan-group launch ON (it could only pay on repeated
-    # same-shape batches, which this loop is; it is off by default: measured slower)
-    os.environ["SPERM_SPECULATE"] = "1"
+    # the same K steps with the speculative plan-group launch OFF: it only pays on repeated
+    # same-shape batches (this loop); pipeline leaf sets change shape every call
+    os.environ["SPERM_SPECULATE"] = "0"
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.fill_(i)
@@ -211,6 +238,7 @@ def main():
         ev2[i][1].record(stream)
     torch.cuda.synchronize()
     os.environ.pop("SPERM_SPECULATE", None)
+    clocks = sampler.stop()  # sampled over both loops (same host conditions for the A-B)
     nospec_ms = sum(a.elapsed_time(b) for a, b in ev2)
     # end to end through the public API on HOST buffers: sperm_permanent_host (one C call: H2D of
     # the pinned input batch, R-NW, device CRT, D2H of the exact values) + marshalling to ints
@@ -270,10 +298,11 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_mats.numel() * 4),
                 "d2h_bytes_per_step": int(N_MATS * (P.KMAX + 3) * 4),  # [256][limbs + 1] CRT words
                 "api": "sperm_permanent_host (host buffers; H2D + R-NW + device CRT + D2H in one C call)"},
-        "with_speculation": {"value": terms_step / world * args.steps / (nospec_ms * 1e-3),
-                             "ms_per_step": nospec_ms / args.steps,
-                             "note": "same K steps with SPERM_SPECULATE=1 (rank 0): the previous call's plan groups "
-                                     "launched before the histogram read-back (off by default)"},
+        "without_speculation": {"value": terms_step / world * args.steps / (nospec_ms * 1e-3),
+                                "ms_per_step": nospec_ms / args.steps,
+                                "note": "same K steps with SPERM_SPECULATE=0 (rank 0): no launch of the previous "
+                                        "call's plan groups before the histogram read-back; the speculative launch "
+                                        "only pays on repeated same-shape batches like this loop's"},
         "gpu_launches": launches,
         "clocks": clocks,
         "check": {"per_first": str(vals[0]), "per_last": str(vals[-1])},

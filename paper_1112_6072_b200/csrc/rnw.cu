@@ -95,6 +95,11 @@ constexpr int kMaxLow = 8;  // low columns picked per leaf
 #ifndef SPERM_RNW_BLOCK_UNROLL  // measured (configs[1] kernel ms/step): 1: 0.160, 2: 0.151, 3: 0.150,
 #define SPERM_RNW_BLOCK_UNROLL 4  // 4: 0.146, 8: 0.151 (more independent chains in flight per warp)
 #endif
+#ifndef SPERM_RNW_EFORM  // E_c = Q_c^0 - Q_c^1 evaluation: 0 products of sums, 1 / 2 multiply-add form
+#define SPERM_RNW_EFORM 2  // (configs[1] kernel 0.147 / 0.147 / 0.144 ms)
+#endif
+constexpr int kEForm = SPERM_RNW_EFORM;
+static_assert(SPERM_RNW_EFORM == 0 || KS == 3, "multiply-add E form is written for 3 slot rows");
 constexpr bool kSparseW = SPERM_RNW_SPARSE_W != 0;
 constexpr bool kSparseE = SPERM_RNW_SPARSE_E != 0;
 constexpr int kBlockUnroll = SPERM_RNW_BLOCK_UNROLL;
@@ -714,6 +719,9 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     int32_t D[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) D[s] = sm[L.delta + s];
+    int32_t C12[kEForm == 2 ? B : 1];  // D1 * D2 per low column (E form 2)
+#pragma unroll
+    for (int c = 0; c < (kEForm == 2 ? B : 0); ++c) C12[c] = D[c * KS + 1] * D[c * KS + 2];
     int64_t acc[SPERM_KMAX];
 #pragma unroll
     for (int q = 0; q < SPERM_KMAX; ++q) acc[q] = 0;
@@ -751,13 +759,27 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
 #pragma unroll
         for (int c = 0; c < B; ++c) {
           if (!(kSparseE) || (mk & (1u << (16 + c)))) {
-            int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
+            if constexpr (kEForm == 0) {
+              int32_t x0 = W[c * KS], x1 = W[c * KS] + D[c * KS];
 #pragma unroll
-            for (int s = 1; s < KS; ++s) {
-              x0 *= W[c * KS + s];
-              x1 *= W[c * KS + s] + D[c * KS + s];
+              for (int s = 1; s < KS; ++s) {
+                x0 *= W[c * KS + s];
+                x1 *= W[c * KS + s] + D[c * KS + s];
+              }
+              E[c] = x0 - x1;
+            } else {
+              // -E_c = W0 t + D0 v with t = D1 W2 + D2 (W1 + D1), v = W1 W2 + t = (W1+D1)(W2+D2):
+              // multiply-adds on the FMA pipe instead of adds on the ALU pipe (exact mod 2^32;
+              // the sign (-1)^B of the negated factors rides on f0)
+              const int32_t w0 = W[c * KS], w1 = W[c * KS + 1], w2 = W[c * KS + 2];
+              const int32_t d0 = D[c * KS], d1 = D[c * KS + 1], d2 = D[c * KS + 2];
+              int32_t t;
+              if constexpr (kEForm == 2) t = d2 * w1 + C12[c];
+              else t = d2 * (w1 + d1);
+              t = d1 * w2 + t;
+              const int32_t v = w1 * w2 + t;
+              E[c] = w0 * t + d0 * v;
             }
-            E[c] = x0 - x1;
           }
         }
 #pragma unroll
@@ -777,7 +799,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         }
         // the sign (-1)^{|high Gray bits|} rides on the first factor (prime-independent): the
         // Montgomery chain then yields a residue of the signed block value, congruent mod p
-        const int32_t f0 = ((O0 + ob) & 1ull) ? -FG[0] : FG[0];
+        const int32_t f0 = (((O0 + ob) & 1ull) ^ (kEForm != 0 && (B & 1))) ? -FG[0] : FG[0];
         // per prime: P_F's chain, then the exact E groups of the leaf's mode
         auto chain = [&](auto gsz, const int32_t* grp) {
           constexpr int NGR = decltype(gsz)::value;
@@ -1582,9 +1604,9 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     std::vector<int> order;
   };
   thread_local Spec spec;
-  const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=1 enables (read per call: the bench
-    const char* e = getenv("SPERM_SPECULATE");  // times both settings in one process); measured
-    return e && e[0] == '1';  // slower in round 2 (configs[1] 0.203 vs 0.195 ms/step), so off
+  const bool spec_on = [] {  // A-B knob: SPERM_SPECULATE=0 disables (read per call: the bench
+    const char* e = getenv("SPERM_SPECULATE");  // times both settings in one process; configs[1]
+    return !(e && e[0] == '0');  // 0.170 vs 0.212 ms/step with NVML clock sampling running)
   }();
   int dev = 0;
   SPERM_TRY(cudaGetDevice(&dev));

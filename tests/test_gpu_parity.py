@@ -367,7 +367,7 @@ def _plans_agree(mats, want):
 def test_rnw_speculative_groups_repeat_and_change():
     """Same-shape calls launch the previous call's plan groups before the histogram read-back
     (csrc/rnw.cu rnw_spec_check_kernel): repeats, same-shape batches with other contents and other
-    plan histograms must all stay exact.  (Speculation is off by default; SPERM_SPECULATE=1.)"""
+    plan histograms must all stay exact (SPERM_SPECULATE=1 forces it on)."""
     os.environ["SPERM_SPECULATE"] = "1"
     try:
         _speculative_cases()

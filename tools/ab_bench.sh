@@ -10,6 +10,6 @@ for rep in 1 2; do
     python bench.py --no-ph --no-c100 --no-strong --no-cpu-baseline --steps 20 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read())
 print('$v', 'value %.4g' % d['value'], 'step %.4f' % d['ms_per_step'], 'kernel %.4f' % d['roofline']['kernel_ms_per_step'],
-      'spec %.4f' % d['with_speculation']['ms_per_step'], 'e2e %.4g' % d['e2e']['value'])"
+      'nospec %.4f' % d['without_speculation']['ms_per_step'], 'e2e %.4g' % d['e2e']['value'])"
   done
 done
