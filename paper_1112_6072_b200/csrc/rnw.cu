@@ -641,6 +641,9 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
   constexpr int NRT = NS + NFIX;   // row sums held in registers
   constexpr int S4 = (NRT + 3) / 4 * 4;
   constexpr int NGF = NFIX / GF;   // exact fixed-row groups
+  // block-loop unroll: kBlockUnroll where registers allow (2-CTA builds with <= 28 register rows,
+  // B <= 7; the others spill when unrolled)
+  constexpr int UNR = (tree_min_blocks(B, NFIX, GF) == 2 && NRT <= 28 && B <= 7) ? kBlockUnroll : 1;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   const TreeSmem L = tree_smem(NRT, NS, n, B);
@@ -736,7 +739,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     int32_t E[B], FG[NGF];
     auto blocks = [&](auto kc) {
       constexpr int K = decltype(kc)::value;
-#pragma unroll kBlockUnroll
+#pragma unroll UNR
       for (uint32_t ob = 0; ob < nblk; ++ob) {
         uint32_t mk = 0xffffffffu;
         if (ob) {  // flip high Gray bit B + hh (warp-uniform column): only the touched row groups
