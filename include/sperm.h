@@ -207,6 +207,18 @@ int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32
                  int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
                  int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
 
+/* sperm_expand_unordered — sperm_expand with the children of the level in an UNSPECIFIED order
+ * (each tile of nodes takes its output range with one atomic add instead of the order-preserving
+ * look-back scan).  Every child, coefficient and job id is the same; only their positions differ
+ * from run to run.  For the H_per recursion below the job level, where a job's
+ * value is the sum over its leaves and their order does not matter; the PH job list itself
+ * (Step 2) uses the ordered sperm_expand.  Same arguments, outputs and errors as sperm_expand. */
+int sperm_expand_unordered(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job,
+                           int n, int64_t count,
+                           int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job, int64_t cap_out,
+                           int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
+                           int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
+
 /* sperm_nnz — number of nonzero entries of each node (device, asynchronous): d_out[m] =
  * |{(i, j) : a_ij != 0}| of matrix m of d_mats [count][n][n].  The "size" scheduling key the
  * load-balance comparison orders jobs by (the paper's alternatives to the estimate order:

@@ -345,7 +345,11 @@ __device__ __forceinline__ unsigned long long st_pack(unsigned long long flag, l
 // preceding tiles by a decoupled look-back, and every warp then writes its children (and
 // early node) in natural order.  The node is read from HBM once.  err bits: 1 overflow of a
 // merged entry or coefficient, 2 output capacity exceeded or output buffer missing.
-template <int US>
+//
+// ORDERED = false (the H_per recursion below the job level, where only each job's SUM matters,
+// not the order of its leaves): the tile's output offsets come from one atomicAdd on the level
+// totals instead of the look-back — no waiting on the preceding tiles.
+template <int US, bool ORDERED>
 __global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, const int32_t* __restrict__ job,
     int n, int64_t count, int stage_words,
@@ -401,7 +405,13 @@ __global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
       ae += s_early[i];
     }
     long long ek = 0, ee = 0;  // exclusive prefix of this tile
-    if (tile == 0) {
+    if (!ORDERED) {
+      if (lane == 0) {
+        unsigned long long* tu = reinterpret_cast<unsigned long long*>(totals);
+        ek = ak ? (long long)atomicAdd(tu, (unsigned long long)ak) : 0;
+        ee = ae ? (long long)atomicAdd(tu + 1, (unsigned long long)ae) : 0;
+      }
+    } else if (tile == 0) {
       if (lane == 0) atomicExch(tile_status, st_pack(kStFlagPre, ak, ae));
     } else {
       if (lane == 0) atomicExch(tile_status + tile, st_pack(kStFlagAgg, ak, ae));
@@ -433,7 +443,7 @@ __global__ void __launch_bounds__(kExpThreads, 5) expand_level_kernel(
     if (lane == 0) {
       s_base[0] = ek;
       s_base[1] = ee;
-      if ((tile + 1) * wpb >= count) {  // the last tile: level totals
+      if (ORDERED && (tile + 1) * wpb >= count) {  // the last tile: level totals
         totals[0] = ek + ak;
         totals[1] = ee + ae;
       }
@@ -511,10 +521,10 @@ extern "C" int sperm_nnz(const int32_t* d_mats, int n, int64_t count, int64_t* d
 static std::mutex g_exp_mu;
 static double g_exp_bytes = 0.0, g_exp_nodes = 0.0;
 
-extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job, int n,
-                            int64_t count, int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job,
-                            int64_t cap_out, int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
-                            int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream) {
+static int expand_level(bool ordered, const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job,
+                        int n, int64_t count, int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job,
+                        int64_t cap_out, int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
+                        int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   keep_pool_memory();
   if (!h_out_count || !h_early_count) return set_error(SPERM_ERR_ARG, "sperm_expand: NULL count outputs");
@@ -538,15 +548,19 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
   unsigned* ticket = reinterpret_cast<unsigned*>(ws + tiles + 2);
   int* err = reinterpret_cast<int*>(ticket + 1);
   const int per_lane = (n * n + 31) / 32;
-  auto kern = per_lane <= 4 ? expand_level_kernel<4> : per_lane <= 8 ? expand_level_kernel<8>
-            : per_lane <= 12 ? expand_level_kernel<12> : expand_level_kernel<16>;
+  auto kern = ordered ? (per_lane <= 4 ? expand_level_kernel<4, true> : per_lane <= 8 ? expand_level_kernel<8, true>
+                         : per_lane <= 12 ? expand_level_kernel<12, true> : expand_level_kernel<16, true>)
+                      : (per_lane <= 4 ? expand_level_kernel<4, false> : per_lane <= 8 ? expand_level_kernel<8, false>
+                         : per_lane <= 12 ? expand_level_kernel<12, false> : expand_level_kernel<16, false>);
   {  // the attribute once per device and kernel, at the 200 KB staging budget (host time per level)
     static std::atomic<unsigned> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned bit = 1u << (dev & 31);
     if (!(attr_done.load() & bit)) {
-      for (auto k : {expand_level_kernel<4>, expand_level_kernel<8>, expand_level_kernel<12>, expand_level_kernel<16>})
+      for (auto k : {expand_level_kernel<4, true>, expand_level_kernel<8, true>, expand_level_kernel<12, true>,
+                     expand_level_kernel<16, true>, expand_level_kernel<4, false>, expand_level_kernel<8, false>,
+                     expand_level_kernel<12, false>, expand_level_kernel<16, false>})
         SPERM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_done.fetch_or(bit);
     }
@@ -585,6 +599,23 @@ extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, 
     g_exp_nodes += (double)count;
   }
   return SPERM_OK;
+}
+
+extern "C" int sperm_expand(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job, int n,
+                            int64_t count, int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job,
+                            int64_t cap_out, int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
+                            int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream) {
+  return expand_level(true, d_in_mats, d_in_coef, d_in_job, n, count, d_out_mats, d_out_coef, d_out_job, cap_out,
+                      d_early_mats, d_early_coef, d_early_job, cap_early, h_out_count, h_early_count, stream);
+}
+
+extern "C" int sperm_expand_unordered(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job,
+                                      int n, int64_t count, int32_t* d_out_mats, int64_t* d_out_coef,
+                                      int32_t* d_out_job, int64_t cap_out, int32_t* d_early_mats,
+                                      int64_t* d_early_coef, int32_t* d_early_job, int64_t cap_early,
+                                      int64_t* h_out_count, int64_t* h_early_count, void* stream) {
+  return expand_level(false, d_in_mats, d_in_coef, d_in_job, n, count, d_out_mats, d_out_coef, d_out_job, cap_out,
+                      d_early_mats, d_early_coef, d_early_job, cap_early, h_out_count, h_early_count, stream);
 }
 
 extern "C" int sperm_expand_stats(double* h_bytes, double* h_nodes, int reset) {

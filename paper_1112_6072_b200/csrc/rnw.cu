@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
       __syncwarp();
       // what a flip of high column h touches (sparse leaves: a column has few rows): bit v < 16 =
       // row-sum group W[4v..4v+3], bit 16 + c = low column c's slot rows, bit 24 = a fixed row
-      for (int h = lane; h < L.nh; h += 32) {
+      for (int h = lane; h < ((kSparseW || kSparseE) ? L.nh : 0); h += 32) {
         uint32_t mk = 0;
         for (int r = 0; r < NRT; ++r)
           if (sm[L.pos + h * S4 + r] != 0) mk |= (1u << (r >> 2)) | (r < NS ? 1u << (16 + r / KS) : 1u << 24);

@@ -128,6 +128,12 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
     return _cat([level] + early)
 
 
+# Below the job level only each job's sum matters, so the recursion's levels are expanded
+# without the order-preserving scan (sperm_expand_unordered); SPERM_EXPAND_ORDERED=1 keeps it (A-B).
+import os as _os
+_LEAF_ORDERED = _os.environ.get("SPERM_EXPAND_ORDERED", "0") == "1"
+
+
 def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None):
     """The same H_per recursion as expand_to_leaves, streamed: a level whose children could
     exceed `budget_bytes` of HBM is split into chunks that are expanded to their leaves one
@@ -176,7 +182,7 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None)
         if stats is not None:
             import time
             t0 = time.perf_counter()
-        (km, kc, kj), (em, ec, ej) = S.sperm_expand(level.mats, level.coef, level.job)
+        (km, kc, kj), (em, ec, ej) = S.sperm_expand(level.mats, level.coef, level.job, ordered=_LEAF_ORDERED)
         if stats is not None:
             stats["expand_calls"] = stats.get("expand_calls", 0) + 1
             stats["expand_host_s"] = stats.get("expand_host_s", 0.0) + time.perf_counter() - t0

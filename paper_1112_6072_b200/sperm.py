@@ -51,6 +51,7 @@ _SIGS = {
     "sperm_reduce_mod": (_I, [_P, _I64, _P, _P]),
     "sperm_fold_mod": (_I, [_P, _I64, _P]),
     "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
+    "sperm_expand_unordered": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "sperm_expand_stats": (_I, [_P, _P, _I]),
     "sperm_nnz": (_I, [_P, _I, _I64, _P, _P]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
@@ -286,9 +287,10 @@ def residues_to_ints(res, k) -> List[int]:
 
 
 # --------------------------------------------------------------------- expansion
-def sperm_expand(mats, coef=None, job=None, stream=None):
+def sperm_expand(mats, coef=None, job=None, stream=None, ordered: bool = True):
     """One BFS level of Algorithm PH Step 2.  Returns ((mats, coef, job) of the
-    children of order n-1, (mats, coef, job) of the unsplit s >= 5 nodes)."""
+    children of order n-1, (mats, coef, job) of the unsplit s >= 5 nodes).
+    ordered=False: sperm_expand_unordered (children in an unspecified order)."""
     import torch
     mats = _dev(mats, torch.int32)
     count, n = int(mats.shape[0]), int(mats.shape[1])
@@ -297,12 +299,13 @@ def sperm_expand(mats, coef=None, job=None, stream=None):
     job = _dev(job, torch.int32)
     oc, ec = ctypes.c_int64(0), ctypes.c_int64(0)
     L = lib()
+    fn = L.sperm_expand if ordered else L.sperm_expand_unordered
     # children are at most 2 per node: allocate that once; s >= 5 (early) nodes are rare, so
     # their buffer is sized by a second call only when the first reports them
     cap = 2 * count
     out = (torch.empty((cap, n - 1, n - 1), dtype=torch.int32, device=dev),
            torch.empty((cap,), dtype=torch.int64, device=dev), torch.empty((cap,), dtype=torch.int32, device=dev))
-    rc = L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]),
+    rc = fn(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]),
                         cap, None, None, None, 0, ctypes.byref(oc), ctypes.byref(ec), _stream(stream))
     if rc not in (OK, ERR_CAPACITY):
         _check(rc)
@@ -310,7 +313,7 @@ def sperm_expand(mats, coef=None, job=None, stream=None):
     early = (torch.empty((ne, n, n), dtype=torch.int32, device=dev),
              torch.empty((ne,), dtype=torch.int64, device=dev), torch.empty((ne,), dtype=torch.int32, device=dev))
     if rc == ERR_CAPACITY:
-        _check(L.sperm_expand(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]),
+        _check(fn(_ptr(mats), _ptr(coef), _ptr(job), n, count, _ptr(out[0]), _ptr(out[1]),
                               _ptr(out[2]), cap, _ptr(early[0]), _ptr(early[1]), _ptr(early[2]), ne,
                               ctypes.byref(oc), ctypes.byref(ec), _stream(stream)))
     return (out[0][:no], out[1][:no], out[2][:no]), early
