@@ -219,6 +219,41 @@ int sperm_expand_unordered(const int32_t* d_in_mats, const int64_t* d_in_coef, c
                            int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
                            int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
 
+/* sperm_expand_subtree — Algorithm H_per's recursion (Step 1's pivot line and
+ * Eq. (2)'s split) applied DEPTH FIRST below the job level: every node of order
+ * n is expanded by the same splits as sperm_expand (pivot reading R2, zero-line children dropped
+ * per R4, s >= 5 nodes not split per R5) down to its leaves of order leaf_order, in one call — one
+ * warp per node walks the node's whole subtree in shared memory, so no intermediate level touches
+ * HBM.  The leaves are the same multiset (matrix, coefficient, job id) as repeated
+ * sperm_expand_unordered calls produce, in an UNSPECIFIED order: for the H_per recursion below
+ * the job level, where a job's value is the sum over its leaves.
+ *
+ *  d_in_mats/coef/job  [count] nodes of order n, 2 <= n <= 32 (device).  d_in_job may be NULL
+ *                      (node index = job id); d_in_coef may be NULL (coefficient 1).
+ *  leaf_order          L, 1 <= L < n: the leaves have order exactly L.
+ *  d_out_mats/coef/job [cap_out] leaves [L][L] (device).
+ *  d_early_*           [cap_early] the s >= 5 nodes met on the way, each padded to order n by an
+ *                      identity block: diag(X, I_{n-o}) for a node X of order o (same permanent),
+ *                      so all have order n (device; may be NULL when cap_early == 0).
+ *  h_out_count, h_early_count  host outputs: numbers written (or needed, see below).
+ * Synchronous w.r.t. the host (the counts are read back).  Errors: SPERM_ERR_ARG (sizes, NULL
+ * pointers, a stack too large for shared memory: sum_{m=L}^{n-1} m(m+1) + 2 n (n|1) words per
+ * warp must fit 56 KB); SPERM_ERR_RANGE (a merged entry or coefficient overflows);
+ * SPERM_ERR_CAPACITY: the leaves exceeded cap_out — the kernel stops taking new nodes, so the
+ * outputs are incomplete and *h_out_count is only a lower bound (re-run on fewer nodes) — or
+ * only the early nodes exceeded cap_early (the leaf outputs and both counts are then exact:
+ * re-run with cap_early = *h_early_count). */
+int sperm_expand_subtree(const int32_t* d_in_mats, const int64_t* d_in_coef, const int32_t* d_in_job,
+                         int n, int64_t count, int leaf_order,
+                         int32_t* d_out_mats, int64_t* d_out_coef, int32_t* d_out_job, int64_t cap_out,
+                         int32_t* d_early_mats, int64_t* d_early_coef, int32_t* d_early_job,
+                         int64_t cap_early, int64_t* h_out_count, int64_t* h_early_count, void* stream);
+
+/* Cumulative algorithmic traffic of the completed sperm_expand_subtree calls since the last reset
+ * (host): bytes = every root read once + every leaf / early node written once (matrix,
+ * coefficient, job id); roots = nodes taken.  reset != 0 clears the counters after reading. */
+int sperm_expand_subtree_stats(double* h_bytes, double* h_roots, int reset);
+
 /* sperm_nnz — number of nonzero entries of each node (device, asynchronous): d_out[m] =
  * |{(i, j) : a_ij != 0}| of matrix m of d_mats [count][n][n].  The "size" scheduling key the
  * load-balance comparison orders jobs by (the paper's alternatives to the estimate order:

@@ -130,15 +130,31 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
 
 # Below the job level only each job's sum matters, so the recursion's levels are expanded
 # without the order-preserving scan (sperm_expand_unordered); SPERM_EXPAND_ORDERED=1 keeps it (A-B).
+# Nodes of order <= L + SUBTREE_DEPTH (<= 32) are expanded depth first to their leaves in one
+# sperm_expand_subtree call (no intermediate level in HBM); SPERM_SUBTREE_DEPTH=0 turns it off.
 import os as _os
 _LEAF_ORDERED = _os.environ.get("SPERM_EXPAND_ORDERED", "0") == "1"
+SUBTREE_DEPTH = int(_os.environ.get("SPERM_SUBTREE_DEPTH", "12"))
 
 
-def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None):
+def subtree_root_order(L: int, depth: int = None) -> int:
+    """Order from which sperm_expand_subtree takes over (0: never): L + depth, at most 32, as
+    long as the warp's stack (one slot per order L..n0-1) fits its 56 KB of shared memory."""
+    depth = SUBTREE_DEPTH if depth is None else depth
+    if depth <= 0 or L < 1 or L >= 32:
+        return 0
+    n0 = min(32, L + depth)
+    while n0 > L and 4 * (2 * n0 * (n0 | 1) + sum(k * (k + 1) + 2 for k in range(L, n0))) > 56 * 1024:
+        n0 -= 1
+    return n0 if n0 > L else 0
+
+
+def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None, subtree_depth: int = None):
     """The same H_per recursion as expand_to_leaves, streamed: a level whose children could
     exceed `budget_bytes` of HBM is split into chunks that are expanded to their leaves one
     after another (depth first over chunks), so the live node sets stay bounded however many
-    leaves a job has.  Yields NodeSets of leaves (order <= L) and of s >= 5 nodes."""
+    leaves a job has.  Yields NodeSets of leaves (order <= L) and of s >= 5 nodes (those met
+    below the subtree order come padded to that order by an identity block, same permanent)."""
     # A level is expanded whole (breadth first: the largest, best-utilised launches) while its own
     # expansion fits the budget.  A level that does not is split into chunks sized so that a
     # chunk's whole subtree down to order L is projected to fit (growth per level = children /
@@ -146,12 +162,21 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None)
     # chunk normally reaches its leaves without nested splits, which would each keep their parent
     # level alive: the live memory stays ~ the chunked level + one chunk's two current levels.
     # Only the first chunk is cut at a time; the rest is re-split with the growth seen by then.
+    # Levels of order <= n0 = subtree_root_order(L) go to sperm_expand_subtree whole (chunked by
+    # the leaves per root seen so far, else the 2^(n0-L) worst case); a chunk whose leaves overflow
+    # its output is re-run in halves.
+    n0 = subtree_root_order(L, subtree_depth)
     seen: Dict[int, List[int]] = {}  # order -> [parents expanded, children produced]
+    seen_sub: List[int] = [0, 0]  # subtree roots taken, leaves produced
+    leaf_bytes = 4 * L * L + 12
 
     def g_at(m: int) -> float:
         if m in seen:
             return seen[m][1] / seen[m][0]
         return max(c / p for p, c in seen.values()) if seen else 2.0
+
+    def leaves_per_root() -> float:
+        return seen_sub[1] / seen_sub[0] if seen_sub[0] else float(2 ** (n0 - L))
 
     stack = [jobs]
     while stack:
@@ -161,6 +186,39 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None)
         if level.n <= L or level.n < 2:
             yield level
             continue
+        if n0 and level.n <= n0:
+            # depth first below order n0: one call per chunk of roots
+            lpr = leaves_per_root()
+            cap_roots = max(1, int(budget_bytes // (leaf_bytes * 1.25 * max(lpr, 1.0))))
+            if level.count > cap_roots:
+                stack.append(NodeSet(level.n, level.mats[cap_roots:], level.coef[cap_roots:], level.job[cap_roots:]))
+                stack.append(NodeSet(level.n, level.mats[:cap_roots], level.coef[:cap_roots], level.job[:cap_roots]))
+                continue
+            cap = max(1, min(int(budget_bytes // leaf_bytes), int(1.25 * lpr * level.count) + 1024))
+            if stats is not None:
+                import time
+                t0 = time.perf_counter()
+            r = S.sperm_expand_subtree(level.mats, L, cap, level.coef, level.job)
+            if stats is not None:
+                stats["subtree_calls"] = stats.get("subtree_calls", 0) + 1
+                stats["expand_host_s"] = stats.get("expand_host_s", 0.0) + time.perf_counter() - t0
+            if r is None:  # more leaves than projected: halves
+                if stats is not None:
+                    stats["subtree_retries"] = stats.get("subtree_retries", 0) + 1
+                if level.count == 1:
+                    raise S.SpermError(S.ERR_CAPACITY, "one node's leaves exceed the leaf budget")
+                h = level.count // 2
+                stack.append(NodeSet(level.n, level.mats[h:], level.coef[h:], level.job[h:]))
+                stack.append(NodeSet(level.n, level.mats[:h], level.coef[:h], level.job[:h]))
+                continue
+            (lm, lc, lj), (em, ec, ej) = r
+            seen_sub[0] += level.count
+            seen_sub[1] += lm.shape[0]
+            if em.shape[0]:
+                yield NodeSet(level.n, em, ec, ej)
+            if lm.shape[0]:
+                yield NodeSet(L, lm, lc, lj)
+            continue
         # bytes per node of one level of order m: its parents (4 m^2 each) and sperm_expand's
         # output slots (2 children of order m-1 and 1 early node of order m per parent)
         per_level = lambda m: 8 * m * m + 8 * (m - 1) ** 2  # noqa: E731
@@ -168,6 +226,9 @@ def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None)
         if level.count > cap:
             peak, mult = 0.0, 1.0
             for m in range(level.n, L, -1):
+                if n0 and m <= n0:  # the subtree call: its roots and its leaves
+                    peak = max(peak, mult * (4 * m * m + 1.25 * leaves_per_root() * leaf_bytes))
+                    break
                 peak = max(peak, mult * per_level(m))
                 mult *= g_at(m)
                 if mult * 8 * L * L > budget_bytes:  # one node's subtree alone exceeds the budget

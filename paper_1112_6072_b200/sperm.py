@@ -53,6 +53,8 @@ _SIGS = {
     "sperm_expand": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "sperm_expand_unordered": (_I, [_P, _P, _P, _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "sperm_expand_stats": (_I, [_P, _P, _I]),
+    "sperm_expand_subtree": (_I, [_P, _P, _P, _I, _I64, _I, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P]),
+    "sperm_expand_subtree_stats": (_I, [_P, _P, _I]),
     "sperm_nnz": (_I, [_P, _I, _I64, _P, _P]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
@@ -317,6 +319,46 @@ def sperm_expand(mats, coef=None, job=None, stream=None, ordered: bool = True):
                               _ptr(out[2]), cap, _ptr(early[0]), _ptr(early[1]), _ptr(early[2]), ne,
                               ctypes.byref(oc), ctypes.byref(ec), _stream(stream)))
     return (out[0][:no], out[1][:no], out[2][:no]), early
+
+
+def sperm_expand_subtree(mats, leaf_order: int, cap: int, coef=None, job=None, stream=None):
+    """H_per's recursion below the job level, depth first (sperm_expand_subtree): every node of
+    mats [count, n, n] (n <= 32) expanded to its leaves of order `leaf_order` in one call.
+    Returns ((mats, coef, job) of the leaves [*, L, L], (mats, coef, job) of the s >= 5 nodes
+    met on the way, padded to order n), or None if more than `cap` leaves were produced (the
+    caller re-runs on fewer nodes)."""
+    import torch
+    mats = _dev(mats, torch.int32)
+    count, n = int(mats.shape[0]), int(mats.shape[1])
+    dev = mats.device
+    coef = _dev(coef, torch.int64)
+    job = _dev(job, torch.int32)
+    L = int(leaf_order)
+    oc, ec = ctypes.c_int64(0), ctypes.c_int64(0)
+    out = (torch.empty((cap, L, L), dtype=torch.int32, device=dev),
+           torch.empty((cap,), dtype=torch.int64, device=dev), torch.empty((cap,), dtype=torch.int32, device=dev))
+    fn = lib().sperm_expand_subtree
+    args = (_ptr(mats), _ptr(coef), _ptr(job), n, count, L, _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), cap)
+    rc = fn(*args, None, None, None, 0, ctypes.byref(oc), ctypes.byref(ec), _stream(stream))
+    if rc == ERR_CAPACITY and oc.value > cap:
+        return None
+    if rc not in (OK, ERR_CAPACITY):
+        _check(rc)
+    ne = ec.value
+    early = (torch.empty((ne, n, n), dtype=torch.int32, device=dev),
+             torch.empty((ne,), dtype=torch.int64, device=dev), torch.empty((ne,), dtype=torch.int32, device=dev))
+    if rc == ERR_CAPACITY:  # only the early nodes did not fit: the counts are exact
+        _check(fn(*args, _ptr(early[0]), _ptr(early[1]), _ptr(early[2]), ne, ctypes.byref(oc), ctypes.byref(ec),
+                  _stream(stream)))
+    no = oc.value
+    return (out[0][:no], out[1][:no], out[2][:no]), early
+
+
+def sperm_expand_subtree_stats(reset: bool = False):
+    """(algorithmic bytes, roots) of the sperm_expand_subtree calls since the last reset."""
+    b, nn = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().sperm_expand_subtree_stats(ctypes.byref(b), ctypes.byref(nn), 1 if reset else 0))
+    return b.value, nn.value
 
 
 def sperm_expand_stats(reset: bool = False):

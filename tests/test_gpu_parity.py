@@ -195,6 +195,92 @@ def test_expand_conserves_permanent():
     assert tot == golden("C60_truncated_icosahedron")
 
 
+def _leaf_multiset(mats, coef, job):
+    m = mats.cpu().numpy()
+    c = coef.cpu().numpy()
+    j = job.cpu().numpy()
+    return sorted((int(j[i]), int(c[i]), m[i].tobytes()) for i in range(m.shape[0]))
+
+
+def _oracle_leaf_multiset(roots, L, pad_to):
+    """oracle.expand_to_leaves of every root (dense numpy [count, n, n], coefs, job ids): the
+    order-L leaves, and the s >= 5 nodes padded to order pad_to by an identity block."""
+    leaves, early = [], []
+    for a, c, j in roots:
+        rows, n = to_rows(a)
+        for cf, m, k in expand_to_leaves((int(c), rows, n), L):
+            d = np.array(to_dense(m, k), dtype=np.int32)
+            if k == L:
+                leaves.append((int(j), int(cf), d.tobytes()))
+            else:
+                e = np.eye(pad_to, dtype=np.int32)
+                e[:k, :k] = d
+                early.append((int(j), int(cf), e.tobytes()))
+    return sorted(leaves), sorted(early)
+
+
+@pytest.mark.parametrize("L", [14, 20, 24])
+def test_subtree_leaves_equal_oracle_c60(L):
+    """sperm_expand_subtree (depth first, in shared memory): the leaves of C60 nodes of order
+    L + 4..8 are the same multiset (job, coefficient, every entry) as the oracle's H_per
+    recursion (expand_to_leaves) produces from the same nodes."""
+    a = truncated_icosahedron()
+    n0 = min(32, L + (8 if L < 20 else 4))
+    s = pipeline.expand_to_leaves(pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=64)[0], n0)[0]
+    assert s.n == n0
+    take = min(s.count, 120 if L < 20 else 40)
+    roots = [(s.mats[i].cpu().numpy(), int(s.coef[i]), int(s.job[i])) for i in range(take)]
+    r = P.sperm_expand_subtree(s.mats[:take], L, 1 << 20, s.coef[:take], s.job[:take])
+    (lm, lc, lj), (em, ec, ej) = r
+    want_leaves, want_early = _oracle_leaf_multiset(roots, L, n0)
+    assert _leaf_multiset(lm, lc, lj) == want_leaves
+    assert _leaf_multiset(em, ec, ej) == want_early == []
+
+
+def test_subtree_random_signed_with_early_nodes():
+    """Signed random matrices of order 12-16 (row and column pivots, s = 1..4 merges and minors,
+    zero-line children, s >= 5 nodes): leaves and identity-padded early nodes equal the
+    oracle's; a too small leaf capacity reports None (re-run on fewer nodes)."""
+    rng = np.random.default_rng(91)
+    for t in range(12):
+        n = int(rng.integers(12, 17))
+        dens = float(rng.uniform(0.15, 0.45))
+        cnt = 6
+        mats = (rng.integers(-3, 5, size=(cnt, n, n)) * (rng.random((cnt, n, n)) < dens)).astype(np.int32)
+        mats += np.eye(n, dtype=np.int32)[None] * rng.integers(1, 3, size=(cnt, 1, 1)).astype(np.int32)
+        coef = rng.integers(-5, 6, size=cnt)
+        L = int(rng.integers(max(2, n - 8), n))
+        job = np.arange(cnt, dtype=np.int32) * 3 + 1
+        r = P.sperm_expand_subtree(dev(mats), L, 1 << 16, dev(coef, torch.int64), dev(job))
+        (lm, lc, lj), (em, ec, ej) = r
+        want_leaves, want_early = _oracle_leaf_multiset(list(zip(mats, coef, job)), L, n)
+        assert _leaf_multiset(lm, lc, lj) == want_leaves, t
+        assert _leaf_multiset(em, ec, ej) == want_early, t
+        if len(want_leaves) > 1:
+            assert P.sperm_expand_subtree(dev(mats), L, len(want_leaves) - 1, dev(coef, torch.int64), dev(job)) is None
+
+
+def test_subtree_argument_errors():
+    """n > 32, L >= n and NULL outputs are SPERM_ERR_ARG; an empty batch returns nothing."""
+    import ctypes
+    L = P.sperm.lib()
+    oc, ec = ctypes.c_int64(0), ctypes.c_int64(0)
+    m = torch.zeros((2, 33, 33), dtype=torch.int32, device="cuda")
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    assert L.sperm_expand_subtree(ptr(m), None, None, 33, 2, 20, None, None, None, 0, None, None, None, 0,
+                                  ctypes.byref(oc), ctypes.byref(ec), None) == P.sperm.ERR_ARG
+    m = torch.eye(20, dtype=torch.int32, device="cuda")[None].repeat(2, 1, 1)
+    assert L.sperm_expand_subtree(ptr(m), None, None, 20, 2, 20, None, None, None, 0, None, None, None, 0,
+                                  ctypes.byref(oc), ctypes.byref(ec), None) == P.sperm.ERR_ARG
+    assert L.sperm_expand_subtree(ptr(m), None, None, 20, 2, 10, None, None, None, 8, None, None, None, 0,
+                                  ctypes.byref(oc), ctypes.byref(ec), None) == P.sperm.ERR_ARG
+    (lm, _, _), (em, _, _) = P.sperm_expand_subtree(m[:0], 10, 4)
+    assert lm.shape == (0, 10, 10) and em.shape[0] == 0
+    # identity: every node is s = 1 down to the leaf, one leaf per root, coefficient 1
+    (lm, lc, lj), _ = P.sperm_expand_subtree(m, 10, 4)
+    assert lm.shape[0] == 2 and (lm.cpu() == torch.eye(10, dtype=torch.int32)).all() and lc.tolist() == [1, 1]
+
+
 # ------------------------------------------------------------------ KKLLL
 def test_kklll_bit_exact_trials():
     rng = np.random.default_rng(5)
