@@ -4,26 +4,38 @@
 // Below the job level a job's value is the sum over its leaves, so the order in which its leaves
 // appear does not matter (the job list itself, PH Step 2, keeps the ordered level kernel of
 // expand.cu).  The level-by-level expansion writes every intermediate node to HBM and reads it
-// back one level later; here one warp takes a root node (order n0 <= 32) and walks its whole
-// subtree down to the leaves of order L in shared memory:
+// back one level later, and builds every child densely (O(n^2) per child).  Here one warp takes a
+// root node (order n0 <= 32) and walks its whole subtree down to the leaves of order L with O(n)
+// work per node:
 //
-//   * the current node lives in a shared-memory buffer (row stride n0 | 1: lane-per-row and
-//     lane-per-column reads are both bank-conflict free); lane i keeps the nonzero counts of row
-//     i and column i in registers, and a child's counts are derived from the parent's in O(n)
-//     (the lines a split touches), so no node is ever rescanned;
+//   * the root is staged once in shared memory (M, row stride n0 | 1: lane-per-row and
+//     lane-per-column accesses are both bank-conflict free) and every node of its subtree is a
+//     VIEW of M: lane i holds the node's row map R[i] and column map C[i] (entry (i, j) of the
+//     node = M[R[i]][C[j]]) and the nonzero counts of its row i and column i;
+//   * a child deletes one row and one column (two shuffles of the maps) and, for Eq. (2)'s merge,
+//     overwrites one line of M in place (line ka := al * line kb + be * line ka: one load pair
+//     and store per lane); its line counts are derived from the parent's in O(n), so no node is
+//     ever rescanned or copied;
 //   * the pivot (reading R2: fewest nonzeros, rows before columns, lowest index) is two warp
 //     min-reductions over the lanes' packed (count, index) keys; the pivot line's nonzeros come
 //     from one ballot;
-//   * a split with two surviving children (s = 3, 4) pushes the second child to the warp's stack
-//     — one slot per order, since the pending siblings of a depth-first walk have distinct
-//     orders — and continues with the first; s = 1, 2 continue in place (double buffer);
-//   * a node of order <= L is a leaf: written densely to HBM (one atomic slot per leaf); a node
-//     with s >= 5 (reading R5: not split) is written to the early outputs padded to order n0 by
-//     an identity block (per(diag(X, I)) = per(X)), so every early node has the same order.
+//   * a split with two surviving children (s = 3, 4) continues with the first and pushes a frame
+//     (the parent's maps, the second child's split and counts) to the warp's stack; every in-place
+//     merge made while a frame is pending logs the line it overwrites, and popping a frame replays
+//     the log back to the frame's mark (M is the parent's again) before applying the second
+//     child's split.  Frames and the log (<= n0 - L entries each) live in a per-warp scratch area
+//     in global memory (L2-resident), so shared memory holds only M and many warps fit per SM;
+//   * a node of order <= L is a leaf: gathered through its maps and written densely to HBM (one
+//     atomic slot per leaf); a node with s >= 5 (reading R5: not split) is written to the early
+//     outputs padded to order n0 by an identity block (per(diag(X, I)) = per(X)).
 //
 // The same children as expand.cu's kernel (same Eq. (2) scalars, the same zero-line test of
 // reading R4, the same overflow checks): the leaves form the same multiset as the level-by-level
 // recursion's, in an unspecified order.
+//
+// History (C100, L = 15): dense children with the stack in shared memory 5.18 s of
+// expansion; stack in global scratch 3.72 s (occupancy was the limit, not the leaf atomic); ncu
+// then showed the dense child copies at ~45 % of the instructions (4300 per leaf) -> this view form.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -36,94 +48,47 @@ namespace sperm {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kSubWarps = 4;  // warps per CTA (shared-memory bound: one stack per warp)
+constexpr int kSubWarps = 4;  // warps per CTA
+// per-warp scratch (words): frames [depth + 1][kFrameW] | undo log [depth + 1][kUndoW]
+constexpr int kFrameW = 112;  // header (12 words) | parent row map [32] | parent column map [32] | child counts [32]
+constexpr int kUndoW = 34;    // line (1 word: column index, or row index | 0x100) | the line's 32 values | pad
 
-// words of the stack slots of orders L .. m-1 (slot(m) = coef (2 words) | m packed line counts |
-// m x m entries, stride m): sum_{k=L}^{m-1} (k(k+1) + 2), every slot an even number of words
-__host__ __device__ __forceinline__ int slot_prefix(int L, int m) {
-  auto F = [](int x) { return x * (x + 1) * (x + 2) / 3; };  // sum_{k=1}^{x} k(k+1)
-  return (F(m - 1) - F(L - 1)) + 2 * (m - L);
-}
-__host__ __device__ __forceinline__ int sub_warp_words(int n0, int L) {
-  const int S = n0 | 1;
-  return ((2 * n0 * S + slot_prefix(L, n0)) + 3) / 4 * 4;
-}
-
-// dst[ii * dstride + jj] = child entry (ii, jj) of the node in src (stride S), for a child that
-// deletes row dr and column dc and merges (merge 1: column keep := al*col(dc) + be*col(keep);
-// merge 2: row keep := al*row(dr) + be*row(keep); 0: none).  m = child order.  Merged entries
-// are computed mod 2^32 (exact: the split already rejected overflowing ones).
-__device__ __forceinline__ void build_child(const int32_t* __restrict__ src, int S, int m, int dr, int dc, int merge,
-                                            int keep, int32_t al, int32_t be, int32_t* __restrict__ dst,
-                                            int dstride, int lane) {
-  const int mm = m * m;
-  const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)m) + 1u;  // e / m exactly for e < 2^16
-  constexpr int UB = 4;
-  for (int base = 0; base < mm; base += 32 * UB) {
-    int32_t r[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int e = base + u * 32 + lane;
-      int32_t v = 0;
-      if (e < mm) {
-        const int ii = (int)__umulhi((uint32_t)e, magic), jj = e - ii * m;
-        const int i = ii + (ii >= dr), j = jj + (jj >= dc);
-        v = src[i * S + j];
-        if (merge == 1 && j == keep)
-          v = (int32_t)((uint32_t)al * (uint32_t)src[i * S + dc] + (uint32_t)be * (uint32_t)v);
-        else if (merge == 2 && i == keep)
-          v = (int32_t)((uint32_t)al * (uint32_t)src[dr * S + j] + (uint32_t)be * (uint32_t)v);
-      }
-      r[u] = v;
-    }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int e = base + u * 32 + lane;
-      if (e < mm) {
-        const int ii = (int)__umulhi((uint32_t)e, magic);
-        dst[ii * dstride + (e - ii * m)] = r[u];
-      }
-    }
-  }
-}
-
-// A candidate child in the pivot's frame (the frame is A for a row pivot, A^T for a column
-// pivot: frame row r = the pivot line).  Minor: delete frame row r and frame column p, coef *= v.
+// A child in the pivot's frame (the frame is A for a row pivot, A^T for a column pivot: frame row
+// r = the pivot line).  Minor: delete frame row r and frame column kb, coef *= the pivot entry.
 // Merge: delete frame row r and frame column kb, frame column ka := al*col(kb) + be*col(ka).
 struct FKid {
   int minor;  // 1 minor, 0 merge
-  int ka, kb;  // merge columns (minor: kb = p)
+  int ka, kb;
   int32_t al, be;
 };
 
-// GSTACK: the stack slots live in a per-warp global scratch area (L2-resident) instead of shared
-// memory, so shared memory holds only the two working buffers and more warps fit per SM.
-// NOATOMIC (timing experiment only, wrong output): leaves go to a per-warp slot, no atomic.
-template <bool GSTACK, bool NOATOMIC>
+// frame entry (physical row fr, physical column fc) of the view: M[fr][fc] for a row pivot,
+// M[fc][fr] for a column pivot (frame rows are the node's columns)
+__device__ __forceinline__ int32_t fat(const int32_t* M, int S, bool colpiv, int fr, int fc) {
+  return colpiv ? M[fc * S + fr] : M[fr * S + fc];
+}
+
 __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, const int32_t* __restrict__ job, int n0,
-    int64_t count, int L, int warp_words, int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef,
+    int64_t count, int L, int32_t* __restrict__ out_mats, int64_t* __restrict__ out_coef,
     int32_t* __restrict__ out_job, int64_t cap_out, int32_t* __restrict__ early_mats,
     int64_t* __restrict__ early_coef, int32_t* __restrict__ early_job, int64_t cap_early,
-    unsigned long long* __restrict__ ws, int* __restrict__ err, int32_t* __restrict__ gstack, int stack_words) {
+    unsigned long long* __restrict__ ws, int* __restrict__ err, int32_t* __restrict__ scratch, int scratch_words) {
   extern __shared__ int32_t ssm[];
   const int lane = threadIdx.x & 31;
-  int32_t* base = ssm + (threadIdx.x >> 5) * warp_words;
   const int S = n0 | 1;
-  int32_t* const Wb0 = base;
-  int32_t* const Wb1 = base + n0 * S;
-  int32_t* const stk = GSTACK ? gstack + ((int64_t)blockIdx.x * kSubWarps + (threadIdx.x >> 5)) * stack_words
-                              : base + 2 * n0 * S;
-  const int64_t L2 = (int64_t)L * L;
+  int32_t* const M = ssm + (threadIdx.x >> 5) * (((n0 * S) + 3) / 4 * 4);
+  int32_t* const frames = scratch + ((int64_t)blockIdx.x * kSubWarps + (threadIdx.x >> 5)) * scratch_words;
+  int32_t* const ulog = frames + (n0 - L + 1) * kFrameW;
   const uint32_t magic0 = (uint32_t)(0xffffffffull / (uint32_t)n0) + 1u;
+  const uint32_t magicL = (uint32_t)(0xffffffffull / (uint32_t)L) + 1u;
   while (true) {
     unsigned long long root = 0;
     if (lane == 0) root = (*(volatile int*)err & 2) ? ~0ull : atomicAdd(ws, 1ull);  // stop on a full output
     root = __shfl_sync(kFull, root, 0);
     if (root >= (unsigned long long)count) break;
     // ---- the root: staged (all of a batch's loads before its stores) and its line counts
-    int cur = 0;
-    int32_t* W = Wb0;
+    __syncwarp();
     {
       const int32_t* g = mats + (int64_t)root * n0 * n0;
       const int nn = n0 * n0;
@@ -139,7 +104,7 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
         for (int u = 0; u < UR; ++u) {
           const int e = b + u * 32 + lane;
           const int i = (int)__umulhi((uint32_t)e, magic0);
-          if (e < nn) W[i * S + (e - i * n0)] = r[u];
+          if (e < nn) M[i * S + (e - i * n0)] = r[u];
         }
       }
     }
@@ -147,31 +112,55 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
     int n = n0;
     int64_t cf = coef ? coef[root] : 1;
     const int32_t jb = job ? job[root] : (int32_t)root;
-    int rc = 0, cc = 0;  // lane i: nonzeros of row i and of column i of the current node
+    int rid = lane, cid = lane;  // the view's row / column maps (lane i: R[i], C[i])
+    int rc = 0, cc = 0;           // lane i: nonzeros of row i and of column i of the view
     if (lane < n)
       for (int j = 0; j < n; ++j) {
-        rc += W[lane * S + j] != 0;
-        cc += W[j * S + lane] != 0;
+        rc += M[lane * S + j] != 0;
+        cc += M[j * S + lane] != 0;
       }
-    uint32_t pending = 0;  // bit m: a node of order m waits in stack slot m
+    int nfr = 0, nlog = 0;  // pending frames, undo-log entries
+    // applies a child's split to the view (maps, and for a merge the line of M, logged while a
+    // frame is pending); frame maps: FR = colpiv ? C : R, FC = colpiv ? R : C
+    auto apply = [&](bool colpiv, int r, const FKid& k) {
+      const int FR = colpiv ? cid : rid, FC = colpiv ? rid : cid;
+      if (!k.minor) {
+        const int pk = __shfl_sync(kFull, FC, k.ka), pb = __shfl_sync(kFull, FC, k.kb);
+        if (nfr > 0) {  // log the whole physical line pk (n0 values) before overwriting it
+          int32_t* u = ulog + nlog * kUndoW;
+          if (lane < n0) u[1 + lane] = fat(M, S, colpiv, lane, pk);
+          if (lane == 0) u[0] = colpiv ? (pk | 0x100) : pk;
+          ++nlog;
+          __syncwarp();  // every lane has read its logged entry before the line is overwritten
+        }
+        if (lane < n) {
+          const int32_t x = fat(M, S, colpiv, FR, pk), y = fat(M, S, colpiv, FR, pb);
+          const int32_t v = (int32_t)((uint32_t)k.al * (uint32_t)y + (uint32_t)k.be * (uint32_t)x);
+          if (colpiv) M[pk * S + FR] = v;
+          else M[FR * S + pk] = v;
+        }
+      }
+      // delete frame row r and frame column kb: lane ii takes the map entry ii + (ii >= r)
+      const int fr2 = __shfl_sync(kFull, FR, min(lane + (lane >= r), 31));
+      const int fc2 = __shfl_sync(kFull, FC, min(lane + (lane >= k.kb), 31));
+      rid = colpiv ? fc2 : fr2;
+      cid = colpiv ? fr2 : fc2;
+      __syncwarp();
+    };
     while (true) {
       bool pop = false;
       if (n <= L) {
-        // ---- leaf (order L): one output slot, dense row-major copy
+        // ---- leaf (order L): one output slot; gathered through the maps, row-major
         unsigned long long slot = 0;
-        if (NOATOMIC) {
-          slot = ((int64_t)blockIdx.x * kSubWarps + (threadIdx.x >> 5)) % (cap_out > 0 ? cap_out : 1);
-          if (lane == 0) atomicAdd(ws + 1, 0ull);
-        } else {
-          if (lane == 0) slot = atomicAdd(ws + 1, 1ull);
-          slot = __shfl_sync(kFull, slot, 0);
-        }
+        if (lane == 0) slot = atomicAdd(ws + 1, 1ull);
+        slot = __shfl_sync(kFull, slot, 0);
         if ((int64_t)slot < cap_out) {
-          int32_t* o = out_mats + (int64_t)slot * L2;
-          const uint32_t mg = (uint32_t)(0xffffffffull / (uint32_t)n) + 1u;
-          for (int e = lane; e < n * n; e += 32) {
-            const int i = (int)__umulhi((uint32_t)e, mg);
-            o[e] = W[i * S + (e - i * n)];
+          int32_t* o = out_mats + (int64_t)slot * L * L;
+          for (int b = 0; b < L * L; b += 32) {
+            const int e = b + lane;
+            const int i = (int)__umulhi((uint32_t)e, magicL), j = e - i * L;
+            const int pr = __shfl_sync(kFull, rid, i & 31), pc = __shfl_sync(kFull, cid, j & 31);
+            if (e < L * L) o[e] = M[pr * S + pc];
           }
           if (lane == 0) {
             out_coef[slot] = cf;
@@ -198,9 +187,11 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
           slot = __shfl_sync(kFull, slot, 0);
           if ((int64_t)slot < cap_early) {
             int32_t* o = early_mats + (int64_t)slot * n0 * n0;
-            for (int e = lane; e < n0 * n0; e += 32) {
+            for (int b = 0; b < n0 * n0; b += 32) {
+              const int e = b + lane;
               const int i = (int)__umulhi((uint32_t)e, magic0), j = e - i * n0;
-              o[e] = (i < n && j < n) ? W[i * S + j] : (i == j ? 1 : 0);
+              const int pr = __shfl_sync(kFull, rid, i & 31), pc = __shfl_sync(kFull, cid, j & 31);
+              if (e < n0 * n0) o[e] = (i < n && j < n) ? M[pr * S + pc] : (i == j ? 1 : 0);
             }
             if (lane == 0) {
               early_coef[slot] = cf;
@@ -209,12 +200,11 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
           }
           pop = true;
         } else {
-          // frame accessors: frame entry (i, j) = A(i, j) for a row pivot, A(j, i) for a column
-          // pivot; frame line counts likewise
-          auto at = [&](int i, int j) -> int32_t { return colpiv ? W[j * S + i] : W[i * S + j]; };
-          const int frc = colpiv ? cc : rc, fcc = colpiv ? rc : cc;
+          const int FR = colpiv ? cid : rid, FC = colpiv ? rid : cid;
+          const int frc = colpiv ? cc : rc, fcc = colpiv ? rc : cc;  // frame line counts
+          const int FRr = __shfl_sync(kFull, FR, r);                 // the pivot line, physical
           // the pivot line's nonzeros p0 < p1 < ... and their values (Eq. (2)'s a, b, c, d)
-          const int32_t pv = lane < n ? at(r, lane) : 0;
+          const int32_t pv = lane < n ? fat(M, S, colpiv, FRr, FC) : 0;
           unsigned pm = __ballot_sync(kFull, pv != 0);
           int p[4];
 #pragma unroll
@@ -229,9 +219,11 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
           int nk;
           if (s == 1) {
             kid[0] = {1, -1, p[0], 0, 0};
+            kid[1] = kid[0];
             nk = 1;
           } else {
             kid[0] = {0, p[0], p[1], v[0], v[1]};
+            kid[1] = kid[0];
             nk = 1;
             if (s == 3) {
               kid[1] = {1, -1, p[2], 0, 0};
@@ -250,11 +242,12 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
           for (int c = 0; c < 2; ++c) {
             if (c >= nk) break;
             const FKid k = kid[c];
+            const int pkb = __shfl_sync(kFull, FC, k.kb);
             int nrc = 1, ncc = 1;  // frame counts of row `lane` / column `lane` in the child
             bool mnz = false;
             if (k.minor) {
               if (lane < n) {
-                nrc = frc - (at(lane, k.kb) != 0);
+                nrc = frc - (fat(M, S, colpiv, FR, pkb) != 0);
                 ncc = fcc - (pv != 0);  // pv = frame (r, lane)
               }
               const int32_t pvk = c == 0 ? v[0] : v[2];
@@ -262,8 +255,9 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
               if (prod > (__int128)INT64_MAX || prod < (__int128)INT64_MIN) ovf = true;
               kcf[c] = (int64_t)prod;
             } else {
+              const int pka = __shfl_sync(kFull, FC, k.ka);
               if (lane < n && lane != r) {
-                const int32_t va = at(lane, k.ka), vb = at(lane, k.kb);
+                const int32_t va = fat(M, S, colpiv, FR, pka), vb = fat(M, S, colpiv, FR, pkb);
                 const long long mv = (long long)k.al * vb + (long long)k.be * va;
                 if (mv > INT32_MAX || mv < INT32_MIN) ovf = true;
                 mnz = mv != 0;
@@ -275,45 +269,39 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
             const bool dead = lane < n && ((lane != r && nrc == 0) || (lane != k.kb && ncc == 0));
             alive[c] = __all_sync(kFull, !dead) ? 1 : 0;
             // child frame index ii <- parent lane ii + (ii >= r), jj <- jj + (jj >= kb)
-            const int fr = __shfl_sync(kFull, nrc, lane + (lane >= r) < 32 ? lane + (lane >= r) : 31);
-            const int fc = __shfl_sync(kFull, ncc, lane + (lane >= k.kb) < 32 ? lane + (lane >= k.kb) : 31);
+            const int fr = __shfl_sync(kFull, nrc, min(lane + (lane >= r), 31));
+            const int fc = __shfl_sync(kFull, ncc, min(lane + (lane >= k.kb), 31));
             crc[c] = colpiv ? fc : fr;
             ccc[c] = colpiv ? fr : fc;
           }
           if (__any_sync(kFull, ovf) && lane == 0) atomicOr(err, 1);
-          // physical deletion / merge of each child (row pivot: frame = A; column pivot: the
-          // frame's column ops are row ops of A)
-          auto phys = [&](const FKid& k, int& dr, int& dc, int& merge, int& keep) {
-            dr = colpiv ? k.kb : r;
-            dc = colpiv ? r : k.kb;
-            merge = k.minor ? 0 : (colpiv ? 2 : 1);
-            keep = k.ka;
-          };
-          const int m = n - 1;
-          int32_t* Wn = cur ? Wb0 : Wb1;
           if (alive[0] && alive[1]) {
-            // second child -> stack slot m (coef | counts | entries, stride m)
-            int dr, dc, mg, kp;
-            phys(kid[1], dr, dc, mg, kp);
-            int32_t* sl = stk + slot_prefix(L, m);
-            build_child(W, S, m, dr, dc, mg, kp, kid[1].al, kid[1].be, sl + 2 + m, m, lane);
-            if (lane < m) sl[2 + lane] = crc[1] | (ccc[1] << 16);
-            if (lane == 0) *reinterpret_cast<int64_t*>(sl) = kcf[1];
-            pending |= 1u << m;
+            // frame: the parent's maps and order, the second child's split, coefficient and counts
+            int32_t* f = frames + nfr * kFrameW;
+            if (lane == 0) {
+              f[0] = nlog;
+              f[1] = n;
+              f[2] = colpiv;
+              f[3] = r;
+              f[4] = kid[1].minor;
+              f[5] = kid[1].ka;
+              f[6] = kid[1].kb;
+              f[7] = kid[1].al;
+              f[8] = kid[1].be;
+              *reinterpret_cast<int64_t*>(f + 10) = kcf[1];
+            }
+            f[12 + lane] = rid;
+            f[44 + lane] = cid;
+            f[76 + lane] = crc[1] | (ccc[1] << 16);
+            ++nfr;
           }
           const int first = alive[0] ? 0 : alive[1] ? 1 : -1;
           if (first < 0) {
             pop = true;
           } else {
             // (selects, not dynamic indexing: the kid / count arrays stay in registers)
-            const FKid kf = first == 0 ? kid[0] : kid[1];
-            int dr, dc, mg, kp;
-            phys(kf, dr, dc, mg, kp);
-            build_child(W, S, m, dr, dc, mg, kp, kf.al, kf.be, Wn, S, lane);
-            __syncwarp();
-            W = Wn;
-            cur ^= 1;
-            n = m;
+            apply(colpiv, r, first == 0 ? kid[0] : kid[1]);
+            n -= 1;
             rc = first == 0 ? crc[0] : crc[1];
             cc = first == 0 ? ccc[0] : ccc[1];
             cf = first == 0 ? kcf[0] : kcf[1];
@@ -321,22 +309,35 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
         }
       }
       if (pop) {
-        if (!pending) break;
-        const int m = __ffs(pending) - 1;  // the deepest pending sibling
-        pending &= pending - 1;
-        const int32_t* sl = stk + slot_prefix(L, m);
+        if (nfr == 0) break;
+        // the newest frame: undo the merges logged since it was pushed (newest first), restore
+        // the parent's view, then apply the second child's split
+        --nfr;
+        const int32_t* f = frames + nfr * kFrameW;
         __syncwarp();
-        const uint32_t mg = (uint32_t)(0xffffffffull / (uint32_t)m) + 1u;
-        for (int e = lane; e < m * m; e += 32) {
-          const int i = (int)__umulhi((uint32_t)e, mg);
-          W[i * S + (e - i * m)] = sl[2 + m + e];
+        const int mark = f[0];
+        while (nlog > mark) {
+          --nlog;
+          const int32_t* u = ulog + nlog * kUndoW;
+          const int line = u[0];
+          if (lane < n0) {
+            if (line & 0x100) M[(line & 0xff) * S + lane] = u[1 + lane];
+            else M[lane * S + line] = u[1 + lane];
+          }
+          __syncwarp();
         }
-        const int pk = lane < m ? sl[2 + lane] : 0;
+        n = f[1];
+        const bool colpiv = f[2] != 0;
+        const int r = f[3];
+        const FKid k = {f[4], f[5], f[6], f[7], f[8]};
+        cf = *reinterpret_cast<const int64_t*>(f + 10);
+        rid = f[12 + lane];
+        cid = f[44 + lane];
+        const int pk = f[76 + lane];
+        apply(colpiv, r, k);
+        n -= 1;
         rc = pk & 0xffff;
         cc = pk >> 16;
-        cf = *reinterpret_cast<const int64_t*>(sl);
-        n = m;
-        __syncwarp();
       }
     }
   }
@@ -370,50 +371,35 @@ extern "C" int sperm_expand_subtree(const int32_t* d_in_mats, const int64_t* d_i
     return set_error(SPERM_ERR_ARG, "sperm_expand_subtree: NULL leaf output");
   if (cap_early > 0 && (!d_early_mats || !d_early_coef || !d_early_job))
     return set_error(SPERM_ERR_ARG, "sperm_expand_subtree: NULL early output");
-  static const int gstack_env = [] {  // A-B knob: 0 = stack in shared memory
-    const char* e = getenv("SPERM_SUBTREE_GSTACK");
-    return e ? atoi(e) : 1;
-  }();
-  static const int noatomic_env = [] {  // timing experiment only (wrong output)
-    const char* e = getenv("SPERM_SUBTREE_NOATOMIC");
-    return e ? atoi(e) : 0;
-  }();
-  const bool gstack = gstack_env != 0;
-  const int stack_words = slot_prefix(L, n);
-  const int ww = gstack ? ((2 * n * (n | 1)) + 3) / 4 * 4 : sub_warp_words(n, L);
-  const size_t smem = (size_t)kSubWarps * ww * 4;
-  if (smem > 227 * 1024) return set_error(SPERM_ERR_ARG, "sperm_expand_subtree: stack exceeds shared memory");
-  auto kern = gstack ? (noatomic_env ? subtree_kernel<true, true> : subtree_kernel<true, false>)
-                     : (noatomic_env ? subtree_kernel<false, true> : subtree_kernel<false, false>);
+  const size_t smem = (size_t)kSubWarps * (((n * (n | 1)) + 3) / 4 * 4) * 4;
+  const int scratch_words = (n - L + 1) * (kFrameW + kUndoW);
   {
     static std::atomic<unsigned> attr_done{0};
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned bit = 1u << (dev & 31);
     if (!(attr_done.load() & bit)) {
-      for (auto k : {subtree_kernel<true, true>, subtree_kernel<true, false>, subtree_kernel<false, true>,
-                     subtree_kernel<false, false>})
-        SPERM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      SPERM_CUDA(cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr_done.fetch_or(bit);
     }
   }
   int per_sm = 0;
-  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kSubWarps, smem));
+  SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, subtree_kernel, 32 * kSubWarps, smem));
   int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
   grid = std::max<int64_t>(1, std::min<int64_t>(grid, (count + kSubWarps - 1) / kSubWarps));
-  // workspace: root ticket, leaf count, early count (u64) | err (i32)
+  // workspace: root ticket, leaf count, early count (u64) | err (i32) | per-warp scratch
   unsigned long long* ws = nullptr;
-  const size_t gwords = gstack ? (size_t)grid * kSubWarps * stack_words : 0;
-  SPERM_CUDA(cudaMallocAsync((void**)&ws, sizeof(unsigned long long) * 4 + 4 * gwords, st));
+  const size_t swords = (size_t)grid * kSubWarps * scratch_words;
+  SPERM_CUDA(cudaMallocAsync((void**)&ws, sizeof(unsigned long long) * 4 + 4 * swords, st));
   SPERM_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * 4, st));
   int* err = reinterpret_cast<int*>(ws + 3);
-  int32_t* gstk = gstack ? reinterpret_cast<int32_t*>(ws + 4) : nullptr;
+  int32_t* scratch = reinterpret_cast<int32_t*>(ws + 4);
   {
     TimingScope ts("expand", st);
     count_launch();
-    kern<<<(unsigned)grid, 32 * kSubWarps, smem, st>>>(d_in_mats, d_in_coef, d_in_job, n, count, L, ww, d_out_mats,
-                                                       d_out_coef, d_out_job, cap_out, d_early_mats, d_early_coef,
-                                                       d_early_job, cap_early, ws, err, gstk, stack_words);
+    subtree_kernel<<<(unsigned)grid, 32 * kSubWarps, smem, st>>>(
+        d_in_mats, d_in_coef, d_in_job, n, count, L, d_out_mats, d_out_coef, d_out_job, cap_out, d_early_mats,
+        d_early_coef, d_early_job, cap_early, ws, err, scratch, scratch_words);
   }
   cudaError_t le = cudaGetLastError();
   if (le != cudaSuccess) {

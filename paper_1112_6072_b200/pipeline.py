@@ -134,19 +134,16 @@ def expand_to_leaves(jobs: NodeSet, L: int) -> List[NodeSet]:
 # sperm_expand_subtree call (no intermediate level in HBM); SPERM_SUBTREE_DEPTH=0 turns it off.
 import os as _os
 _LEAF_ORDERED = _os.environ.get("SPERM_EXPAND_ORDERED", "0") == "1"
-SUBTREE_DEPTH = int(_os.environ.get("SPERM_SUBTREE_DEPTH", "12"))
+SUBTREE_DEPTH = int(_os.environ.get("SPERM_SUBTREE_DEPTH", "32"))
 
 
 def subtree_root_order(L: int, depth: int = None) -> int:
-    """Order from which sperm_expand_subtree takes over (0: never): L + depth, at most 32, as
-    long as the warp's stack (one slot per order L..n0-1) fits its 56 KB of shared memory."""
+    """Order from which sperm_expand_subtree takes over (0: never): L + depth, at most 32 (one
+    lane per line)."""
     depth = SUBTREE_DEPTH if depth is None else depth
     if depth <= 0 or L < 1 or L >= 32:
         return 0
-    n0 = min(32, L + depth)
-    while n0 > L and 4 * (2 * n0 * (n0 | 1) + sum(k * (k + 1) + 2 for k in range(L, n0))) > 56 * 1024:
-        n0 -= 1
-    return n0 if n0 > L else 0
+    return min(32, L + depth)
 
 
 def iter_leaves(jobs: NodeSet, L: int, budget_bytes: int = 16 << 30, stats=None, subtree_depth: int = None):
