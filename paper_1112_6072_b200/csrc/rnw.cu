@@ -158,7 +158,7 @@ __device__ __forceinline__ M mask_below(int n) {  // bits 0..n-1
 
 template <typename M, int U>
 __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
-                                const int64_t* __restrict__ coef, int min_primes, int max_primes, int allow_tree,
+                                const int64_t* __restrict__ coef, int min_primes, int max_primes, int lift, int allow_tree,
                                 int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err,
                                 unsigned long long* __restrict__ leaf_acc) {
   const int lane = threadIdx.x & 31;
@@ -298,8 +298,10 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     for (M b = my_supp; b; b &= b - 1) my_q = sat_mul(my_q, R[mffs(b) - 1]);
   }
 
-  // ---- number of primes (lane 0)
-  int k = min_primes;
+  // ---- number of primes (lane 0).  k = the leaf's own need; a leaf whose exact value fits the
+  // symmetric range of one or two primes (2 |coef| bound < p_0 [p_1]) is evaluated mod those alone
+  // when `lift` is set, and the finalize lifts its exact value to the residues of min_primes primes
+  int k = lift ? 1 : min_primes;
   if (lane == 0) {
     if (range_bad) atomicOr(err, 1);
     double lb = zero ? -1.0 : fmin(lr, lc);
@@ -314,6 +316,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (max_primes <= 0) atomicOr(err, 2);
       k = kcap;
     }
+    if (k > 2) k = max(k, min_primes);  // one- and two-prime leaves are lifted
   }
   k = __shfl_sync(0xffffffffu, k, 0);
   // ---- tree plans: lane l tests plan l+1 (exact-arithmetic bounds); the first feasible wins
@@ -854,6 +857,20 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
 constexpr int kMaxMexp = 48;
 constexpr int kFinThreads = 256;  // 32 leaves x 8 primes per block iteration
 
+// p_0^-1 mod p_1 (Garner's step for the lifted two-prime leaves)
+__host__ __device__ constexpr uint64_t modpow_c(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1;
+  b %= m;
+  while (e) {
+    if (e & 1) r = r * b % m;
+    b = b * b % m;
+    e >>= 1;
+  }
+  return r;
+}
+constexpr uint64_t kInvP0ModP1 = modpow_c(2147483647ull, 2147483629ull - 2, 2147483629ull);
+static_assert(2147483647ull % 2147483629ull * kInvP0ModP1 % 2147483629ull == 1, "p0^-1 mod p1");
+
 // Per-call scale factors f[q][mexp] = (-1)^(n-1) 2^(1-n) R^mexp mod p_q (R = 2^32: the kernels'
 // Montgomery factors), computed on the host (fin_table) and passed by value.
 struct FinTable {
@@ -866,7 +883,8 @@ struct FinTable {
 __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
     int n, int64_t count, const int2* __restrict__ meta, const unsigned long long* __restrict__ leaf_acc,
     const int64_t* __restrict__ coef, const int32_t* __restrict__ job, uint32_t* __restrict__ leaf_res,
-    int32_t* __restrict__ leaf_k, unsigned long long* __restrict__ job_acc, int64_t num_jobs, const FinTable tab) {
+    int32_t* __restrict__ leaf_k, unsigned long long* __restrict__ job_acc, int64_t num_jobs, const FinTable tab,
+    int min_primes) {
   __shared__ uint32_t s_f[SPERM_KMAX][kMaxMexp];
   for (int t = threadIdx.x; t < SPERM_KMAX * kMaxMexp; t += blockDim.x) s_f[t / kMaxMexp][t % kMaxMexp] = tab.f[t / kMaxMexp][t % kMaxMexp];
   __shared__ unsigned long long s_val[kFinThreads];
@@ -883,14 +901,39 @@ __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
     if (leaf < count) {
       const int2 mt = meta[leaf];
       const int k = meta_k(mt);
-      if (q == 0 && leaf_k) leaf_k[leaf] = k;
+      const int keff = max(k, min_primes);
+      if (q == 0 && leaf_k) leaf_k[leaf] = keff;
       jb = job ? job[leaf] : 0;
+      const int64_t cf = coef ? coef[leaf] : 1;
       if (q < k) {
         val = n == 0 ? 1 : (leaf_acc[leaf * SPERM_KMAX + q] % pq) * s_f[q][mt.y] % pq;
-        const int64_t cf = coef ? coef[leaf] : 1;
         int64_t cm = cf % (int64_t)pq;
         if (cm < 0) cm += (int64_t)pq;
         val = val * (uint64_t)cm % pq;
+      } else if (q < keff) {
+        // lifted leaf (prep: 2 |coef| * bound < p_0 [p_1]): its exact value V is the symmetric
+        // residue mod p_0, or Garner's combination of the residues mod p_0 and p_1, and V mod p_q
+        // is the residue the leaf contributes here
+        auto res = [&](int qq) {
+          const uint64_t pp = (uint64_t)c_p[qq];
+          uint64_t v = n == 0 ? 1 : (leaf_acc[leaf * SPERM_KMAX + qq] % pp) * s_f[qq][mt.y] % pp;
+          int64_t cm = cf % (int64_t)pp;
+          if (cm < 0) cm += (int64_t)pp;
+          return v * (uint64_t)cm % pp;
+        };
+        const uint64_t p0 = (uint64_t)c_p[0], p1 = (uint64_t)c_p[1];
+        const uint64_t r0 = res(0);
+        int64_t V;
+        if (k == 1) {
+          V = r0 > p0 / 2 ? (int64_t)r0 - (int64_t)p0 : (int64_t)r0;
+        } else {
+          const uint64_t r1 = res(1);
+          const uint64_t t = (r1 + p1 - r0 % p1) % p1 * kInvP0ModP1 % p1;
+          const uint64_t u = r0 + p0 * t, m01 = p0 * p1;  // < p0 p1 < 2^62
+          V = u > m01 / 2 ? (int64_t)u - (int64_t)m01 : (int64_t)u;
+        }
+        int64_t r = V % (int64_t)pq;
+        val = (uint64_t)(r < 0 ? r + (int64_t)pq : r);
       }
       if (leaf_res) leaf_res[idx] = (uint32_t)val;
     }
@@ -1312,6 +1355,15 @@ int first_plan() {
   return (p >= 0 && p < kNumPlans) ? p : 1;
 }
 
+// Leaves lifted in the finalize (prep's `lift`): a leaf whose exact value fits the symmetric range
+// of p_0 (or p_0 p_1) is evaluated mod p_0 (and p_1) only, whatever min_primes asks (the R-NW
+// block loop then runs one or two Montgomery chains instead of min_primes).  A-B knob:
+// SPERM_LIFT=0 turns it off.
+bool lift_enabled() {
+  const char* e = getenv("SPERM_LIFT");
+  return !(e && e[0] == '0');
+}
+
 // f[q][y] = (-1)^(n-1) 2^(1-n) (2^32)^y mod p_q (exact uint64 arithmetic on the host)
 FinTable fin_table(int n) {
   FinTable t;
@@ -1643,7 +1695,8 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       }
     }
     prep<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
-                                                                       first_plan(), meta, perm, err, leaf_acc);
+                                                                       lift_enabled() ? 1 : 0, first_plan(), meta,
+                                                                       perm, err, leaf_acc);
     SPERM_TRY(cudaGetLastError());
     count_launch();
     if (small_group)
@@ -1798,7 +1851,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     const int64_t fblocks = std::min<int64_t>((tot + kFinThreads - 1) / kFinThreads, (int64_t)sm_count() * 8);
     rnw_finalize_kernel<<<(unsigned)fblocks, kFinThreads, 0, st>>>(
         n, count, meta, leaf_acc, d_coef, d_job, d_leaf_res, d_leaf_k, (unsigned long long*)d_job_acc, num_jobs,
-        fin_table(n));
+        fin_table(n), min_primes);
   }
   cudaError_t le = cudaGetLastError();
   cleanup();

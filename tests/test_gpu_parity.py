@@ -119,6 +119,37 @@ def test_rnw_order_and_job_accumulators():
     assert P.sperm_crt(red[7], 2) == sum(want)
 
 
+def test_rnw_lifted_one_prime_leaves():
+    """Leaves whose |coef| * bound fits one (two) primes are evaluated mod p_0 (p_1) and lifted to min_primes
+    residues in the finalize: every residue (signed values, signed coefficients, zero, mixed with
+    leaves that need several primes) equals the exact value mod p_q, and equals the unlifted run
+    (SPERM_LIFT=0)."""
+    rng = np.random.default_rng(31)
+    mats = rng.integers(-3, 4, size=(48, 12, 12)) * (rng.random((48, 12, 12)) < 0.35)
+    mats[5] = 0
+    mats[7] = rng.integers(-2**8, 2**8, size=(12, 12))  # needs several primes itself
+    mats[11] = rng.integers(-4, 5, size=(12, 12))  # two primes: lifted by Garner's step
+    cf = rng.integers(-9, 10, size=48)
+    cf[9] = 10**12
+    want = [int(c) * h_per(m) for c, m in zip(cf, mats)]
+    runs = []
+    for lift in ("1", "0"):
+        os.environ["SPERM_LIFT"] = lift
+        try:
+            res, k = P.sperm_permanent(dev(mats), coef=dev(cf, torch.int64), min_primes=4)
+        finally:
+            os.environ.pop("SPERM_LIFT", None)
+        r = res.cpu().numpy().view(np.uint32)
+        kk = k.cpu().numpy()
+        assert (kk >= 4).all()
+        for i, w in enumerate(want):
+            for q in range(kk[i]):
+                assert int(r[i, q]) == w % P.sperm_prime(q), (lift, i, q)
+        assert P.residues_to_ints(res, k) == want
+        runs.append(r.copy())
+    assert (runs[0] == runs[1]).all()
+
+
 # ------------------------------------------------------------------ expansion
 def _gpu_jobs(a, J):
     sets = pipeline.pre_expand(pipeline.root_nodeset(a), jobs_at_least=J)
