@@ -167,40 +167,54 @@ __global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restric
 // of a zero, and a zero's sign never reaches a pivot magnitude |b|^2, a nonzero sum or the
 // product of the d_k — so X is bit-identical with the update skipped.
 // pivot of column k (rows >= k): first row with maximal re^2 + im^2 — per lane ascending with a
-// strict >, then a (larger value, then smaller row) butterfly; lane 0 publishes it
-__device__ __forceinline__ void pivot_reduce(double bm, int bi, int lane, double& s_d, int& s_p) {
+// strict >, then a (larger value, then smaller row) butterfly; lane 0 publishes it, and the last
+// row of the column holding a nonzero entry (the multipliers below it are zero)
+__device__ __forceinline__ void pivot_reduce(double bm, int bi, int last, int lane, double& s_d, int& s_p,
+                                             int& s_last) {
   for (int o = 16; o; o >>= 1) {
     const double om = __shfl_xor_sync(0xffffffffu, bm, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (om > bm || (om == bm && oi < bi)) { bm = om; bi = oi; }
   }
+  last = __reduce_max_sync(0xffffffffu, last);
   if (lane == 0) {
     s_d = bm;
     s_p = bi;
+    s_last = last;
   }
 }
 __device__ __forceinline__ void pivot_scan(const double2* b, int ns, int n, int k, int lane, double& s_d,
-                                           int& s_p) {
+                                           int& s_p, int& s_last) {
   double bm = -1.0;
-  int bi = n;
+  int bi = n, last = -1;
   for (int i = k + lane; i < n; i += 32) {
     const double2 v = b[i * ns + k];
     const double mg = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
     if (mg > bm) { bm = mg; bi = i; }
+    if (v.x != 0.0 || v.y != 0.0) last = i;
   }
-  pivot_reduce(bm, bi, lane, s_d, s_p);
+  pivot_reduce(bm, bi, last, lane, s_d, s_p, s_last);
 }
 
+// Per elimination step only rows k+1..rmax are updated, rmax = the last row with a nonzero entry
+// in column k (every multiplier below it is zero; warp 0 finds it in the pivot search), and
+// columns whose pivot-row entry u_j is zero are skipped.  A skipped entry b_ij - l_i u_j with
+// l_i = 0 or u_j = 0 equals b_ij up to the sign of a zero, which never reaches |b|^2, a nonzero
+// sum or the d_k, so X stays bit-identical while the work follows the band of the sparse job
+// matrices (their fill-in stays near the diagonal) instead of the full (n-k)^2 trailing block.
+// (Measured: an exact last-nonzero-column bound of the pivot row, found by a warp reduction and
+// a shared atomic in the exchange phase, doubled the step time — that phase is on every step's
+// critical path — so columns are only skipped by their zero u_j.)
 template <int NT>
 __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
                                                                 const int32_t* __restrict__ ids, int trials,
-                                                                uint64_t seed, double* __restrict__ xout) {
+                                                                uint64_t seed, double* __restrict__ xout, int band) {
   extern __shared__ double2 ksm2[];  // b[n][ns] (row stride ns = n | 1: column scans conflict-free) | lv[n]
   const int ns = n | 1;
   double2* b = ksm2;
   double2* lv = ksm2 + n * ns;
   __shared__ double s_d;
-  __shared__ int s_p;
+  __shared__ int s_p, s_last;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const double S32 = 0.8660254037844386;
   const int64_t items = count * (int64_t)trials;
@@ -222,17 +236,19 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
     }
     __syncthreads();
     double x = 1.0;
-    if (w == 0) pivot_scan(b, ns, n, 0, lane, s_d, s_p);  // later pivots come out of the update
+    if (w == 0) pivot_scan(b, ns, n, 0, lane, s_d, s_p, s_last);  // later pivots come out of the update
     __syncthreads();
     for (int k = 0; k < n; ++k) {
       const double d = s_d;
       const int p = s_p;
+      const int rmax = band ? s_last : n - 1;
       if (d == 0.0) { x = 0.0; break; }  // CTA-uniform
       x = __dmul_rn(x, d);
       if (k + 1 == n) break;
       // one phase, one barrier: the row exchange of columns > k (column k is never read again
-      // for X) and the multipliers, which read column k only — with the exchange applied on the
-      // fly: the pivot value is row p's, and row i = p (after the exchange: old row k) reads row k's
+      // for X) and the multipliers of rows k+1..rmax, which read column k only — with the
+      // exchange applied on the fly: the pivot value is row p's, and row i = p (after the
+      // exchange: old row k) reads row k's
       if (p != k)
         for (int j = k + 1 + t; j < n; j += NT) {
           const double2 u = b[k * ns + j];
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
         const double2 pk = b[p * ns + k];
         const double y = __drcp_rn(d);
         const bool d_ok = div_range_ok(d);
-        for (int i = k + 1 + t; i < n; i += NT) {
+        for (int i = k + 1 + t; i <= rmax; i += NT) {
           const double2 v = b[(i == p ? k : i) * ns + k];
           lv[i] = make_double2(div_by(__dadd_rn(__dmul_rn(v.x, pk.x), __dmul_rn(v.y, pk.y)), d, y, d_ok),
                                div_by(__dsub_rn(__dmul_rn(v.y, pk.x), __dmul_rn(v.x, pk.y)), d, y, d_ok));
@@ -251,16 +267,17 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
       }
       __syncthreads();
       if (w == 0) {
-        // warp 0: column k+1 (the next pivot column), then the next pivot search over it while
-        // the update of columns > k+1 is still running — s_d/s_p were last read before the barrier
+        // warp 0: column k+1 (the next pivot column) in rows k+1..rmax, then the next pivot search
+        // over the whole column while the update of columns > k+1 is still running — s_d/s_p/s_last
+        // were last read before the barrier
         const int j = k + 1;
         const double2 u = b[k * ns + j];
         const bool nz = u.x != 0.0 || u.y != 0.0;
         double bm = -1.0;
-        int bi = n;
+        int bi = n, last = -1;
         for (int i = j + lane; i < n; i += 32) {
           double2 v = b[i * ns + j];
-          if (nz) {
+          if (nz && i <= rmax) {
             const double2 l = lv[i];
             v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
             v.y = __dsub_rn(v.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
@@ -268,18 +285,20 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
           }
           const double mg = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
           if (mg > bm) { bm = mg; bi = i; }
+          if (v.x != 0.0 || v.y != 0.0) last = i;
         }
-        pivot_reduce(bm, bi, lane, s_d, s_p);
-      } else {
-        // columns > k+1: thread t' = t - 32 -> column j = k+2 + t' % m, rows k+1 + t' / m + G * r;
-        // when the m columns outnumber the NT - 32 threads, whole columns j = k+2 + t' + (NT-32) * c
+        pivot_reduce(bm, bi, last, lane, s_d, s_p, s_last);
+      } else if (rmax > k) {
+        // columns k+2..n-1, rows k+1..rmax: thread t' = t - 32 -> column j = k+2 + t' % m, rows
+        // k+1 + t' / m + G * r; when the m columns outnumber the NT - 32 threads, whole columns
+        // j = k+2 + t' + (NT-32) * c
         const int m = n - k - 2;
         const int tt = t - 32;
         auto column = [&](int j, int g, int G) {
           const double2 u = b[k * ns + j];
           if (u.x != 0.0 || u.y != 0.0) {
 #pragma unroll 4
-            for (int i = k + 1 + g; i < n; i += G) {
+            for (int i = k + 1 + g; i <= rmax; i += G) {
               const double2 l = lv[i];
               double2 v = b[i * ns + j];
               v.x = __dsub_rn(v.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
@@ -369,7 +388,11 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     grid = std::max<int64_t>(1, std::min(grid, items));
     TimingScope ts("kklll", st);
     count_launch();
-    kern<<<(unsigned)grid, nt, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+    static const int band = [] {  // A-B knob: SPERM_KKLLL_BAND=0 updates the whole trailing block
+      const char* e = getenv("SPERM_KKLLL_BAND");
+      return e ? atoi(e) : 1;
+    }();
+    kern<<<(unsigned)grid, nt, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs, band);
   }
   cudaError_t le = cudaGetLastError();
   if (le == cudaSuccess) {
