@@ -31,7 +31,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "R-NW Gray-code terms/s (configs[1]: 256 x n=24 3-regular, exact per(A))"
+METRIC = ("R-NW Gray-code terms/s, closed-form-equivalent (2^(n-1) terms per n x n matrix; configs[1]: "
+          "256 x n=24 3-regular, exact per(A))")
 UNIT = "terms/s"
 N_MATS, ORDER, SEED = 256, 24, 2024
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -272,6 +273,17 @@ def main():
     terms_step = P.sperm_rnw_terms(ORDER, N_MATS) * world
     value = terms_step * args.steps / (total_ms * 1e-3)
     e2e_value = terms_step * args.steps / (e2e_total * 1e-3)
+    # dram read + write bytes of the step's R-NW launches from the committed ncu --set full capture
+    # of this build's bench step (tools/ncu_traffic.py -> profiles_bench/rnw_traffic.json; profiles/ does not travel to the GPU box)
+    traffic, traffic_note = None, "no ncu capture committed for this build"
+    try:
+        with open(os.path.join(ROOT, "profiles_bench", "rnw_traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj["bytes_per_step"]
+        traffic_note = (f"dram__bytes_read.sum + dram__bytes_write.sum of the step's R-NW launches, ncu --set full "
+                        f"({tj['source']}, {tj['launches_per_step']} launches per step)")
+    except Exception:
+        pass
     # roofline of the dominant kernel (rnw_main) on this rank
     pk, pk_kind = peaks()
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
@@ -295,10 +307,7 @@ def main():
                    "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world} weak"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_ops / 1e9, "unit": "Gop/s",
                      "frac": (achieved / peak_ops) if peak_ops else None,
-                     # dram__bytes_read.sum + dram__bytes_write.sum of the step's four R-NW launches
-                     # (ncu --set full, profiles/r01_final_ncu.txt): the kernel is not memory bound
-                     "traffic": 832000, "traffic_note": "dram read+write bytes of the step's three R-NW launches, "
-                                                         "ncu --set full (profiles/r01_v8_rnw_tree_ncu.txt)",
+                     "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": "rnw_tree_kernel / rnw_generic_kernel (all R-NW launches of the step)",
                      "kernel_ms_per_step": rnw_avg_s * 1e3, "launches_per_step": rnw_launches / max(args.steps, 1),
                      "kernel_share_of_step": rnw_ms / instr_ms,
@@ -308,6 +317,11 @@ def main():
                      "terms_per_s_kernel": st_terms / rnw_s if rnw_s else None,
                      "peak_note": f"{nsm} SM x 64 lane-ops/clk per int pipe (mul, alu; measured tools/microbench) "
                                   f"x {sm_mhz:.0f} MHz ({pk_kind} sm_max); bound = busier pipe"},
+        "per_A": {"batch_ms_device": total_ms / args.steps, "matrices_per_s": N_MATS * world * args.steps / (total_ms * 1e-3),
+                  "batch_ms_e2e": e2e_total / args.steps,
+                  "note": "exact per(A) of every matrix of the 256-matrix batch per step (the headline terms/s count "
+                          "2^(n-1) equivalent Gray-code terms per matrix; the closed-form block sums evaluate 2^B "
+                          "of them per block, DESIGN.md 5.1)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_mats.numel() * 4),
                 "d2h_bytes_per_step": int(N_MATS * (P.KMAX + 3) * 4),  # [256][limbs + 1] CRT words
                 "api": "sperm_permanent_host (host buffers; H2D + R-NW + device CRT + D2H in one C call)"},
@@ -481,6 +495,8 @@ def bench_c100(P, torch, leaf_order: int = 15, jobs_at_least: int = 159):
     P.sperm_timing_enable(True)
     P.sperm_timing_reset()
     P.sperm_rnw_stats(reset=True)
+    P.sperm_expand_stats(reset=True)
+    P.sperm_expand_subtree_stats(reset=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = pipeline.permanent(paper_graph("C100"), jobs_at_least=jobs_at_least, leaf_order=leaf_order,
@@ -489,6 +505,8 @@ def bench_c100(P, torch, leaf_order: int = 15, jobs_at_least: int = 159):
     wall = time.perf_counter() - t0
     stages = {name: P.sperm_timing_get(name)[0] for name in ("expand", "kklll", "rnw_prep", "rnw", "rnw_finalize")}
     terms = P.sperm_rnw_stats(reset=True)[0]
+    lvl_bytes, lvl_nodes = P.sperm_expand_stats(reset=True)
+    sub_bytes, sub_roots = P.sperm_expand_subtree_stats(reset=True)
     P.sperm_timing_enable(False)
     # the paper's load-balance study on this run's measured job costs T_i (SM cycles of each job's
     # R-NW leaves): Kendall tau (Eq. 10, Table 3) and Tables 5-7's efficiencies of Step 3 at m
@@ -505,7 +523,12 @@ def bench_c100(P, torch, leaf_order: int = 15, jobs_at_least: int = 159):
             "per": str(r.value), "paper_table_T12_total": str(pin), "matches_paper": r.value == pin,
             "wall_s": wall, "jobs": r.num_jobs, "leaves": r.leaves, "terms": terms,
             "stage_ms": stages, "stage_note": "device time per stage (library CUDA-event timers, one stream); "
-                                              "per-job cycle counters on (measure_jobs)",
+                                              "per-job cycle counters on (measure_jobs); 'expand' = the level "
+                                              "kernels down to order 32 + the depth-first subtree kernel below",
+            "expansion_bytes": {"level_kernels": lvl_bytes, "level_parents": lvl_nodes, "subtree_kernel": sub_bytes,
+                                "subtree_roots": sub_roots,
+                                "note": "algorithmic bytes: parents/roots read once, children/leaves written once"},
+            "leaves_per_s": r.leaves / (wall if wall else 1.0),
             "kendall_tau_T_estimate": tau_est, "kendall_tau_T_size": tau_size,
             "tau_z_estimate": P.tau_z(tau_est, len(T)),
             "paper_tau_T_AP_table3": 0.4919, "paper_tau_T_P_table3": 0.5334,
