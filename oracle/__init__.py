@@ -14,6 +14,8 @@ KKLLL estimator.  Citations are PAPER.md line numbers.
   permanent.py  Eq. (1) brute force; Ryser's inclusion-exclusion (R-NW family)
   hybrid.py     Eq. (2) expansion, Algorithm H_per, Algorithm PH Step 2 (BFS)
   frontier.py   row-frontier DP over used-column sets (independent pin tool)
+  frontier.c    the same DP in C (cfrontier.py loads it): the n = 96 goldens
+  stats.py      Kendall's tau with the tie correction, Eqs. (7)-(10), by definition
   kklll.py      Algorithm KKLLL with a counter-based RNG
   schedule.py   LS / LPT / estimated order
   crt.py        Chinese remaindering and the Bregman / row-sum bounds
