@@ -49,7 +49,13 @@
 namespace sperm {
 namespace {
 
-constexpr int kRnwThreads = 256;  // 8 warps per CTA
+#ifndef SPERM_RNW_THREADS  // threads per R-NW CTA (A-B builds: 128)
+#define SPERM_RNW_THREADS 256
+#endif
+#ifndef SPERM_RNW_WARPS2  // resident warps per SM the register-heavy ("2-CTA") tree plans are
+#define SPERM_RNW_WARPS2 16  // bounded for (16: 2 x 256 threads, <= 128 registers)
+#endif
+constexpr int kRnwThreads = SPERM_RNW_THREADS;  // 8 warps per CTA
 constexpr int kMaxLaneBits = 14;  // terms per lane <= 2^14
 constexpr int KS = 3;             // slot rows per low column (tree plans)
 constexpr int kNumNFix = 7;
@@ -76,9 +82,13 @@ constexpr int kNumPlans = 13;
 // resident 256-thread CTAs per SM a tree kernel is compiled for: 3 (<= 85 registers, 24 warps to
 // hide the fixed-latency multiply chains of short blocks) where ptxas fits it without spilling
 // (-Xptxas -v over all plans and NFIX), else 2
+__host__ __device__ constexpr int tree_warps(int B, int nfix, int gf) {
+  return gf == 4 ? ((B <= 4 && 3 * B + nfix <= 24) || (B == 5 && nfix <= 4) || (B <= 3 && nfix <= 16) ? 24
+                                                                                                   : SPERM_RNW_WARPS2)
+                 : (3 * B + nfix <= 20 ? 24 : SPERM_RNW_WARPS2);
+}
 __host__ __device__ constexpr int tree_min_blocks(int B, int nfix, int gf) {
-  return gf == 4 ? ((B <= 4 && 3 * B + nfix <= 24) || (B == 5 && nfix <= 4) || (B <= 3 && nfix <= 16) ? 3 : 2)
-                 : (3 * B + nfix <= 20 ? 3 : 2);
+  return tree_warps(B, nfix, gf) / (kRnwThreads / 32);
 }
 constexpr int kMaxLow = 8;  // low columns picked per leaf
 // Tree-kernel block loop variants (A-B builds, tools/build_variant.py): a flip of a high column
@@ -646,7 +656,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
   constexpr int NGF = NFIX / GF;   // exact fixed-row groups
   // block-loop unroll: kBlockUnroll where registers allow (2-CTA builds with <= 28 register rows,
   // B <= 7; the others spill when unrolled)
-  constexpr int UNR = (tree_min_blocks(B, NFIX, GF) == 2 && NRT <= 28 && B <= 7) ? kBlockUnroll : 1;
+  constexpr int UNR = (tree_warps(B, NFIX, GF) < 24 && NRT <= 28 && B <= 7) ? kBlockUnroll : 1;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   const TreeSmem L = tree_smem(NRT, NS, n, B);
@@ -731,7 +741,11 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     int64_t acc[SPERM_KMAX];
 #pragma unroll
     for (int q = 0; q < SPERM_KMAX; ++q) acc[q] = 0;
-    const uint64_t O0 = t0 >> B;
+    // The lane's blocks are O0 + ob, O0 = t0 >> B = (chunk * 32 + lane) << (m - B), ob < 2^(m-B):
+    // O0 + ob = O0 | ob, so the Gray bits a block needs (bit 0: the sign; bit hh + 1 <= m - B:
+    // the flip direction) are those of the 32-bit ob | ext, ext = bit 0 of (chunk * 32 + lane)
+    // moved to position m - B — no 64-bit arithmetic in the block loop.
+    const uint32_t ext = (uint32_t)(((chunk << 5) + (uint64_t)lane) & 1ull) << (m - B);
     const uint32_t nblk = 1u << (m - B);
     // the block loop, instantiated for the leaf's prime count K = 1, 2, 3 (straight-line prime
     // loops) and for K = SPERM_KMAX with a runtime bound; the E mode is tested once per block.
@@ -740,15 +754,19 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     // the flipped high column touches (its warp-uniform mask; the first block computes all)
     constexpr int NP2 = (B + 1) / 2, NP4 = (B + 3) / 4;
     int32_t E[B], FG[NGF];
-    auto blocks = [&](auto kc) {
+    // instantiated per prime count K and per E mode EM (the leaf's exact E grouping: 2 quads,
+    // 1 pairs, 0 singles; warp-uniform per leaf), so the loop body has no mode branches
+    auto blocks = [&](auto kc, auto emc) {
       constexpr int K = decltype(kc)::value;
+      constexpr int EM = decltype(emc)::value;
 #pragma unroll UNR
       for (uint32_t ob = 0; ob < nblk; ++ob) {
         uint32_t mk = 0xffffffffu;
+        const uint32_t gb = ob | ext;  // the block's low Gray-relevant bits (see ext)
         if (ob) {  // flip high Gray bit B + hh (warp-uniform column): only the touched row groups
           const int hh = __ffs(ob) - 1;
           mk = (uint32_t)sm[L.mask + hh];
-          const bool add = !(((O0 + ob) >> (hh + 1)) & 1ull);
+          const bool add = !((gb >> (hh + 1)) & 1u);
           const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
 #pragma unroll
           for (int v = 0; v < S4 / 4; ++v) {
@@ -789,10 +807,10 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           }
         }
 #pragma unroll
-        for (int j = 0; j < NP2; ++j)
+        for (int j = 0; j < (EM != 0 ? NP2 : 0); ++j)
           P2[j] = 2 * j + 1 < B ? (int32_t)((uint32_t)E[2 * j] * (uint32_t)E[2 * j + 1]) : E[2 * j];
 #pragma unroll
-        for (int j = 0; j < NP4; ++j)
+        for (int j = 0; j < (EM == 2 || EM < 0 ? NP4 : 0); ++j)
           P4[j] = 2 * j + 1 < NP2 ? (int32_t)((uint32_t)P2[2 * j] * (uint32_t)P2[2 * j + 1]) : P2[2 * j];
         if (!(kSparseE) || (mk & (1u << 24))) {
 #pragma unroll
@@ -805,7 +823,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         }
         // the sign (-1)^{|high Gray bits|} rides on the first factor (prime-independent): the
         // Montgomery chain then yields a residue of the signed block value, congruent mod p
-        const int32_t f0 = (((O0 + ob) & 1ull) ^ (kEForm != 0 && (B & 1))) ? -FG[0] : FG[0];
+        const int32_t f0 = ((gb & 1u) ^ (kEForm != 0 && (B & 1))) ? -FG[0] : FG[0];
         // per prime: P_F's chain, then the exact E groups of the leaf's mode
         auto chain = [&](auto gsz, const int32_t* grp) {
           constexpr int NGR = decltype(gsz)::value;
@@ -821,20 +839,34 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
             acc[q] += (int64_t)v;
           }
         };
-        if (emode == 2) chain(std::integral_constant<int, NP4>{}, P4);  // warp-uniform per leaf
+        if constexpr (EM == 2) chain(std::integral_constant<int, NP4>{}, P4);
+        else if constexpr (EM == 1) chain(std::integral_constant<int, NP2>{}, P2);
+        else if constexpr (EM == 0) chain(std::integral_constant<int, B>{}, E);
+        else if (emode == 2) chain(std::integral_constant<int, NP4>{}, P4);  // EM < 0: per block
         else if (emode == 1) chain(std::integral_constant<int, NP2>{}, P2);
         else chain(std::integral_constant<int, B>{}, E);
       }
     };
+    // (the mode-specialised loops triple the code; only the unrolled 2-CTA variants (<= 28 register
+    // rows) get them — specialised, several 3-CTA and wide variants spilled)
+    auto by_mode = [&](auto kc) {
+      if constexpr (UNR > 1) {  // the 2-CTA variants with <= 28 register rows
+        if (emode == 2) blocks(kc, std::integral_constant<int, 2>{});  // warp-uniform per leaf
+        else if (emode == 1) blocks(kc, std::integral_constant<int, 1>{});
+        else blocks(kc, std::integral_constant<int, 0>{});
+      } else {
+        blocks(kc, std::integral_constant<int, -1>{});
+      }
+    };
     if constexpr (NRT <= 40) {
       switch (k) {
-        case 1: blocks(std::integral_constant<int, 1>{}); break;
-        case 2: blocks(std::integral_constant<int, 2>{}); break;
-        case 3: blocks(std::integral_constant<int, 3>{}); break;
-        default: blocks(std::integral_constant<int, SPERM_KMAX>{}); break;
+        case 1: by_mode(std::integral_constant<int, 1>{}); break;
+        case 2: by_mode(std::integral_constant<int, 2>{}); break;
+        case 3: by_mode(std::integral_constant<int, 3>{}); break;
+        default: by_mode(std::integral_constant<int, SPERM_KMAX>{}); break;
       }
-    } else {  // many register-resident rows: one copy of the loop (no spills)
-      blocks(std::integral_constant<int, SPERM_KMAX>{});
+    } else {  // many register-resident rows: one copy of the loop per mode (no spills)
+      by_mode(std::integral_constant<int, SPERM_KMAX>{});
     }
 #pragma unroll
     for (int q = 0; q < SPERM_KMAX; ++q) {
