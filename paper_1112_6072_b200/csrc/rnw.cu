@@ -166,18 +166,35 @@ __device__ __forceinline__ M mask_below(int n) {  // bits 0..n-1
   return n >= (int)(8 * sizeof(M)) ? ~M(0) : (M(1) << n) - 1;
 }
 
-template <typename M, int U>
+// segment collectives of the prep kernel: a W-lane segment (W = 32 or 16) of the warp
+template <int W>
+__device__ __forceinline__ unsigned seg_mask() { return W == 32 ? 0xffffffffu : 0xffffu << (threadIdx.x & 16); }
+template <int W>
+__device__ __forceinline__ unsigned seg_ballot(bool p) {
+  const unsigned b = __ballot_sync(seg_mask<W>(), p);
+  return W == 32 ? b : (b >> (threadIdx.x & 16)) & 0xffffu;
+}
+template <int W>
+__device__ __forceinline__ constexpr unsigned seg_full() { return W == 32 ? 0xffffffffu : 0xffffu; }
+
+template <typename M, int U, int W>
 __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg, int64_t count,
                                 const int64_t* __restrict__ coef, int min_primes, int max_primes, int lift, int allow_tree,
                                 int2* __restrict__ meta, int8_t* __restrict__ perm, int* __restrict__ err,
                                 unsigned long long* __restrict__ leaf_acc) {
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int64_t leaf = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (leaf >= count) return;
+  // one W-lane segment per leaf (W = 32, or 16 for n <= 16: two leaves per warp, no idle lanes);
+  // `lane` is the lane within the segment, collectives stay inside it (seg_* helpers)
+  const int lane = threadIdx.x & (W - 1);
+  const unsigned SM = seg_mask<W>();  // the segment's lanes: segments branch independently
+  const int wib = threadIdx.x / W;
+  const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / W;
+  if (seg - (threadIdx.x & 31) / W >= count) return;  // the whole warp is past the end
+  // a segment past the end (W = 16, odd count) repeats the last leaf, writing the same values,
+  // so both segments of the warp stay in every collective
+  const int64_t leaf = seg < count ? seg : count - 1;
   if (lane < SPERM_KMAX) leaf_acc[leaf * SPERM_KMAX + lane] = 0;  // the R-NW accumulators
   // stage the leaf in shared memory with coalesced loads; the per-lane row/column scans
-  // below then read shared memory (one warp per leaf, 8 warps per CTA)
+  // below then read shared memory (one segment per leaf, 256 / W segments per CTA)
   extern __shared__ int32_t prep_sm[];
   const int ns = n + 1;  // padded row stride: the row scans a[i*ns + j] hit distinct banks
   int32_t* sa = prep_sm + wib * (n * ns);
@@ -188,33 +205,34 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     const int32_t* g = mats + leaf * (int64_t)n * n;
     const int nn = n * n;
     const uint32_t magic = (uint32_t)(0xffffffffull / (uint32_t)n) + 1u;  // e / n for e < 2^16
-    for (int base = 0; base < nn; base += 32 * U) {
+    for (int base = 0; base < nn; base += W * U) {
       int32_t r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = base + u * 32 + lane;
+        const int e = base + u * W + lane;
         r[u] = e < nn ? g[e] : 0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = base + u * 32 + lane;
+        const int e = base + u * W + lane;
         const int i = (int)__umulhi((uint32_t)e, magic);
         if (e < nn) sa[i * ns + (e - i * n)] = r[u];
       }
     }
-    __syncwarp();
+    __syncwarp(SM);
   }
   const int32_t* a = sa;
-  __shared__ int64_t sR[8][SPERM_NMAX];
-  __shared__ M sSupp[8][SPERM_NMAX];
-  __shared__ int sCnt[8][SPERM_NMAX];
-  __shared__ int sBl[8][SPERM_NMAX];  // bit length of each row bound: R_i < 2^bl_i
+  constexpr int NSEG = 256 / W;
+  __shared__ int64_t sR[NSEG][SPERM_NMAX];
+  __shared__ M sSupp[NSEG][SPERM_NMAX];
+  __shared__ int sCnt[NSEG][SPERM_NMAX];
+  __shared__ int sBl[NSEG][SPERM_NMAX];  // bit length of each row bound: R_i < 2^bl_i
   int64_t* R = sR[wib];
   M* supp = sSupp[wib];
   int* cnt = sCnt[wib];
   double lr = 0.0, lc = 0.0, br = 0.0, bc = 0.0;  // log2 of row/col sum bounds, Bregman-Minc
   bool zero = false, range_bad = false, binary = true;
-  for (int i = lane; i < n; i += 32) {
+  for (int i = lane; i < n; i += W) {
     int64_t r = 0, c = 0;
     M sm = 0;
     int nz = 0;
@@ -242,21 +260,21 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (c <= SPERM_NMAX) bc += breg_term((int)c);
     }
   }
-  for (int o = 16; o; o >>= 1) {
-    lr += __shfl_xor_sync(0xffffffffu, lr, o);
-    lc += __shfl_xor_sync(0xffffffffu, lc, o);
-    br += __shfl_xor_sync(0xffffffffu, br, o);
-    bc += __shfl_xor_sync(0xffffffffu, bc, o);
+  for (int o = W / 2; o; o >>= 1) {
+    lr += __shfl_xor_sync(SM, lr, o, W);
+    lc += __shfl_xor_sync(SM, lc, o, W);
+    br += __shfl_xor_sync(SM, br, o, W);
+    bc += __shfl_xor_sync(SM, bc, o, W);
   }
-  zero = __any_sync(0xffffffffu, zero);
-  range_bad = __any_sync(0xffffffffu, range_bad);
-  binary = __all_sync(0xffffffffu, binary);
+  zero = seg_ballot<W>(zero) != 0;
+  range_bad = seg_ballot<W>(range_bad) != 0;
+  binary = seg_ballot<W>(binary) == seg_full<W>();
   // Bregman-Minc: per(A) <= prod_i (r_i!)^(1/r_i) for a 0/1 matrix (and by columns)
   if (binary) {
     lr = fmin(lr, br);
     lc = fmin(lc, bc);
   }
-  __syncwarp();
+  __syncwarp(SM);
 
   // ---- tree plan: greedy pick of up to kMaxLow low columns with disjoint supports of <= 3
   // rows, lane l starting from column l mod n; picks packed one byte each (no local memory)
@@ -269,9 +287,9 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     for (int lvl = 1; lvl <= KS; ++lvl) {
       // columns with exactly lvl nonzeros, visited in the lane's rotated order l0, l0+1, ...
       M m = 0;
-      for (int c0 = 0; c0 < n; c0 += 32) {
+      for (int c0 = 0; c0 < n; c0 += W) {
         const int j = c0 + lane;
-        m |= (M)__ballot_sync(0xffffffffu, j < n && cnt[j] == lvl) << c0;
+        m |= (M)seg_ballot<W>(j < n && cnt[j] == lvl) << c0;
       }
       M rot = l0 ? ((m >> l0) | (m << (n - l0))) & nmask : m;
       while (rot) {
@@ -287,11 +305,11 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     }
   }
   // best lane: most picks, lowest lane on ties
-  int key = (np << 8) | (31 - lane);
-  for (int o = 16; o; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
-  const int best = 31 - (key & 0xff);
+  int key = (np << 8) | (W - 1 - lane);
+  for (int o = W / 2; o; o >>= 1) key = max(key, __shfl_xor_sync(SM, key, o, W));
+  const int best = W - 1 - (key & 0xff);
   np = key >> 8;
-  packed = __shfl_sync(0xffffffffu, packed, best);
+  packed = __shfl_sync(SM, packed, best, W);
   // lane c < np: support of low column c and the product of its slot rows' bounds
   auto sat_mul = [](int64_t x, int64_t y) -> int64_t {
     // saturating product of non-negative bounds (no 64-bit division): saturate at 2^40 when the
@@ -328,7 +346,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     }
     if (k > 2) k = max(k, min_primes);  // one- and two-prime leaves are lifted
   }
-  k = __shfl_sync(0xffffffffu, k, 0);
+  k = __shfl_sync(SM, k, 0, W);
   // ---- tree plans: lane l tests plan l+1 (exact-arithmetic bounds); the first feasible wins
   const int pl = lane + 1;
   bool feasible = false;
@@ -347,8 +365,8 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
 #pragma unroll
     for (int c = 0; c < kMaxLow; ++c) {  // warp-uniform shuffles, per-lane plan bounds
       if (c >= np) break;                  // warp-uniform: no plan uses more than np columns
-      const int64_t q = __shfl_sync(0xffffffffu, my_q, c);
-      const M sc = __shfl_sync(0xffffffffu, my_supp, c);
+      const int64_t q = __shfl_sync(SM, my_q, c, W);
+      const M sc = __shfl_sync(SM, my_supp, c, W);
       if (c < B) {
         slot_rows |= sc;
         if (q >= ((int64_t)1 << 30)) qok = false;
@@ -384,13 +402,13 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       if (ok) pmexp = nfix_of(fi) / GF - 1 + ngroups;
     }
   }
-  const unsigned fmask = __ballot_sync(0xffffffffu, feasible);
+  const unsigned fmask = seg_ballot<W>(feasible);
   if (fmask) {
     const int win = __ffs(fmask) - 1;  // lowest plan index = preferred
     const int wpl = win + 1, B = plan_b(wpl);
-    const int wfi = __shfl_sync(0xffffffffu, fi, win);
+    const int wfi = __shfl_sync(SM, fi, win, W);
     const int NF = nfix_of(wfi);
-    slot_rows = __shfl_sync(0xffffffffu, slot_rows, win);
+    slot_rows = __shfl_sync(SM, slot_rows, win, W);
     // permutation record, written by all lanes in parallel: rows [slot rows of low column c
     // (ascending, -1 padded to KS)..., fixed rows ascending, -1 to NS + NF]; columns [low
     // columns, high columns ascending, nw]
@@ -402,12 +420,12 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     for (int c = 0; c < B; ++c) low |= M(1) << ((packed >> (8 * c)) & 0xff);
     // nw column: the non-low column with most nonzeros (highest index on ties)
     int nwkey = -1;
-    for (int j = lane; j < n; j += 32)
+    for (int j = lane; j < n; j += W)
       if (!((low >> j) & 1)) nwkey = max(nwkey, (cnt[j] << 8) | j);
-    for (int o = 16; o; o >>= 1) nwkey = max(nwkey, __shfl_xor_sync(0xffffffffu, nwkey, o));
+    for (int o = W / 2; o; o >>= 1) nwkey = max(nwkey, __shfl_xor_sync(SM, nwkey, o, W));
     const int nw = nwkey & 0xff;
     const M high = nmask & ~low & ~(M(1) << nw);
-    for (int i = lane; i < n; i += 32) {
+    for (int i = lane; i < n; i += W) {
       const M below = (M(1) << i) - 1;
       if ((fixed >> i) & 1) {
         pr[B * KS + mpop(fixed & below)] = (int8_t)i;
@@ -424,7 +442,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
       pc[lane] = (int8_t)j;
       for (int s = mpop(supp[j]); s < KS; ++s) pr[lane * KS + s] = -1;
     }
-    for (int f = n - mpop(slot_rows) + lane; f < NF; f += 32) pr[B * KS + f] = -1;
+    for (int f = n - mpop(slot_rows) + lane; f < NF; f += W) pr[B * KS + f] = -1;
     if (lane == 0) pc[n - 1] = (int8_t)nw;
     if (lane == win) {
       pr[kPermGend] = (int8_t)emode;  // this lane tested the winning plan
@@ -1704,13 +1722,20 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   const bool small_group = count <= kSmallGroup;
   {
     TimingScope ts("rnw_prep", st);
-    const int64_t threads = count * 32;
+    // one 16-lane segment per leaf for n <= 16 (two leaves per warp), else one warp
+    static const int prep16 = [] {  // A-B knob: SPERM_PREP16=0 keeps one warp per leaf
+      const char* e = getenv("SPERM_PREP16");
+      return e ? atoi(e) : 1;
+    }();
+    const int W = (n <= 16 && prep16) ? 16 : 32;
+    const int64_t threads = count * W;
     count_launch();
-    const size_t prep_smem = (size_t)8 * n * (n + 1) * sizeof(int32_t);  // padded rows, 8 warps
-    const int per_lane = (n * n + 31) / 32;
-    auto prep = n > 32 ? rnw_prep_kernel<unsigned long long, 16>
-              : per_lane <= 4 ? rnw_prep_kernel<uint32_t, 4> : per_lane <= 8 ? rnw_prep_kernel<uint32_t, 8>
-              : per_lane <= 12 ? rnw_prep_kernel<uint32_t, 12> : rnw_prep_kernel<uint32_t, 16>;
+    const size_t prep_smem = (size_t)(256 / W) * n * (n + 1) * sizeof(int32_t);  // padded rows per segment
+    const int per_lane = (n * n + W - 1) / W;
+    auto prep = n > 32 ? rnw_prep_kernel<unsigned long long, 16, 32>
+              : W == 16 ? (per_lane <= 8 ? rnw_prep_kernel<uint32_t, 8, 16> : rnw_prep_kernel<uint32_t, 16, 16>)
+              : per_lane <= 4 ? rnw_prep_kernel<uint32_t, 4, 32> : per_lane <= 8 ? rnw_prep_kernel<uint32_t, 8, 32>
+              : per_lane <= 12 ? rnw_prep_kernel<uint32_t, 12, 32> : rnw_prep_kernel<uint32_t, 16, 32>;
     {  // the attribute once per device, for the largest order (host time per call)
       static std::atomic<unsigned> prep_attr{0};
       int dev = 0;
@@ -1718,11 +1743,12 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       const unsigned bit = 1u << (dev & 31);
       if (!(prep_attr.load() & bit)) {
         const int max_smem = 8 * SPERM_NMAX * (SPERM_NMAX + 1) * (int)sizeof(int32_t);
-        for (auto kf : {rnw_prep_kernel<uint32_t, 4>, rnw_prep_kernel<uint32_t, 8>, rnw_prep_kernel<uint32_t, 12>,
-                        rnw_prep_kernel<uint32_t, 16>})
+        for (auto kf : {rnw_prep_kernel<uint32_t, 4, 32>, rnw_prep_kernel<uint32_t, 8, 32>,
+                        rnw_prep_kernel<uint32_t, 12, 32>, rnw_prep_kernel<uint32_t, 16, 32>,
+                        rnw_prep_kernel<uint32_t, 8, 16>, rnw_prep_kernel<uint32_t, 16, 16>})
           SPERM_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<unsigned long long, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       max_smem));
+        SPERM_TRY(cudaFuncSetAttribute(rnw_prep_kernel<unsigned long long, 16, 32>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
         prep_attr.fetch_or(bit);
       }
     }
