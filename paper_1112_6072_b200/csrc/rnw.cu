@@ -105,6 +105,9 @@ constexpr int kMaxLow = 8;  // low columns picked per leaf
 #ifndef SPERM_RNW_BLOCK_UNROLL  // measured (configs[1] kernel ms/step): 1: 0.160, 2: 0.151, 3: 0.150,
 #define SPERM_RNW_BLOCK_UNROLL 4  // 4: 0.146, 8: 0.151 (more independent chains in flight per warp)
 #endif
+#ifndef SPERM_RNW_EMODE_NRT  // 3-CTA tree plans with at most this many register rows also get
+#define SPERM_RNW_EMODE_NRT 16  // block loops specialised per E mode (B = 4, NFIX = 4: C100's leaves)
+#endif
 #ifndef SPERM_RNW_EFORM  // E_c = Q_c^0 - Q_c^1 evaluation: 0 products of sums, 1 / 2 multiply-add form
 #define SPERM_RNW_EFORM 2  // (configs[1] kernel 0.147 / 0.147 / 0.144 ms)
 #endif
@@ -868,7 +871,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     // (the mode-specialised loops triple the code; only the unrolled 2-CTA variants (<= 28 register
     // rows) get them — specialised, several 3-CTA and wide variants spilled)
     auto by_mode = [&](auto kc) {
-      if constexpr (UNR > 1) {  // the 2-CTA variants with <= 28 register rows
+      if constexpr (UNR > 1 || NRT <= SPERM_RNW_EMODE_NRT) {  // unrolled 2-CTA variants, small plans
         if (emode == 2) blocks(kc, std::integral_constant<int, 2>{});  // warp-uniform per leaf
         else if (emode == 1) blocks(kc, std::integral_constant<int, 1>{});
         else blocks(kc, std::integral_constant<int, 0>{});
