@@ -930,6 +930,18 @@ struct FinTable {
   uint32_t f[SPERM_KMAX][kMaxMexp];
 };
 
+// v mod p for any 64-bit v and an odd p < 2^31: the quotient is estimated in fp64 (v and 1/p
+// each rounded to 53 bits, the product truncated: within 3 * 2^-19 of v / p, so off by at most
+// one) and the remainder corrected exactly in 64-bit wrap-around arithmetic (it lies in (-p, 2p))
+// — instead of a 64-bit integer division per residue.
+__device__ __forceinline__ uint32_t mod_u64(uint64_t v, uint32_t p, double ip) {
+  const uint64_t qe = (uint64_t)__dmul_rz(__ull2double_rn(v), ip);
+  int64_t r = (int64_t)(v - qe * (uint64_t)p);
+  if (r < 0) r += p;
+  else if (r >= (int64_t)p) r -= p;
+  return (uint32_t)r;
+}
+
 // Leaf residues per = f[q][mexp] S mod p_q, times the leaf coefficient; accumulated into the job
 // rows and the total row.  A grid-stride kernel: 32 leaves per block iteration, each (job, q)
 // run of equal jobs added with one atomic.
@@ -944,7 +956,15 @@ __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
   __shared__ int32_t s_job[kFinThreads / SPERM_KMAX];
   __syncthreads();
   const int q = threadIdx.x % SPERM_KMAX, li = threadIdx.x / SPERM_KMAX;
-  const uint64_t pq = (uint64_t)c_p[q];
+  const uint32_t pq = (uint32_t)c_p[q];
+  const double iq = 1.0 / (double)pq;
+  const uint32_t p0 = (uint32_t)c_p[0], p1 = (uint32_t)c_p[1];
+  const double i0 = 1.0 / (double)p0, i1 = 1.0 / (double)p1;
+  // signed v mod p in [0, p)
+  auto smod = [](int64_t v, uint32_t p, double ip) -> uint32_t {
+    const uint32_t r = mod_u64(v < 0 ? 0ull - (uint64_t)v : (uint64_t)v, p, ip);
+    return (v < 0 && r) ? p - r : r;
+  };
   for (int64_t base = (int64_t)blockIdx.x * kFinThreads; base < count * SPERM_KMAX;
        base += (int64_t)gridDim.x * kFinThreads) {
     const int64_t idx = base + threadIdx.x;
@@ -958,35 +978,31 @@ __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
       if (q == 0 && leaf_k) leaf_k[leaf] = keff;
       jb = job ? job[leaf] : 0;
       const int64_t cf = coef ? coef[leaf] : 1;
+      // coef * f[qq][mexp] * S mod p_qq (S = the leaf's accumulated sum)
+      auto res = [&](int qq, uint32_t pp, double ip) -> uint32_t {
+        const uint32_t v = n == 0 ? 1u
+                                  : mod_u64((uint64_t)mod_u64(leaf_acc[leaf * SPERM_KMAX + qq], pp, ip) * s_f[qq][mt.y],
+                                            pp, ip);
+        return mod_u64((uint64_t)v * smod(cf, pp, ip), pp, ip);
+      };
       if (q < k) {
-        val = n == 0 ? 1 : (leaf_acc[leaf * SPERM_KMAX + q] % pq) * s_f[q][mt.y] % pq;
-        int64_t cm = cf % (int64_t)pq;
-        if (cm < 0) cm += (int64_t)pq;
-        val = val * (uint64_t)cm % pq;
+        val = res(q, pq, iq);
       } else if (q < keff) {
         // lifted leaf (prep: 2 |coef| * bound < p_0 [p_1]): its exact value V is the symmetric
         // residue mod p_0, or Garner's combination of the residues mod p_0 and p_1, and V mod p_q
         // is the residue the leaf contributes here
-        auto res = [&](int qq) {
-          const uint64_t pp = (uint64_t)c_p[qq];
-          uint64_t v = n == 0 ? 1 : (leaf_acc[leaf * SPERM_KMAX + qq] % pp) * s_f[qq][mt.y] % pp;
-          int64_t cm = cf % (int64_t)pp;
-          if (cm < 0) cm += (int64_t)pp;
-          return v * (uint64_t)cm % pp;
-        };
-        const uint64_t p0 = (uint64_t)c_p[0], p1 = (uint64_t)c_p[1];
-        const uint64_t r0 = res(0);
+        const uint32_t r0 = res(0, p0, i0);
         int64_t V;
         if (k == 1) {
           V = r0 > p0 / 2 ? (int64_t)r0 - (int64_t)p0 : (int64_t)r0;
         } else {
-          const uint64_t r1 = res(1);
-          const uint64_t t = (r1 + p1 - r0 % p1) % p1 * kInvP0ModP1 % p1;
-          const uint64_t u = r0 + p0 * t, m01 = p0 * p1;  // < p0 p1 < 2^62
+          const uint32_t r1 = res(1, p1, i1);
+          const uint32_t t = mod_u64((uint64_t)mod_u64((uint64_t)r1 + p1 - mod_u64(r0, p1, i1), p1, i1) * kInvP0ModP1,
+                                     p1, i1);
+          const uint64_t u = r0 + (uint64_t)p0 * t, m01 = (uint64_t)p0 * p1;  // < p0 p1 < 2^62
           V = u > m01 / 2 ? (int64_t)u - (int64_t)m01 : (int64_t)u;
         }
-        int64_t r = V % (int64_t)pq;
-        val = (uint64_t)(r < 0 ? r + (int64_t)pq : r);
+        val = smod(V, pq, iq);
       }
       if (leaf_res) leaf_res[idx] = (uint32_t)val;
     }
