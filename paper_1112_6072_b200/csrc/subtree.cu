@@ -63,10 +63,9 @@ struct FKid {
 };
 
 // frame entry (physical row fr, physical column fc) of the view: M[fr][fc] for a row pivot,
-// M[fc][fr] for a column pivot (frame rows are the node's columns)
-__device__ __forceinline__ int32_t fat(const int32_t* M, int S, bool colpiv, int fr, int fc) {
-  return colpiv ? M[fc * S + fr] : M[fr * S + fc];
-}
+// M[fc][fr] for a column pivot (frame rows are the node's columns) = M[fr * ra + fc * ca] with the
+// frame strides ra = colpiv ? 1 : S, ca = colpiv ? S : 1 — the kernel keeps fr * ra and fc * ca
+// (scaled indices) so that an access is one add
 
 __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
     const int32_t* __restrict__ mats, const int64_t* __restrict__ coef, const int32_t* __restrict__ job, int n0,
@@ -125,19 +124,20 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
     auto apply = [&](bool colpiv, int r, const FKid& k) {
       const int FR = colpiv ? cid : rid, FC = colpiv ? rid : cid;
       if (!k.minor) {
+        const int ra = colpiv ? 1 : S, ca = colpiv ? S : 1;
         const int pk = __shfl_sync(kFull, FC, k.ka), pb = __shfl_sync(kFull, FC, k.kb);
+        const int pkA = pk * ca, pbA = pb * ca;
         if (nfr > 0) {  // log the whole physical line pk (n0 values) before overwriting it
           int32_t* u = ulog + nlog * kUndoW;
-          if (lane < n0) u[1 + lane] = fat(M, S, colpiv, lane, pk);
+          if (lane < n0) u[1 + lane] = M[lane * ra + pkA];
           if (lane == 0) u[0] = colpiv ? (pk | 0x100) : pk;
           ++nlog;
           __syncwarp();  // every lane has read its logged entry before the line is overwritten
         }
         if (lane < n) {
-          const int32_t x = fat(M, S, colpiv, FR, pk), y = fat(M, S, colpiv, FR, pb);
-          const int32_t v = (int32_t)((uint32_t)k.al * (uint32_t)y + (uint32_t)k.be * (uint32_t)x);
-          if (colpiv) M[pk * S + FR] = v;
-          else M[FR * S + pk] = v;
+          const int frA = FR * ra;
+          const int32_t x = M[frA + pkA], y = M[frA + pbA];
+          M[frA + pkA] = (int32_t)((uint32_t)k.al * (uint32_t)y + (uint32_t)k.be * (uint32_t)x);
         }
       }
       // delete frame row r and frame column kb: lane ii takes the map entry ii + (ii >= r)
@@ -156,11 +156,21 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
         slot = __shfl_sync(kFull, slot, 0);
         if ((int64_t)slot < cap_out) {
           int32_t* o = out_mats + (int64_t)slot * L * L;
-          for (int b = 0; b < L * L; b += 32) {
-            const int e = b + lane;
-            const int i = (int)__umulhi((uint32_t)e, magicL), j = e - i * L;
-            const int pr = __shfl_sync(kFull, rid, i & 31), pc = __shfl_sync(kFull, cid, j & 31);
-            if (e < L * L) o[e] = M[pr * S + pc];
+          if (L <= 16) {  // two rows per step: half-warp h writes row 2t + h, lane j of it column j
+            const int h = lane >> 4, j = lane & 15;
+            const int pc = __shfl_sync(kFull, cid, j);
+            for (int i0 = 0; i0 < L; i0 += 2) {
+              const int i = i0 + h;
+              const int pr = __shfl_sync(kFull, rid, i & 31);
+              if (i < L && j < L) o[i * L + j] = M[pr * S + pc];
+            }
+          } else {
+            for (int b = 0; b < L * L; b += 32) {
+              const int e = b + lane;
+              const int i = (int)__umulhi((uint32_t)e, magicL), j = e - i * L;
+              const int pr = __shfl_sync(kFull, rid, i & 31), pc = __shfl_sync(kFull, cid, j & 31);
+              if (e < L * L) o[e] = M[pr * S + pc];
+            }
           }
           if (lane == 0) {
             out_coef[slot] = cf;
@@ -202,9 +212,10 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
         } else {
           const int FR = colpiv ? cid : rid, FC = colpiv ? rid : cid;
           const int frc = colpiv ? cc : rc, fcc = colpiv ? rc : cc;  // frame line counts
-          const int FRr = __shfl_sync(kFull, FR, r);                 // the pivot line, physical
+          const int frA = FR * (colpiv ? 1 : S), fcA = FC * (colpiv ? S : 1);  // scaled (see above)
+          const int FRrA = __shfl_sync(kFull, frA, r);                           // the pivot line
           // the pivot line's nonzeros p0 < p1 < ... and their values (Eq. (2)'s a, b, c, d)
-          const int32_t pv = lane < n ? fat(M, S, colpiv, FRr, FC) : 0;
+          const int32_t pv = lane < n ? M[FRrA + fcA] : 0;
           unsigned pm = __ballot_sync(kFull, pv != 0);
           int p[4];
 #pragma unroll
@@ -242,12 +253,12 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
           for (int c = 0; c < 2; ++c) {
             if (c >= nk) break;
             const FKid k = kid[c];
-            const int pkb = __shfl_sync(kFull, FC, k.kb);
+            const int pkbA = __shfl_sync(kFull, fcA, k.kb);
             int nrc = 1, ncc = 1;  // frame counts of row `lane` / column `lane` in the child
             bool mnz = false;
             if (k.minor) {
               if (lane < n) {
-                nrc = frc - (fat(M, S, colpiv, FR, pkb) != 0);
+                nrc = frc - (M[frA + pkbA] != 0);
                 ncc = fcc - (pv != 0);  // pv = frame (r, lane)
               }
               const int32_t pvk = c == 0 ? v[0] : v[2];
@@ -255,9 +266,9 @@ __global__ void __launch_bounds__(32 * kSubWarps) subtree_kernel(
               if (prod > (__int128)INT64_MAX || prod < (__int128)INT64_MIN) ovf = true;
               kcf[c] = (int64_t)prod;
             } else {
-              const int pka = __shfl_sync(kFull, FC, k.ka);
+              const int pkaA = __shfl_sync(kFull, fcA, k.ka);
               if (lane < n && lane != r) {
-                const int32_t va = fat(M, S, colpiv, FR, pka), vb = fat(M, S, colpiv, FR, pkb);
+                const int32_t va = M[frA + pkaA], vb = M[frA + pkbA];
                 const long long mv = (long long)k.al * vb + (long long)k.be * va;
                 if (mv > INT32_MAX || mv < INT32_MIN) ovf = true;
                 mnz = mv != 0;
