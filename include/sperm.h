@@ -274,13 +274,22 @@ int sperm_expand_stats(double* h_bytes, double* h_nodes, int reset);
  * (PAPER.md:218-220): E[X] = per(pattern).  Randomness is the counter-based
  * generator of DESIGN.md reading K1 keyed by (seed, d_ids[m] or m, trial, i, j);
  * det by complex LU with partial pivoting in IEEE fp64 without contraction
- * (reading K2), so estimates are reproducible bit for bit.
+ * (reading K2), so estimates are reproducible bit for bit.  Orders >= 48 run a
+ * frontal LU (one warp per trial over the rows and columns pivoting can still change; the
+ * same operations per entry) and re-run jobs that overflow its front in a CTA-per-trial LU;
+ * the call then synchronizes once (the overflow flags are read back).
  *  d_mats    [count][n][n] int32 (device); d_ids [count] int32 or NULL.
  *  d_est     [count] double out (device).
  *  d_trials_out [count][trials] double out (device) or NULL: every X.  */
 int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d_ids,
                    int trials, uint64_t seed, double* d_est, double* d_trials_out,
                    void* stream);
+
+
+/* Jobs that went through sperm_estimate's frontal warp-per-trial kernel (orders >= 48) since the
+ * last reset, and how many of them it handed to the CTA kernel (front > 24 rows, window > 64
+ * columns, or a row with > 12 nonzeros).  Host; reset != 0 clears the counters after reading. */
+int sperm_estimate_stats(double* h_jobs, double* h_redo, int reset);
 
 /* ---------------------------------------------------------------- schedule */
 /* sperm_schedule — the improved Step 3 and LPT

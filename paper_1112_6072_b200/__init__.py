@@ -9,6 +9,6 @@ libsperm.so (csrc/, C ABI in include/sperm.h) holds the sm_100a kernels:
 `sperm` is the thin ctypes binding; `pipeline` sequences the calls (Algorithm PH).
 """
 from .sperm import (  # noqa: F401
-    KMAX, NMAX, DeviceQueue, SpermError, lib, primes, residues_to_ints, residues_to_ints_device, sperm_bound_primes, sperm_crt, sperm_estimate, sperm_expand, sperm_expand_stats, sperm_expand_subtree, sperm_expand_subtree_stats, sperm_fold_mod, sperm_kendall_tau, sperm_launch_count, sperm_list_schedule, replay_efficiency, sperm_interpolate_mod, sperm_nnz, tau_z,
+    KMAX, NMAX, DeviceQueue, SpermError, lib, primes, residues_to_ints, residues_to_ints_device, sperm_bound_primes, sperm_crt, sperm_estimate, sperm_estimate_stats, sperm_expand, sperm_expand_stats, sperm_expand_subtree, sperm_expand_subtree_stats, sperm_fold_mod, sperm_kendall_tau, sperm_launch_count, sperm_list_schedule, replay_efficiency, sperm_interpolate_mod, sperm_nnz, tau_z,
     sperm_permanent, sperm_permanent_host, sperm_prime, sperm_reduce_mod, sperm_rnw_stats, sperm_rnw_terms, sperm_schedule, sperm_timing_enable,
     sperm_timing_get, sperm_timing_reset, sperm_version)

@@ -11,7 +11,10 @@
 //           div_by; K2), so the value equals the reference evaluation bit for bit.
 // The estimate is the trial-order sum of X divided by N (K3).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -322,6 +325,240 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
   }
 }
 
+// ---------------------------------------------------------------------------- frontal kernel
+// One WARP per trial for the sparse job matrices (round 2).  Partial pivoting keeps the fill of a
+// sparse matrix near the diagonal, so at step k only a FRONT of rows (not yet eliminated, first
+// original nonzero column <= k: every other row is still zero in columns <= k) and a WINDOW of
+// columns k..E (E = the largest last-nonzero column of a pivot row so far: every column right
+// of it is untouched) can change.  The front (<= kFrR rows, one lane each) is kept in shared
+// memory over a circular window of kFrC columns; a row entering the front, and a column entering
+// the window, is initialised from the job matrix and the trial's roots (counter-based, so any
+// entry can be regenerated).  Every update is the oracle's operation on the same entry in the same
+// order (a skipped entry b - l u has l = 0 or u = 0: b up to the sign of a zero, see above), the
+// multipliers the same correctly rounded quotients, and the pivot the first maximal |b_ik|^2 by
+// POSITION — each row's position under the oracle's physical row swaps is tracked (rowAt/posOf)
+// — so X is bit-identical to the oracle's.  A job whose front or window overflows (or whose rows
+// have more than kNzRow nonzeros) is flagged and re-run by the CTA kernel above.
+constexpr int kFrR = 24;    // front rows (lanes 0..23)
+constexpr int kFrC = 64;    // window columns (circular, power of two)
+constexpr int kNzRow = 12;  // original nonzeros per row in the row table
+constexpr int kRowTab = 2 + kNzRow;
+
+// per job and row: first nonzero column, nonzero count, the nonzero columns ascending (int8);
+// over[job] = 1 if a row has more than kNzRow nonzeros.  One warp per job.
+__global__ void kklll_rowtab_kernel(const int32_t* __restrict__ mats, int n, int64_t count, int8_t* __restrict__ tab,
+                                    int* __restrict__ over) {
+  const int lane = threadIdx.x & 31;
+  const int64_t job = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (job >= count) return;
+  const int32_t* a = mats + job * (int64_t)n * n;
+  int8_t* t = tab + job * (int64_t)n * kRowTab;
+  bool bad = false;
+  for (int i = lane; i < n; i += 32) {
+    int c = 0, first = n;
+    for (int j = 0; j < n; ++j)
+      if (a[i * n + j] != 0) {
+        if (c < kNzRow) t[i * kRowTab + 2 + c] = (int8_t)j;
+        first = min(first, j);
+        ++c;
+      }
+    if (c > kNzRow) bad = true;
+    t[i * kRowTab] = (int8_t)first;
+    t[i * kRowTab + 1] = (int8_t)min(c, kNzRow);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) over[job] = 1;
+}
+
+__global__ void __launch_bounds__(32) kklll_front_kernel(int n, int64_t count, const int32_t* __restrict__ ids,
+                                                           int trials, uint64_t seed, const int8_t* __restrict__ tab,
+                                                           double* __restrict__ xout, int* __restrict__ over) {
+  // F[kFrR][kFrC] | rowAt[128] posOf[128] | the current job's row table [n][kRowTab] (int8)
+  extern __shared__ double2 fsm[];
+  double2* F = fsm;
+  int8_t* rowAt = reinterpret_cast<int8_t*>(fsm + kFrR * kFrC);
+  int8_t* posOf = rowAt + 128;
+  int8_t* rts = posOf + 128;
+  const int lane = threadIdx.x;
+  const double S32 = 0.8660254037844386;
+  const int64_t items = count * (int64_t)trials;
+  int64_t cached = -1;
+  int fz[4];  // first nonzero column of rows lane, lane + 32, lane + 64, lane + 96
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t job = item / trials;
+    const int trial = (int)(item % trials);
+    if (over[job]) continue;  // the CTA kernel recomputes the job
+    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
+    __syncwarp();
+    if (job != cached) {  // the job's row table into shared memory (trials of a job follow each other)
+      const int8_t* rt = tab + job * (int64_t)n * kRowTab;
+      for (int e = lane; e < n * kRowTab; e += 32) rts[e] = rt[e];
+      cached = job;
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 4; ++t) fz[t] = lane + 32 * t < n ? rts[(lane + 32 * t) * kRowTab] : 127;
+    }
+    for (int i = lane; i < n; i += 32) {
+      rowAt[i] = (int8_t)i;
+      posOf[i] = (int8_t)i;
+    }
+    __syncwarp();
+    // the lane's front row: original index (-1: free slot) and current position
+    int myrow = -1, mypos = 0;
+    unsigned freem = (1u << kFrR) - 1u;  // free slots (warp-uniform)
+    double2* my = F + min(lane, kFrR - 1) * kFrC;  // lanes >= kFrR never own a row (reads only)
+    int E = -1;         // window right edge
+    bool fail = false;  // front or window overflow
+    // the lane's row over window columns lo..hi: zeros, then its original nonzeros (Step 1 of KKLLL:
+    // the trial's cube roots, regenerated from the counter-based generator)
+    auto init_cols = [&](int lo, int hi) {
+      if (myrow < 0 || lo > hi) return;
+      for (int j = lo; j <= hi; ++j) my[j & (kFrC - 1)] = make_double2(0.0, 0.0);
+      const int8_t* r = rts + myrow * kRowTab;
+      const int c = r[1];
+      for (int t = 0; t < c; ++t) {
+        const int j = r[2 + t];
+        if (j >= lo && j <= hi) {
+          const int ri = root_index(key, (uint64_t)myrow, (uint64_t)j);
+          my[j & (kFrC - 1)] = make_double2(ri == 0 ? 1.0 : -0.5, ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32));
+        }
+      }
+    };
+    double x = 1.0;
+    for (int k = 0; k < n; ++k) {
+      // window covers column k (columns E+1..k enter: original values of the front rows)
+      if (E < k) {
+        init_cols(E + 1, k);
+        E = k;
+      }
+      // rows whose first nonzero is column k enter the front
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (32 * t >= n) break;
+        unsigned ent = __ballot_sync(0xffffffffu, fz[t] == k);
+        while (ent) {
+          const int row = 32 * t + __ffs(ent) - 1;
+          ent &= ent - 1;
+          if (!freem) {
+            fail = true;
+            break;
+          }
+          const int slot = __ffs(freem) - 1;
+          freem &= freem - 1;
+          if (lane == slot) {
+            myrow = row;
+            mypos = posOf[row];
+            init_cols(k, E);
+          }
+        }
+      }
+      if (fail) break;
+      __syncwarp();
+      // pivot: first maximal |b_ik|^2 by position over the front (a nonnegative double orders
+      // like its bit pattern: two 32-bit REDUX, then the minimal position)
+      const double2 bk = myrow >= 0 ? my[k & (kFrC - 1)] : make_double2(0.0, 0.0);
+      const double mag = myrow >= 0 ? __dadd_rn(__dmul_rn(bk.x, bk.x), __dmul_rn(bk.y, bk.y)) : 0.0;
+      const unsigned mh = myrow >= 0 ? (unsigned)__double2hiint(mag) : 0u;
+      const unsigned ml = myrow >= 0 ? (unsigned)__double2loint(mag) : 0u;
+      const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
+      const bool c1 = myrow >= 0 && mh == bh;
+      const unsigned bl_ = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
+      const bool c2 = c1 && ml == bl_;
+      const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)mypos : 0xffffffffu);
+      const int ps = __ffs(__ballot_sync(0xffffffffu, c2 && mypos == bp)) - 1;  // pivot lane
+      const double d = __hiloint2double((int)bh, (int)bl_);
+      if (d == 0.0 || ps < 0) {
+        x = 0.0;
+        break;
+      }
+      x = __dmul_rn(x, d);
+      if (k + 1 == n) break;
+      const int prow = __shfl_sync(0xffffffffu, myrow, ps);
+      const double2* pr = F + ps * kFrC;
+      // the pivot row's last nonzero: an original nonzero right of the window extends it
+      {
+        const int8_t* r = rts + prow * kRowTab;
+        const int c = r[1];
+        const int cl = c > 0 ? r[2 + c - 1] : -1;
+        if (cl > E) {
+          if (cl - k + 1 > kFrC) {
+            fail = true;
+            break;
+          }
+          init_cols(E + 1, cl);
+          E = cl;
+          __syncwarp();
+        }
+      }
+      // the pivot row's nonzero columns k+1..E as a bit mask of offsets j - k - 1 (< 63)
+      unsigned long long um = 0;
+      for (int j0 = k + 1; j0 <= E; j0 += 32) {
+        const int j = j0 + lane;
+        bool nz = false;
+        if (j <= E) {
+          const double2 u = pr[j & (kFrC - 1)];
+          nz = u.x != 0.0 || u.y != 0.0;
+        }
+        um |= (unsigned long long)__ballot_sync(0xffffffffu, nz) << (j0 - k - 1);
+      }
+      // multipliers l_i = b_ik conj(b_kk) / |b_kk|^2 (one reciprocal + Markstein, as above), then
+      // the update of the pivot row's nonzero columns, four independent columns per step
+      const double2 pk = pr[k & (kFrC - 1)];
+      double2 l = make_double2(0.0, 0.0);
+      const bool act = myrow >= 0 && lane != ps && (bk.x != 0.0 || bk.y != 0.0);
+      if (act) {
+        const double y = __drcp_rn(d);
+        const bool d_ok = div_range_ok(d);
+        l = make_double2(div_by(__dadd_rn(__dmul_rn(bk.x, pk.x), __dmul_rn(bk.y, pk.y)), d, y, d_ok),
+                         div_by(__dsub_rn(__dmul_rn(bk.y, pk.x), __dmul_rn(bk.x, pk.y)), d, y, d_ok));
+      }
+      while (um) {
+        int jj[4];
+        bool ok[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          ok[t] = um != 0;
+          jj[t] = ok[t] ? (k + 1 + __ffsll((long long)um) - 1) & (kFrC - 1) : 0;
+          um &= um - 1;
+        }
+        double2 u[4], v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          u[t] = pr[jj[t]];
+          v[t] = my[jj[t]];
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          if (act && ok[t]) {
+            v[t].x = __dsub_rn(v[t].x, __dsub_rn(__dmul_rn(l.x, u[t].x), __dmul_rn(l.y, u[t].y)));
+            v[t].y = __dsub_rn(v[t].y, __dadd_rn(__dmul_rn(l.x, u[t].y), __dmul_rn(l.y, u[t].x)));
+            my[jj[t]] = v[t];
+          }
+        }
+      }
+      // the oracle's row exchange: the row at position k moves to the pivot's position
+      const int pp = __shfl_sync(0xffffffffu, mypos, ps);
+      const int rk = rowAt[k];
+      __syncwarp();
+      if (lane == 0) {
+        rowAt[pp] = (int8_t)rk;
+        posOf[rk] = (int8_t)pp;
+        rowAt[k] = (int8_t)prow;
+        posOf[prow] = (int8_t)k;
+      }
+      if (myrow == rk) mypos = pp;
+      // the pivot row leaves the front
+      if (lane == ps) myrow = -1;
+      freem |= 1u << ps;
+      __syncwarp();
+    }
+    if (fail) {
+      if (lane == 0) over[job] = 1;
+    } else if (lane == 0) {
+      xout[item] = x;
+    }
+  }
+}
+
 __global__ void kklll_mean_kernel(const double* __restrict__ xs, int64_t count, int trials,
                                   double* __restrict__ est) {
   const int64_t job = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -336,6 +573,18 @@ __global__ void kklll_mean_kernel(const double* __restrict__ xs, int64_t count, 
 }  // namespace sperm
 
 using namespace sperm;
+
+static std::mutex g_front_mu;
+static double g_front_jobs = 0.0, g_front_redo = 0.0;
+
+// jobs estimated through the frontal kernel path and jobs it handed to the CTA kernel (overflow)
+extern "C" int sperm_estimate_stats(double* h_jobs, double* h_redo, int reset) {
+  std::lock_guard<std::mutex> lk(g_front_mu);
+  if (h_jobs) *h_jobs = g_front_jobs;
+  if (h_redo) *h_redo = g_front_redo;
+  if (reset) g_front_jobs = g_front_redo = 0.0;
+  return SPERM_OK;
+}
 
 extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const int32_t* d_ids, int trials,
                               uint64_t seed, double* d_est, double* d_trials_out, void* stream) {
@@ -365,34 +614,116 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     count_launch();
     kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else {
-    // shared-memory-resident LU, one 256-thread CTA per trial, as many trials per SM as fit
-    // (measured on the fullerene-96 jobs: 128 threads 1.37 s, 256 1.31 s, 512 1.97 s)
-    // (128-thread CTAs below order SPERM_KKLLL_T128_MAX: more trials per SM, cheaper barriers)
-    // (measured, 128 vs 256 threads: C60 jobs, order 32: 44.5 vs 75.1 ms; fullerene-96, order 67:
-    // 1287 vs 1080 ms; C100, order 72: 2595 vs 1919 ms — bit-identical trials either way)
-    static const int t128_max = [] {
-      const char* e = getenv("SPERM_KKLLL_T128_MAX");
-      return e ? atoi(e) : 48;
+    // shared-memory-resident LU, one CTA per trial (smem_kernel on jobs [j0, j0 + cnt) of the
+    // given matrices / ids, trials written to out)
+    auto run_smem = [&](const int32_t* mats, int64_t cnt, const int32_t* idsp, double* out) -> int {
+      // (measured on the fullerene-96 jobs: 128 threads 1.37 s, 256 1.31 s, 512 1.97 s)
+      // (128-thread CTAs below order SPERM_KKLLL_T128_MAX: more trials per SM, cheaper barriers)
+      // (measured, 128 vs 256 threads: C60 jobs, order 32: 44.5 vs 75.1 ms; fullerene-96, order 67:
+      // 1287 vs 1080 ms; C100, order 72: 2595 vs 1919 ms — bit-identical trials either way)
+      static const int t128_max = [] {
+        const char* e = getenv("SPERM_KKLLL_T128_MAX");
+        return e ? atoi(e) : 48;
+      }();
+      static const int t64_max = [] {  // 64-thread CTAs below this order (C60 jobs: 39.8 vs 44.5 ms)
+        const char* e = getenv("SPERM_KKLLL_T64_MAX");
+        return e ? atoi(e) : 40;
+      }();
+      const int nt = n < t64_max ? 64 : n < t128_max ? 128 : 256;
+      auto kern = nt == 64 ? kklll_smem_kernel<64> : nt == 128 ? kklll_smem_kernel<128> : kklll_smem_kernel<256>;
+      const size_t smem = sizeof(double2) * ((size_t)n * (n | 1) + n);
+      SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0;
+      SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
+      const int64_t it = cnt * (int64_t)trials;
+      int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+      grid = std::max<int64_t>(1, std::min(grid, it));
+      static const int band = [] {  // A-B knob: SPERM_KKLLL_BAND=0 updates the whole trailing block
+        const char* e = getenv("SPERM_KKLLL_BAND");
+        return e ? atoi(e) : 1;
+      }();
+      count_launch();
+      kern<<<(unsigned)grid, nt, smem, st>>>(mats, n, cnt, idsp, trials, seed, out, band);
+      SPERM_LAUNCH_CHECK("kklll_smem_kernel");
+      return SPERM_OK;
+    };
+    static const int front_min = [] {  // A-B knob: smallest order for the frontal kernel
+      const char* e = getenv("SPERM_KKLLL_FRONT_MIN");  // (measured: C60 jobs, order 32: 68 ms frontal
+      return e ? atoi(e) : 48;  // vs 32 ms CTA; C100 order 79: 254 vs 377 ms; fullerene-96 order 67: 764 vs 904)
     }();
-    static const int t64_max = [] {  // 64-thread CTAs below this order (C60 jobs: 39.8 vs 44.5 ms)
-      const char* e = getenv("SPERM_KKLLL_T64_MAX");
-      return e ? atoi(e) : 40;
-    }();
-    const int nt = n < t64_max ? 64 : n < t128_max ? 128 : 256;
-    auto kern = nt == 64 ? kklll_smem_kernel<64> : nt == 128 ? kklll_smem_kernel<128> : kklll_smem_kernel<256>;
-    const size_t smem = sizeof(double2) * ((size_t)n * (n | 1) + n);
-    SPERM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
-    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
-    grid = std::max<int64_t>(1, std::min(grid, items));
     TimingScope ts("kklll", st);
-    count_launch();
-    static const int band = [] {  // A-B knob: SPERM_KKLLL_BAND=0 updates the whole trailing block
-      const char* e = getenv("SPERM_KKLLL_BAND");
-      return e ? atoi(e) : 1;
-    }();
-    kern<<<(unsigned)grid, nt, smem, st>>>(d_mats, n, count, d_ids, trials, seed, xs, band);
+    if (n < front_min) {
+      const int rc = run_smem(d_mats, count, d_ids, xs);
+      if (rc != SPERM_OK) return rc;
+    } else {
+      // frontal warp-per-trial kernel; jobs it flags (front / window / row-table overflow) are
+      // re-run by the CTA kernel
+      int8_t* tab = nullptr;
+      int* over = nullptr;
+      SPERM_CUDA(cudaMallocAsync((void**)&tab, (size_t)count * n * kRowTab, st));
+      SPERM_CUDA(cudaMallocAsync((void**)&over, sizeof(int) * count, st));
+      SPERM_CUDA(cudaMemsetAsync(over, 0, sizeof(int) * count, st));
+      count_launch();
+      kklll_rowtab_kernel<<<(unsigned)((count * 32 + 127) / 128), 128, 0, st>>>(d_mats, n, count, tab, over);
+      SPERM_LAUNCH_CHECK("kklll_rowtab_kernel");
+      const size_t fsmem = sizeof(double2) * kFrR * kFrC + 256 + (size_t)kKNmax * kRowTab;
+      static std::atomic<unsigned> attr_done{0};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (!(attr_done.load() & (1u << (dev & 31)))) {
+        SPERM_CUDA(cudaFuncSetAttribute(kklll_front_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+        attr_done.fetch_or(1u << (dev & 31));
+      }
+      int per_sm = 0;
+      SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_front_kernel, 32, fsmem));
+      int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+      grid = std::max<int64_t>(1, std::min(grid, items));
+      count_launch();
+      kklll_front_kernel<<<(unsigned)grid, 32, fsmem, st>>>(n, count, d_ids, trials, seed, tab, xs, over);
+      SPERM_LAUNCH_CHECK("kklll_front_kernel");
+      std::vector<int> h_over((size_t)count);
+      SPERM_CUDA(cudaMemcpyAsync(h_over.data(), over, sizeof(int) * count, cudaMemcpyDeviceToHost, st));
+      cudaFreeAsync(tab, st);
+      cudaFreeAsync(over, st);
+      SPERM_CUDA(cudaStreamSynchronize(st));
+      std::vector<int64_t> redo;
+      for (int64_t j = 0; j < count; ++j)
+        if (h_over[j]) redo.push_back(j);
+      {
+        std::lock_guard<std::mutex> lk(g_front_mu);
+        g_front_jobs += (double)count;
+        g_front_redo += (double)redo.size();
+      }
+      if (!redo.empty()) {
+        // the flagged jobs, gathered, through the CTA kernel, scattered back
+        const int64_t r = (int64_t)redo.size();
+        int32_t* gm = nullptr;
+        int32_t* gi = nullptr;
+        double* gx = nullptr;
+        SPERM_CUDA(cudaMallocAsync((void**)&gm, sizeof(int32_t) * r * n * n, st));
+        SPERM_CUDA(cudaMallocAsync((void**)&gi, sizeof(int32_t) * r, st));
+        SPERM_CUDA(cudaMallocAsync((void**)&gx, sizeof(double) * r * trials, st));
+        std::vector<int32_t> h_ids((size_t)r);
+        for (int64_t t = 0; t < r; ++t) {
+          SPERM_CUDA(cudaMemcpyAsync(gm + t * n * n, d_mats + redo[t] * n * n, sizeof(int32_t) * n * n,
+                                     cudaMemcpyDeviceToDevice, st));
+          if (d_ids)
+            SPERM_CUDA(cudaMemcpyAsync(gi + t, d_ids + redo[t], sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+          else
+            h_ids[t] = (int32_t)redo[t];
+        }
+        if (!d_ids) SPERM_CUDA(cudaMemcpyAsync(gi, h_ids.data(), sizeof(int32_t) * r, cudaMemcpyHostToDevice, st));
+        const int rc = run_smem(gm, r, gi, gx);
+        if (rc != SPERM_OK) return rc;
+        for (int64_t t = 0; t < r; ++t)
+          SPERM_CUDA(cudaMemcpyAsync(xs + redo[t] * trials, gx + t * trials, sizeof(double) * trials,
+                                     cudaMemcpyDeviceToDevice, st));
+        SPERM_CUDA(cudaStreamSynchronize(st));  // h_ids is read by the copy above
+        cudaFreeAsync(gm, st);
+        cudaFreeAsync(gi, st);
+        cudaFreeAsync(gx, st);
+      }
+    }
   }
   cudaError_t le = cudaGetLastError();
   if (le == cudaSuccess) {

@@ -57,6 +57,7 @@ _SIGS = {
     "sperm_expand_subtree_stats": (_I, [_P, _P, _I]),
     "sperm_nnz": (_I, [_P, _I, _I64, _P, _P]),
     "sperm_estimate": (_I, [_P, _I, _I64, _P, _I, ctypes.c_uint64, _P, _P, _P]),
+    "sperm_estimate_stats": (_I, [_P, _P, _I]),
     "sperm_schedule": (_I, [_P, _I64, _I, _I, ctypes.c_uint64, _P, _P, _P]),
     "sperm_kendall_tau": (_I, [_P, _P, _I64, _P, _P]),
     "sperm_list_schedule": (_I, [_P, _P, _I64, _I, _P, _P]),
@@ -392,6 +393,13 @@ def sperm_estimate(mats, trials: int = 0, seed: int = 1, ids=None, keep_trials: 
     _check(lib().sperm_estimate(_ptr(mats), n, count, _ptr(ids), int(trials), int(seed) & (2**64 - 1),
                                 _ptr(est), _ptr(xs), _stream(stream)))
     return (est, xs) if keep_trials else est
+
+
+def sperm_estimate_stats(reset: bool = False):
+    """(jobs through the frontal KKLLL kernel, jobs it handed to the CTA kernel) since the last reset."""
+    a, b = ctypes.c_double(0), ctypes.c_double(0)
+    _check(lib().sperm_estimate_stats(ctypes.byref(a), ctypes.byref(b), 1 if reset else 0))
+    return a.value, b.value
 
 
 # --------------------------------------------------------------------- schedule

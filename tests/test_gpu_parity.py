@@ -345,6 +345,31 @@ def test_kklll_bit_exact_large_orders(n):
     assert (xs[1] == 0).all()
 
 
+def test_kklll_frontal_bit_exact_on_job_matrices():
+    """The frontal warp-per-trial kernel (orders >= 48) on whole-path job matrices (C60 jobs of
+    order 48, fullerene n=70 jobs of order 51): every trial bit-identical to the oracle, and the
+    frontal path (not the CTA fallback) handled the jobs; a dense matrix overflows the front and is
+    re-run by the CTA kernel, still exact."""
+    from workloads import random_fullerene
+    P.sperm_estimate_stats(reset=True)
+    for a, J, take, T in ((truncated_icosahedron(), 16, 3, 8), (random_fullerene(70, 2024, 1)[0], 80, 2, 6)):
+        jobs = pre_expand(a, jobs_at_least=J)
+        mats = np.array([to_dense(m, k) for _, m, k in jobs[:take]], dtype=np.int64)
+        assert mats.shape[1] >= 48
+        est, xs = P.sperm_estimate(dev(mats), trials=T, seed=9, keep_trials=True)
+        xs = xs.cpu().numpy()
+        for j in range(take):
+            ref = [kklll_trial(mats[j], 9, j, t) for t in range(T)]
+            assert np.array_equal(xs[j], np.array(ref)), j
+    jobs_front, redo = P.sperm_estimate_stats(reset=True)
+    assert jobs_front == 5 and redo == 0
+    rng = np.random.default_rng(2)
+    dense = (rng.random((1, 50, 50)) < 0.5).astype(np.int64)
+    est, xs = P.sperm_estimate(dev(dense), trials=4, seed=1, keep_trials=True)
+    assert np.array_equal(xs.cpu().numpy()[0], np.array([kklll_trial(dense[0], 1, 0, t) for t in range(4)]))
+    assert P.sperm_estimate_stats(reset=True) == (1.0, 1.0)
+
+
 def test_kklll_ids_and_default_trials():
     a = dodecahedron()
     est = P.sperm_estimate(dev(a[None]), trials=0, seed=3, ids=dev([5]))
