@@ -428,7 +428,7 @@ def choose_leaf_order(jobsets, order, num_jobs, k_total, nonneg, device, sample_
 
 def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order=20, trials: int = 0,
               seed: int = 1, policy: str = "estimate", batch_jobs: int = 4096, group=None,
-              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = 16 << 30,
+              device="cuda", measure_jobs: bool = False, leaf_budget_bytes: int = None,
               assignment: str = "static", store=None, dynamic_chunk: int = 0,
               fold_every: int = FOLD_EVERY, queue: str = "device") -> PHResult:
     """per(A) by Algorithm PH with the improved Step 3 on one or more GPUs.
@@ -449,6 +449,8 @@ def permanent(a, jobs_at_least: int = 1, job_order: int = 1, leaf_order=20, tria
     import torch
     import torch.distributed as dist
     rank, world = (dist.get_rank(group), dist.get_world_size(group)) if group is not None else (0, 1)
+    if leaf_budget_bytes is None:  # HBM budget of the streamed leaf sets (SPERM_LEAF_BUDGET_GB, default 16)
+        leaf_budget_bytes = int(float(_os.environ.get("SPERM_LEAF_BUDGET_GB", "16")) * (1 << 30))
     k_total = bound_primes(a)
     # nonnegative A: every leaf term is >= 0, so each job value and the total lie in
     # [0, per(A)] and k_total primes reconstruct all of them; leaves may be capped at k_total

@@ -472,10 +472,14 @@ class DeviceQueue:
             _check(lib().sperm_queue_open(buf, ctypes.byref(self.ptr)))
             self.handle = bytes(handle)
         self.scratch = torch.zeros(1, dtype=torch.int64, device="cuda")
+        # claims run on their own stream: a claim does not wait for the caller's queued work (the
+        # rank claims its next chunk while the GPU finishes the current one's last kernels)
+        self.stream = torch.cuda.Stream()
 
     def claim(self, chunk: int, stream=None) -> int:
         start = ctypes.c_int64(0)
-        _check(lib().sperm_queue_claim(self.ptr, int(chunk), _ptr(self.scratch), ctypes.byref(start), _stream(stream)))
+        _check(lib().sperm_queue_claim(self.ptr, int(chunk), _ptr(self.scratch), ctypes.byref(start),
+                                       _stream(stream if stream is not None else self.stream)))
         return start.value
 
     def close(self):
