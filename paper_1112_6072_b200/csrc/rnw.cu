@@ -190,6 +190,7 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   const int lane = threadIdx.x & (W - 1);
   const unsigned SM = seg_mask<W>();  // the segment's lanes: segments branch independently
   const int wib = threadIdx.x / W;
+  cudaTriggerProgrammaticLaunchCompletion();  // the grouping kernel may be scheduled already
   const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / W;
   if (seg - (threadIdx.x & 31) / W >= count) return;  // the whole warp is past the end
   // a segment past the end (W = 16, odd count) repeats the last leaf, writing the same values,
@@ -547,6 +548,7 @@ __global__ void __launch_bounds__(kRnwThreads) rnw_generic_kernel(
     const int2* __restrict__ meta, unsigned long long* __restrict__ queue, uint64_t total_items,
     unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles,
     const int* __restrict__ go) {
+  cudaGridDependencySynchronize();  // a PDL launch: the grouping kernel's writes are visible
   if (go && *go == 0) return;  // a speculative launch whose plan histogram did not match
   using L = GLayout<NP>;
   extern __shared__ int4 smem4[];
@@ -669,6 +671,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     const int2* __restrict__ meta, const int8_t* __restrict__ perm, unsigned long long* __restrict__ queue,
     uint64_t total_items, unsigned long long* __restrict__ leaf_acc, unsigned long long* __restrict__ leaf_cycles,
     const int* __restrict__ go) {
+  cudaGridDependencySynchronize();  // a PDL launch: the grouping kernel's writes are visible
   if (go && *go == 0) return;  // a speculative launch whose plan histogram did not match
   constexpr int B = plan_b(PLAN), GF = plan_gf(PLAN);
   constexpr int NS = B * KS;       // slot rows
@@ -1116,6 +1119,8 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
   __shared__ unsigned long long s_hx[kNumKeys];
   __shared__ int s_wc[kSmallGroupThreads / 32][kNumKeys];  // per-warp key counts, then prefixes
   __shared__ int s_bad;
+  cudaTriggerProgrammaticLaunchCompletion();  // the first plan group may be scheduled already
+  cudaGridDependencySynchronize();             // a PDL launch: prep's meta is complete and visible
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
     s_h[t] = s_hk[t] = 0;
@@ -1216,7 +1221,26 @@ struct Launch {
   cudaStream_t st;
   unsigned long long* leaf_cycles;  // optional per-leaf SM-cycle counters
   const int* go;                    // speculative launch: run only if *go != 0 (else NULL)
+  bool pdl = false;                 // programmatic dependent launch after the previous kernel on st
 };
+
+// cudaLaunchKernelEx with programmatic stream serialization: the kernel's CTAs may start while the
+// previous kernel on the stream finishes; it calls cudaGridDependencySynchronize() before reading
+// what that kernel wrote (a no-op when launched without the attribute).
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 // Non-blocking streams and reusable events for the plan groups, one pool per device (streams
 // and events belong to the device that was current when they were created).  Events are leased
@@ -1324,8 +1348,8 @@ int launch_persistent(K kernel, size_t smem, const Launch& L, uint64_t total, bo
   grid = std::max<uint64_t>(1, std::min(grid, blocks_needed));
   (void)tree;
   count_launch();
-  kernel<<<(unsigned)grid, kRnwThreads, smem, L.st>>>(L.mats, L.n, L.m, L.cbits, L.leaves, L.meta, L.perm,
-                                                        L.queue, total, L.leaf_acc, L.leaf_cycles, L.go);
+  SPERM_CUDA(launch_pdl(kernel, dim3((unsigned)grid), dim3(kRnwThreads), smem, L.st, L.pdl, L.mats, L.n, L.m,
+                        L.cbits, L.leaves, L.meta, L.perm, L.queue, total, L.leaf_acc, L.leaf_cycles, L.go));
   SPERM_LAUNCH_CHECK("rnw kernel");
   return SPERM_OK;
 }
@@ -1428,6 +1452,14 @@ int first_plan() {
 // of p_0 (or p_0 p_1) is evaluated mod p_0 (and p_1) only, whatever min_primes asks (the R-NW
 // block loop then runs one or two Montgomery chains instead of min_primes).  A-B knob:
 // SPERM_LIFT=0 turns it off.
+// Programmatic dependent launch of the grouping kernel after prep and of the first speculative plan
+// group after the grouping (small batches): their CTAs are scheduled while the previous kernel
+// finishes.  A-B knob: SPERM_PDL=0.
+bool pdl_enabled() {
+  const char* e = getenv("SPERM_PDL");
+  return !(e && e[0] == '0');
+}
+
 bool lift_enabled() {
   const char* e = getenv("SPERM_LIFT");
   return !(e && e[0] == '0');
@@ -1777,9 +1809,10 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     SPERM_TRY(cudaGetLastError());
     count_launch();
     if (small_group)
-      rnw_group_small_kernel<<<1, (unsigned)std::min<int64_t>(kSmallGroupThreads, (count + 31) / 32 * 32), 0, st>>>((int)count, d_order, meta, ids + count, hist,
-                                                               hist + kNumKeys, hist_kx, err, spec.hist,
-                                                               speculate ? 1 : 0, go);
+      SPERM_TRY(launch_pdl(rnw_group_small_kernel, dim3(1),
+                           dim3((unsigned)std::min<int64_t>(kSmallGroupThreads, (count + 31) / 32 * 32)), 0, st,
+                           pdl_enabled(), (int)count, d_order, (const int2*)meta, (int32_t*)(ids + count), hist,
+                           hist + kNumKeys, hist_kx, (const int*)err, spec.hist, speculate ? 1 : 0, go));
     else
       rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist,
                                                                        hist + kNumKeys, hist_kx);
@@ -1830,6 +1863,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
       if (gs != st) SPERM_CUDA(cudaStreamWaitEvent(gs, fork, 0));
       Launch L{d_mats, n, 0, 0, sorted + offs[key], hh[key], meta, perm, queue + key, leaf_acc, gs,
                (unsigned long long*)d_leaf_cycles, go};
+      L.pdl = gs == st && go != nullptr && small_group && pdl_enabled();  // right after the grouping kernel
       const int r = launch_key(key, NPg, L);
       if (gs != st) {
         cudaEvent_t join = lease.get();
