@@ -141,8 +141,10 @@ __device__ __forceinline__ int32_t smont(int32_t a, int32_t b, int32_t p, int32_
   const int32_t m = (int32_t)t * pinv;
   return (int32_t)(t >> 32) - __mulhi(m, p);
 }
-// per-leaf metadata: x = k | plan << 8 | nfix_idx << 16 | G << 24, y = Montgomery exponent
-__device__ __forceinline__ int meta_k(int2 m) { return m.x & 0xff; }
+// per-leaf metadata: x = k | err << 4 | plan << 8 | nfix_idx << 16 | G << 24, y = Montgomery
+// exponent; err (prep): bit 0 a row abs sum >= 2^30, bit 1 the bound needs more than max_primes
+__device__ __forceinline__ int meta_k(int2 m) { return m.x & 0xf; }
+__device__ __forceinline__ int meta_err(int2 m) { return (m.x >> 4) & 0x3; }
 __device__ __forceinline__ int meta_plan(int2 m) { return (m.x >> 8) & 0xff; }
 __device__ __forceinline__ int meta_G(int2 m) { return (m.x >> 24) & 0xff; }
 
@@ -334,8 +336,9 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   // symmetric range of one or two primes (2 |coef| bound < p_0 [p_1]) is evaluated mod those alone
   // when `lift` is set, and the finalize lifts its exact value to the residues of min_primes primes
   int k = lift ? 1 : min_primes;
+  int ebits = 0;  // meta_err; also OR-ed into *err when err != NULL (small batches: the grouping kernel)
   if (lane == 0) {
-    if (range_bad) atomicOr(err, 1);
+    if (range_bad) ebits |= 1;
     double lb = zero ? -1.0 : fmin(lr, lc);
     const int64_t cf = coef ? coef[leaf] : 1;
     if (cf == 0) lb = -1.0;
@@ -345,12 +348,14 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
     const int kcap = max_primes > 0 ? max_primes : SPERM_KMAX;
     while (k <= SPERM_KMAX && 30.99999 * k <= need) ++k;
     if (k > kcap) {
-      if (max_primes <= 0) atomicOr(err, 2);
+      if (max_primes <= 0) ebits |= 2;
       k = kcap;
     }
     if (k > 2) k = max(k, min_primes);  // one- and two-prime leaves are lifted
+    if (ebits && err) atomicOr(err, ebits);
+    k |= ebits << 4;
   }
-  k = __shfl_sync(SM, k, 0, W);
+  k = __shfl_sync(SM, k, 0, W);  // k | err << 4: meta.x's low byte
   // ---- tree plans: lane l tests plan l+1 (exact-arithmetic bounds); the first feasible wins
   const int pl = lane + 1;
   bool feasible = false;
@@ -945,6 +950,39 @@ __device__ __forceinline__ uint32_t mod_u64(uint64_t v, uint32_t p, double ip) {
   return (uint32_t)r;
 }
 
+// Residue q of a leaf (Step 4): coef * f[q][mexp] * S_q mod p_q for q < k (S_q = the
+// leaf's accumulated sum mod p_q), and for k <= q < keff the lifted value — a leaf whose exact value
+// fits the symmetric range of p_0 (k = 1) or p_0 p_1 (k = 2) is reconstructed (symmetric residue, or
+// Garner's step) and reduced mod p_q.  `f` = the call's table f[SPERM_KMAX][kMaxMexp]; acc(qq) = S_qq.
+template <typename AccFn>
+__device__ __forceinline__ uint32_t fin_residue(int n, int q, int k, int mexp, int64_t cf, const uint32_t* f,
+                                                AccFn acc) {
+  auto smod = [](int64_t v, uint32_t p, double ip) -> uint32_t {  // signed v mod p in [0, p)
+    const uint32_t r = mod_u64(v < 0 ? 0ull - (uint64_t)v : (uint64_t)v, p, ip);
+    return (v < 0 && r) ? p - r : r;
+  };
+  auto res = [&](int qq, uint32_t pp, double ip) -> uint32_t {
+    const uint32_t v = n == 0 ? 1u : mod_u64((uint64_t)mod_u64(acc(qq), pp, ip) * f[qq * kMaxMexp + mexp], pp, ip);
+    return mod_u64((uint64_t)v * smod(cf, pp, ip), pp, ip);
+  };
+  const uint32_t pq = (uint32_t)c_p[q];
+  const double iq = 1.0 / (double)pq;
+  if (q < k) return res(q, pq, iq);
+  const uint32_t p0 = (uint32_t)c_p[0], p1 = (uint32_t)c_p[1];
+  const double i0 = 1.0 / (double)p0, i1 = 1.0 / (double)p1;
+  const uint32_t r0 = res(0, p0, i0);
+  int64_t V;
+  if (k == 1) {
+    V = r0 > p0 / 2 ? (int64_t)r0 - (int64_t)p0 : (int64_t)r0;
+  } else {
+    const uint32_t r1 = res(1, p1, i1);
+    const uint32_t t = mod_u64((uint64_t)mod_u64((uint64_t)r1 + p1 - mod_u64(r0, p1, i1), p1, i1) * kInvP0ModP1, p1, i1);
+    const uint64_t u = r0 + (uint64_t)p0 * t, m01 = (uint64_t)p0 * p1;  // < p0 p1 < 2^62
+    V = u > m01 / 2 ? (int64_t)u - (int64_t)m01 : (int64_t)u;
+  }
+  return smod(V, pq, iq);
+}
+
 // Leaf residues per = f[q][mexp] S mod p_q, times the leaf coefficient; accumulated into the job
 // rows and the total row.  A grid-stride kernel: 32 leaves per block iteration, each (job, q)
 // run of equal jobs added with one atomic.
@@ -959,15 +997,6 @@ __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
   __shared__ int32_t s_job[kFinThreads / SPERM_KMAX];
   __syncthreads();
   const int q = threadIdx.x % SPERM_KMAX, li = threadIdx.x / SPERM_KMAX;
-  const uint32_t pq = (uint32_t)c_p[q];
-  const double iq = 1.0 / (double)pq;
-  const uint32_t p0 = (uint32_t)c_p[0], p1 = (uint32_t)c_p[1];
-  const double i0 = 1.0 / (double)p0, i1 = 1.0 / (double)p1;
-  // signed v mod p in [0, p)
-  auto smod = [](int64_t v, uint32_t p, double ip) -> uint32_t {
-    const uint32_t r = mod_u64(v < 0 ? 0ull - (uint64_t)v : (uint64_t)v, p, ip);
-    return (v < 0 && r) ? p - r : r;
-  };
   for (int64_t base = (int64_t)blockIdx.x * kFinThreads; base < count * SPERM_KMAX;
        base += (int64_t)gridDim.x * kFinThreads) {
     const int64_t idx = base + threadIdx.x;
@@ -980,33 +1009,9 @@ __global__ void __launch_bounds__(kFinThreads) rnw_finalize_kernel(
       const int keff = max(k, min_primes);
       if (q == 0 && leaf_k) leaf_k[leaf] = keff;
       jb = job ? job[leaf] : 0;
-      const int64_t cf = coef ? coef[leaf] : 1;
-      // coef * f[qq][mexp] * S mod p_qq (S = the leaf's accumulated sum)
-      auto res = [&](int qq, uint32_t pp, double ip) -> uint32_t {
-        const uint32_t v = n == 0 ? 1u
-                                  : mod_u64((uint64_t)mod_u64(leaf_acc[leaf * SPERM_KMAX + qq], pp, ip) * s_f[qq][mt.y],
-                                            pp, ip);
-        return mod_u64((uint64_t)v * smod(cf, pp, ip), pp, ip);
-      };
-      if (q < k) {
-        val = res(q, pq, iq);
-      } else if (q < keff) {
-        // lifted leaf (prep: 2 |coef| * bound < p_0 [p_1]): its exact value V is the symmetric
-        // residue mod p_0, or Garner's combination of the residues mod p_0 and p_1, and V mod p_q
-        // is the residue the leaf contributes here
-        const uint32_t r0 = res(0, p0, i0);
-        int64_t V;
-        if (k == 1) {
-          V = r0 > p0 / 2 ? (int64_t)r0 - (int64_t)p0 : (int64_t)r0;
-        } else {
-          const uint32_t r1 = res(1, p1, i1);
-          const uint32_t t = mod_u64((uint64_t)mod_u64((uint64_t)r1 + p1 - mod_u64(r0, p1, i1), p1, i1) * kInvP0ModP1,
-                                     p1, i1);
-          const uint64_t u = r0 + (uint64_t)p0 * t, m01 = (uint64_t)p0 * p1;  // < p0 p1 < 2^62
-          V = u > m01 / 2 ? (int64_t)u - (int64_t)m01 : (int64_t)u;
-        }
-        val = smod(V, pq, iq);
-      }
+      if (q < keff)
+        val = fin_residue(n, q, k, mt.y, coef ? coef[leaf] : 1, &s_f[0][0],
+                          [&](int qq) { return (uint64_t)leaf_acc[leaf * SPERM_KMAX + qq]; });
       if (leaf_res) leaf_res[idx] = (uint32_t)val;
     }
     if (job_acc) {
@@ -1114,19 +1119,24 @@ constexpr int kSmallGroupThreads = 1024;
 __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
     int count, const int32_t* __restrict__ order, const int2* __restrict__ meta, int32_t* __restrict__ sorted,
     int* __restrict__ hist, int* __restrict__ hist_k, unsigned long long* __restrict__ hist_kx,
-    const int* __restrict__ err, KeyHist pred, int spec, int* __restrict__ go) {
+    int* __restrict__ err, unsigned long long* __restrict__ queue, KeyHist pred, int spec, int* __restrict__ go) {
   __shared__ int s_h[kNumKeys], s_hk[kNumKeys], s_cur[kNumKeys];
   __shared__ unsigned long long s_hx[kNumKeys];
   __shared__ int s_wc[kSmallGroupThreads / 32][kNumKeys];  // per-warp key counts, then prefixes
-  __shared__ int s_bad;
+  __shared__ int s_bad, s_err;
   cudaTriggerProgrammaticLaunchCompletion();  // the first plan group may be scheduled already
   cudaGridDependencySynchronize();             // a PDL launch: prep's meta is complete and visible
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // small batches skip the workspace memset: this kernel writes every word the plan groups and
+  // the host read (histograms, the groups' work counters, err from the leaves' meta_err, go)
   for (int t = threadIdx.x; t < kNumKeys; t += blockDim.x) {
     s_h[t] = s_hk[t] = 0;
     s_hx[t] = 0;
+    queue[t] = 0;
   }
+  if (threadIdx.x == 0) s_err = 0;
   __syncthreads();
+  int eb = 0;
   for (int base = 0; base < count; base += blockDim.x) {
     const int i = base + threadIdx.x;
     const bool live = i < count;
@@ -1137,6 +1147,7 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
       key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
       kk = meta_k(mt);
       y = mt.y;
+      eb |= meta_err(mt);
     }
     const unsigned same = __match_any_sync(0xffffffffu, key);
     const int c1 = __popc(same), ck = __reduce_add_sync(same, (unsigned)kk),
@@ -1147,6 +1158,8 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
       atomicAdd(&s_hx[key], (unsigned long long)(unsigned)cx);
     }
   }
+  eb = __reduce_or_sync(0xffffffffu, eb);
+  if (lane == 0 && eb) atomicOr(&s_err, eb);
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of the key counts: 4 keys per lane, then a warp scan
     int c[4], tot = 0;
@@ -1168,7 +1181,10 @@ __global__ void __launch_bounds__(kSmallGroupThreads) rnw_group_small_kernel(
       if (k < kNumKeys) s_cur[k] = off;
       off += c[u];
     }
-    if (lane == 0) s_bad = *err;
+    if (lane == 0) {
+      s_bad = s_err;
+      *err = s_err;
+    }
   }
   for (int base = 0; base < count; base += blockDim.x) {
     for (int t = threadIdx.x; t < nwarps * kNumKeys; t += blockDim.x) s_wc[t / kNumKeys][t % kNumKeys] = 0;
@@ -1745,7 +1761,8 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
   const size_t small_bytes = sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * 2 * kNumKeys;
   SPERM_TRY(cudaMallocAsync((void**)&small, small_bytes, st));
-  SPERM_TRY(cudaMemsetAsync(small, 0, small_bytes, st));
+  const bool small_group = count <= kSmallGroup;
+  if (!small_group) SPERM_TRY(cudaMemsetAsync(small, 0, small_bytes, st));  // (small: the grouping kernel)
   // per-group work counters after the histograms (8-byte aligned: 4 + 2*48 ints = 400 bytes)
   unsigned long long* queue = reinterpret_cast<unsigned long long*>(small + 4 + 2 * kNumKeys);
   unsigned long long* hist_kx = queue + kNumKeys;
@@ -1769,8 +1786,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   const bool speculate = spec_on && n > 0 && spec.dev == dev && spec.n == n && spec.count == count &&
                          spec.NPg == NPg && spec.minp == min_primes && spec.maxp == max_primes &&
                          spec.plan0 == first_plan();
-  int* go = small;  // small[0]: zeroed above
-  const bool small_group = count <= kSmallGroup;
+  int* go = small;  // small[0]: zeroed above / written by the grouping kernel
   {
     TimingScope ts("rnw_prep", st);
     // one 16-lane segment per leaf for n <= 16 (two leaves per warp), else one warp
@@ -1781,7 +1797,12 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     const int W = (n <= 16 && prep16) ? 16 : 32;
     const int64_t threads = count * W;
     count_launch();
-    const size_t prep_smem = (size_t)(256 / W) * n * (n + 1) * sizeof(int32_t);  // padded rows per segment
+    // CTA width: 256 threads, narrowed (down to one warp) while the grid would cover fewer than two
+    // CTAs per SM — a small batch (configs[1]: 256 leaves = 32 CTAs of 256) otherwise runs on a
+    // fifth of the SMs, its warps sharing their SMs' issue slots (ncu: 10 of 11.7 us)
+    int prep_threads = 256;
+    while (prep_threads > 32 && (threads + prep_threads - 1) / prep_threads < 2 * (int64_t)sm_count()) prep_threads >>= 1;
+    const size_t prep_smem = (size_t)(prep_threads / W) * n * (n + 1) * sizeof(int32_t);  // padded rows per segment
     const int per_lane = (n * n + W - 1) / W;
     auto prep = n > 32 ? rnw_prep_kernel<unsigned long long, 16, 32>
               : W == 16 ? (per_lane <= 8 ? rnw_prep_kernel<uint32_t, 8, 16> : rnw_prep_kernel<uint32_t, 16, 16>)
@@ -1803,16 +1824,16 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
         prep_attr.fetch_or(bit);
       }
     }
-    prep<<<(unsigned)((threads + 255) / 256), 256, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
+    prep<<<(unsigned)((threads + prep_threads - 1) / prep_threads), prep_threads, prep_smem, st>>>(d_mats, n, NPg, count, d_coef, min_primes, max_primes,
                                                                        lift_enabled() ? 1 : 0, first_plan(), meta,
-                                                                       perm, err, leaf_acc);
+                                                                       perm, small_group ? nullptr : err, leaf_acc);
     SPERM_TRY(cudaGetLastError());
     count_launch();
     if (small_group)
       SPERM_TRY(launch_pdl(rnw_group_small_kernel, dim3(1),
                            dim3((unsigned)std::min<int64_t>(kSmallGroupThreads, (count + 31) / 32 * 32)), 0, st,
                            pdl_enabled(), (int)count, d_order, (const int2*)meta, (int32_t*)(ids + count), hist,
-                           hist + kNumKeys, hist_kx, (const int*)err, spec.hist, speculate ? 1 : 0, go));
+                           hist + kNumKeys, hist_kx, err, queue, spec.hist, speculate ? 1 : 0, go));
     else
       rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist,
                                                                        hist + kNumKeys, hist_kx);
