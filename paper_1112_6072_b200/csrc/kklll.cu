@@ -325,6 +325,120 @@ __global__ void __launch_bounds__(NT) kklll_smem_kernel(const int32_t* __restric
   }
 }
 
+// ---------------------------------------------------------------------------- warp kernel
+// One WARP per trial for orders n <= 32, B row-major in shared memory (row stride 33 double2: a
+// lane-per-column row access and a lane-per-row column access are both bank-conflict-free).
+// Lane j owns column j in the row operations (exchange, update) and row j in the column
+// operations (pivot search, multipliers), so a step needs no CTA barrier, only __syncwarp:
+//   pivot: lane i reads b_ik, |b_ik|^2, two REDUX maxima over the bit pattern (non-negative
+//          doubles order like their bits) and a ballot give the first maximal row p;
+//   exchange rows k, p in columns >= k (physically, as the oracle does);
+//   multipliers l_i of the rows with a nonzero b_ik (correctly rounded quotients, div_by) go to
+//   shared memory; the rows are then visited in turn (warp-uniform bit loop over their ballot),
+//   each lane updating its column if its pivot-row entry u_j is nonzero.
+// Rows with b_ik = 0 and columns with u_j = 0 are skipped (b - l u = b up to the sign of a zero,
+// see above), every other operation is the oracle's on the same entry in the same order: X is
+// bit-identical.  Each warp takes a contiguous range of (job, trial) items, so the job's column
+// supports (a 32-bit row mask per lane) are rebuilt only when the job changes; a trial's B is
+// zero-filled and its nonzeros drawn by iterating the lane's mask.
+constexpr int kWarpNS = 33;
+__global__ void __launch_bounds__(32) kklll_warp_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
+                                                        const int32_t* __restrict__ ids, int trials, uint64_t seed,
+                                                        double* __restrict__ xout) {
+  extern __shared__ double2 wsm2[];  // b[n][33] | lv[32]
+  double2* b = wsm2;
+  double2* lv = wsm2 + n * kWarpNS;
+  const int lane = threadIdx.x;
+  const unsigned FULL = 0xffffffffu;
+  const double S32 = 0.8660254037844386;
+  const int64_t items = count * (int64_t)trials;
+  const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+  int64_t item = (int64_t)blockIdx.x * per;
+  const int64_t end = item + per < items ? item + per : items;
+  if (item >= end) return;
+  int64_t job = item / trials;
+  int trial = (int)(item - job * trials);
+  int64_t cur_job = -1;
+  uint32_t colmask = 0;  // rows with a nonzero in column `lane` of the job's pattern
+  uint64_t jid = 0;
+  for (; item < end; ++item) {
+    if (job != cur_job) {
+      const int32_t* a = mats + job * (int64_t)n * n;
+      colmask = 0;
+      for (int i = 0; i < n; ++i)
+        if (lane < n && a[i * n + lane] != 0) colmask |= 1u << i;
+      jid = (uint64_t)(ids ? ids[job] : job);
+      cur_job = job;
+    }
+    const uint64_t key = trial_key(seed, jid, (uint64_t)trial);
+    __syncwarp();  // the previous trial is done with b
+    for (int i = 0; i < n; ++i) b[i * kWarpNS + lane] = make_double2(0.0, 0.0);
+    for (uint32_t mk = colmask; mk; mk &= mk - 1) {
+      const int i = __ffs(mk) - 1;
+      const int ri = root_index(key, (uint64_t)i, (uint64_t)lane);
+      b[i * kWarpNS + lane] = make_double2(ri == 0 ? 1.0 : -0.5, ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32));
+    }
+    __syncwarp();
+    double x = 1.0;
+    for (int k = 0; k < n; ++k) {
+      const bool inr = lane >= k && lane < n;
+      double2 v = make_double2(0.0, 0.0);
+      if (inr) v = b[lane * kWarpNS + k];
+      const double mg = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(mg);
+      const unsigned hi = inr ? (unsigned)(bits >> 32) : 0u;
+      const unsigned mh = __reduce_max_sync(FULL, hi);
+      const bool c1 = inr && hi == mh;
+      const unsigned lo = c1 ? (unsigned)bits : 0u;
+      const unsigned ml = __reduce_max_sync(FULL, lo);
+      const unsigned win = __ballot_sync(FULL, c1 && lo == ml);
+      const int p = __ffs(win) - 1;  // first maximal row (lane k is always in range: win != 0)
+      const double d = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+      if (d == 0.0) { x = 0.0; break; }  // warp-uniform
+      x = __dmul_rn(x, d);
+      if (k + 1 == n) break;
+      double2 u = make_double2(0.0, 0.0);  // my column's entry of the pivot row (after the exchange)
+      if (p != k) {
+        if (inr) {
+          const double2 t0 = b[k * kWarpNS + lane];
+          u = b[p * kWarpNS + lane];
+          b[k * kWarpNS + lane] = u;
+          b[p * kWarpNS + lane] = t0;
+        }
+        __syncwarp();
+      } else if (inr) {
+        u = b[k * kWarpNS + lane];
+      }
+      const double2 pk = b[k * kWarpNS + k];  // broadcast
+      const double y = __drcp_rn(d);
+      const bool d_ok = div_range_ok(d);
+      const bool below = lane > k && lane < n;
+      double2 vi = make_double2(0.0, 0.0);
+      if (below) vi = b[lane * kWarpNS + k];
+      const bool nzr = vi.x != 0.0 || vi.y != 0.0;
+      const unsigned rows = __ballot_sync(FULL, nzr);
+      if (nzr)
+        lv[lane] = make_double2(div_by(__dadd_rn(__dmul_rn(vi.x, pk.x), __dmul_rn(vi.y, pk.y)), d, y, d_ok),
+                                div_by(__dsub_rn(__dmul_rn(vi.y, pk.x), __dmul_rn(vi.x, pk.y)), d, y, d_ok));
+      __syncwarp();
+      const bool unz = below && (u.x != 0.0 || u.y != 0.0);
+      for (unsigned r = rows; r; r &= r - 1) {
+        const int i = __ffs(r) - 1;
+        const double2 l = lv[i];
+        if (unz) {
+          double2 w = b[i * kWarpNS + lane];
+          w.x = __dsub_rn(w.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
+          w.y = __dsub_rn(w.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
+          b[i * kWarpNS + lane] = w;
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) xout[item] = x;
+    if (++trial == trials) { trial = 0; ++job; }
+  }
+}
+
 // ---------------------------------------------------------------------------- frontal kernel
 // One WARP per trial for the sparse job matrices (round 2).  Partial pivoting keeps the fill of a
 // sparse matrix near the diagonal, so at step k only a FRONT of rows (not yet eliminated, first
@@ -602,7 +716,29 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     const char* e = getenv("SPERM_KKLLL_SMEM_MIN");  // measured crossover: n = 23 register kernel
     return e ? atoi(e) : 28;                          // 76 vs 267 ms, 27: 170 vs 163, 32: 115 vs 80
   }();
-  if (n <= 32 && n < smem_min) {
+  static const int warp_min = [] {  // A-B knob: smallest order for the warp-per-trial kernel (n <= 32)
+    const char* e = getenv("SPERM_KKLLL_WARP_MIN");
+    return e ? atoi(e) : 28;
+  }();
+  if (n <= 32 && n >= warp_min) {
+    const size_t wsmem = sizeof(double2) * ((size_t)n * kWarpNS + 32);
+    static std::atomic<unsigned> wattr{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(wattr.load() & (1u << (dev & 31)))) {
+      SPERM_CUDA(cudaFuncSetAttribute(kklll_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(double2) * (32 * kWarpNS + 32))));
+      wattr.fetch_or(1u << (dev & 31));
+    }
+    int per_sm = 0;
+    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kklll_warp_kernel, 32, wsmem));
+    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
+    grid = std::max<int64_t>(1, std::min(grid, items));
+    TimingScope ts("kklll", st);
+    count_launch();
+    kklll_warp_kernel<<<(unsigned)grid, 32, wsmem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
+    SPERM_LAUNCH_CHECK("kklll_warp_kernel");
+  } else if (n <= 32 && n < smem_min) {
     const int NC = n <= 8 ? 8 : n <= 16 ? 16 : n <= 24 ? 24 : 32;
     auto kern = NC == 8 ? kklll_reg_kernel<8> : NC == 16 ? kklll_reg_kernel<16> : NC == 24 ? kklll_reg_kernel<24>
                                                                                           : kklll_reg_kernel<32>;

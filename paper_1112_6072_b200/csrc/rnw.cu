@@ -111,6 +111,20 @@ constexpr int kMaxLow = 8;  // low columns picked per leaf
 #ifndef SPERM_RNW_EFORM  // E_c = Q_c^0 - Q_c^1 evaluation: 0 products of sums, 1 / 2 multiply-add form
 #define SPERM_RNW_EFORM 2  // (configs[1] kernel 0.147 / 0.147 / 0.144 ms)
 #endif
+// Grouped block loop: the lane's blocks are run in groups of SPERM_RNW_GROUP consecutive blocks
+// (a power of two; 0 = the plain loop, unrolled kBlockUnroll times where registers allow).  Inside
+// a group the flipped high column, the sign bit and (mostly) the flip direction are compile-time
+// constants.  Measured (B200): configs[1] kernel 0.1336 -> 0.123 ms/step, C100 order-15 leaves 19.5
+// -> 17.0 ms per 4M (with the per-leaf setup loops rolled; see there), order-16 17.0 -> 14.4 ms, C60
+// order-32 leaves 76 -> 66 ms.  Groups of 8 spill in the 3-CTA variants (order-15: 17.5 ms), of 2
+// save less (18.0 ms).  SPERM_RNW_GROUP_FENCE: a compiler fence between the blocks of a group keeps
+// ptxas from hoisting the next blocks' loads (without it: spills, configs[1] 0.133 ms).
+#ifndef SPERM_RNW_GROUP
+#define SPERM_RNW_GROUP 4
+#endif
+#ifndef SPERM_RNW_GROUP_FENCE
+#define SPERM_RNW_GROUP_FENCE 1
+#endif
 constexpr int kEForm = SPERM_RNW_EFORM;
 static_assert(SPERM_RNW_EFORM == 0 || KS == 3, "multiply-add E form is written for 3 slot rows");
 constexpr bool kSparseW = SPERM_RNW_SPARSE_W != 0;
@@ -685,7 +699,10 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
   constexpr int NGF = NFIX / GF;   // exact fixed-row groups
   // block-loop unroll: kBlockUnroll where registers allow (2-CTA builds with <= 28 register rows,
   // B <= 7; the others spill when unrolled)
-  constexpr int UNR = (tree_warps(B, NFIX, GF) < 24 && NRT <= 28 && B <= 7) ? kBlockUnroll : 1;
+  constexpr bool kUnr = tree_warps(B, NFIX, GF) < 24 && NRT <= 28 && B <= 7;
+  // GRP: blocks per group of the grouped block loop (0: the plain loop, unrolled UNR times)
+  constexpr int GRP = SPERM_RNW_GROUP;
+  constexpr int UNR = (kUnr && GRP == 0) ? kBlockUnroll : 1;
   extern __shared__ int4 smem4[];
   const int lane = threadIdx.x & 31;
   const TreeSmem L = tree_smem(NRT, NS, n, B);
@@ -713,6 +730,9 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
       const int32_t* a = mats + leaf * (int64_t)n * n;
       const int8_t* pr = perm + leaf * kPermW;
       const int8_t* pc = pr + kPermRows;
+      // (per-leaf setup loops are kept rolled: the hot code of a small-leaf launch — setup, one or
+      // two block-loop instantiations, the reduction — has to fit the 32 KB L1.5 instruction cache)
+#pragma unroll 1
       for (int e = lane; e < L.nh * S4; e += 32) {
         const int h = e / S4, r = e - (e / S4) * S4;
         const int row = r < NRT ? pr[r] : -1;
@@ -721,16 +741,19 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         sm[L.neg + e] = -v;
       }
       const int nw = pc[n - 1];
+#pragma unroll 1
       for (int r = lane; r < S4; r += 32) {
         const int row = r < NRT ? pr[r] : -1;
         int32_t w0 = 1;
         if (row >= 0) {
           int32_t s = 0;
+#pragma unroll 1
           for (int j = 0; j < n; ++j) s += a[row * n + j];
           w0 = 2 * a[row * n + nw] - s;
         }
         sm[L.w0 + r] = w0;
       }
+#pragma unroll 1
       for (int s = lane; s < NS; s += 32) {
         const int row = pr[s];
         sm[L.delta + s] = row >= 0 ? 2 * a[row * n + pc[s / KS]] : 0;
@@ -755,10 +778,15 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     for (int r = 0; r < S4; ++r) W[r] = sm[L.w0 + r];
     {
       const uint64_t g0 = t0 ^ (t0 >> 1);
+#pragma unroll 1
       for (int h = max(m - 1 - B, 0); h < L.nh; ++h)
         if ((g0 >> (B + h)) & 1ull) {
+          const int4* col = reinterpret_cast<const int4*>(sm + L.pos + h * S4);
 #pragma unroll
-          for (int r = 0; r < S4; ++r) W[r] += sm[L.pos + h * S4 + r];
+          for (int v = 0; v < S4 / 4; ++v) {
+            const int4 d = col[v];
+            W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
+          }
         }
     }
     int32_t D[NS];
@@ -788,26 +816,21 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
     auto blocks = [&](auto kc, auto emc) {
       constexpr int K = decltype(kc)::value;
       constexpr int EM = decltype(emc)::value;
-#pragma unroll UNR
-      for (uint32_t ob = 0; ob < nblk; ++ob) {
-        uint32_t mk = 0xffffffffu;
-        const uint32_t gb = ob | ext;  // the block's low Gray-relevant bits (see ext)
-        if (ob) {  // flip high Gray bit B + hh (warp-uniform column): only the touched row groups
-          const int hh = __ffs(ob) - 1;
-          mk = (uint32_t)sm[L.mask + hh];
-          const bool add = !((gb >> (hh + 1)) & 1u);
-          const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
+      // flip high Gray bit B + hh (warp-uniform column): add or subtract its doubled column
+      auto flip = [&](int hh, bool add, uint32_t mk) {
+        const int4* col = reinterpret_cast<const int4*>(sm + (add ? L.pos : L.neg) + hh * S4);
 #pragma unroll
-          for (int v = 0; v < S4 / 4; ++v) {
-            if (!(kSparseW) || (mk & (1u << v))) {
-              const int4 d = col[v];
-              W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
-            }
+        for (int v = 0; v < S4 / 4; ++v) {
+          if (!(kSparseW) || (mk & (1u << v))) {
+            const int4 d = col[v];
+            W[4 * v] += d.x; W[4 * v + 1] += d.y; W[4 * v + 2] += d.z; W[4 * v + 3] += d.w;
           }
         }
-        // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1); exact products
-        // of pairs and quads of the E_c (used when the leaf's E mode says they fit int32;
-        // wrapped otherwise and then unused)
+      };
+      // the block's sum over its 2^B low-bit patterns: prod_c (Q_c^0 - Q_c^1); exact products
+      // of pairs and quads of the E_c (used when the leaf's E mode says they fit int32;
+      // wrapped otherwise and then unused); `odd` = bit 0 of the block's high Gray index
+      auto eval = [&](bool odd, uint32_t mk) {
         int32_t P2[NP2], P4[NP4];
 #pragma unroll
         for (int c = 0; c < B; ++c) {
@@ -852,7 +875,7 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         }
         // the sign (-1)^{|high Gray bits|} rides on the first factor (prime-independent): the
         // Montgomery chain then yields a residue of the signed block value, congruent mod p
-        const int32_t f0 = ((gb & 1u) ^ (kEForm != 0 && (B & 1))) ? -FG[0] : FG[0];
+        const int32_t f0 = (odd ^ (kEForm != 0 && (B & 1))) ? -FG[0] : FG[0];
         // per prime: P_F's chain, then the exact E groups of the leaf's mode
         auto chain = [&](auto gsz, const int32_t* grp) {
           constexpr int NGR = decltype(gsz)::value;
@@ -874,12 +897,48 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         else if (emode == 2) chain(std::integral_constant<int, NP4>{}, P4);  // EM < 0: per block
         else if (emode == 1) chain(std::integral_constant<int, NP2>{}, P2);
         else chain(std::integral_constant<int, B>{}, E);
+      };
+      if (GRP > 1 && nblk >= (uint32_t)GRP) {
+        // groups of GRP consecutive blocks ob = o + i, i < GRP (GRP a power of two, o a multiple
+        // of it): for i > 0 the flipped column hh = ctz(i) and the block's sign bit i & 1 are
+        // compile-time constants (shared-memory loads with immediate offsets, no select on the
+        // sign), and so is the flip direction, bit hh + 1 of ob | ext, except for i = GRP / 2
+        // (and i = 0), where it is a bit of o | ext.  nblk >= GRP >= 2 puts ext at bit >= 1.
+        constexpr int LG = GRP >= 8 ? 3 : GRP >= 4 ? 2 : 1;
+        for (uint32_t o = 0; o < nblk; o += GRP) {
+          const uint32_t go_ = o | ext;
+          if (o) {
+            const int hh = __ffs(o) - 1;
+            flip(hh, !((go_ >> (hh + 1)) & 1u), 0xffffffffu);
+          }
+          eval(false, 0xffffffffu);
+#pragma unroll
+          for (int i = 1; i < (GRP > 1 ? GRP : 1); ++i) {
+            const int hh = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3;  // ctz(i), i < 16
+            const bool add = (hh + 1 < LG) ? !((i >> (hh + 1)) & 1) : !((go_ >> LG) & 1u);
+            if (SPERM_RNW_GROUP_FENCE) asm volatile("" ::: "memory");  // keep the blocks in order
+            flip(hh, add, 0xffffffffu);
+            eval((i & 1) != 0, 0xffffffffu);
+          }
+        }
+      } else {
+#pragma unroll UNR
+        for (uint32_t ob = 0; ob < nblk; ++ob) {
+          uint32_t mk = 0xffffffffu;
+          const uint32_t gb = ob | ext;  // the block's low Gray-relevant bits (see ext)
+          if (ob) {  // only the touched row groups (sparse variants)
+            const int hh = __ffs(ob) - 1;
+            if (kSparseW || kSparseE) mk = (uint32_t)sm[L.mask + hh];
+            flip(hh, !((gb >> (hh + 1)) & 1u), mk);
+          }
+          eval((gb & 1u) != 0, mk);
+        }
       }
     };
     // (the mode-specialised loops triple the code; only the unrolled 2-CTA variants (<= 28 register
     // rows) get them — specialised, several 3-CTA and wide variants spilled)
     auto by_mode = [&](auto kc) {
-      if constexpr (UNR > 1 || NRT <= SPERM_RNW_EMODE_NRT) {  // unrolled 2-CTA variants, small plans
+      if constexpr (kUnr || NRT <= SPERM_RNW_EMODE_NRT) {  // unrolled 2-CTA variants, small plans
         if (emode == 2) blocks(kc, std::integral_constant<int, 2>{});  // warp-uniform per leaf
         else if (emode == 1) blocks(kc, std::integral_constant<int, 1>{});
         else blocks(kc, std::integral_constant<int, 0>{});
@@ -903,8 +962,13 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
         int64_t v = acc[q];
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) {
-          int64_t r = v % c_p[q];
-          if (r < 0) r += c_p[q];
+          // v mod p without a 64-bit division: |v| < 32 lanes x 2^14 blocks x 2^31 = 2^50 is exact
+          // in fp64, the rounded quotient is off by at most one
+          const int32_t p = prime_p(q);
+          int64_t r = v - (int64_t)p * __double2ll_rn((double)v * (1.0 / (double)p));
+          if (r < 0) r += p;
+          if (r < 0) r += p;
+          if (r >= p) r -= p;
           atomicAdd(leaf_acc + leaf * SPERM_KMAX + q, (unsigned long long)r);
         }
       }
@@ -1049,8 +1113,13 @@ __global__ void fold_mod_kernel(unsigned long long* __restrict__ acc, int64_t ro
 
 // evaluation-order leaf ids, their plan keys, and per key: leaves, sum of k (primes) and sum
 // of k * mexp (Montgomery products per block value, summed over primes: the op model's input)
+// The sort key is the plan key with a 4-bit sub-key below it (SPERM_RNW_SUBKEY): the leaf's prime
+// class (k = 1, 2, 3, more) and its exact-E mode, i.e. the block-loop instantiation it runs, so
+// that the warps of a persistent grid, which take leaves in sorted order, sit in the same loop
+// copy at the same time (instruction-cache footprint); the caller's order holds within a sub-key.
 __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order, const int2* __restrict__ meta,
-                                uint8_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist,
+                                const int8_t* __restrict__ perm, int subkey,
+                                uint16_t* __restrict__ keys, int32_t* __restrict__ ids, int* __restrict__ hist,
                                 int* __restrict__ hist_k, unsigned long long* __restrict__ hist_kx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int key = 0;
@@ -1060,7 +1129,10 @@ __global__ void rnw_keys_kernel(int64_t count, const int32_t* __restrict__ order
     mt = meta[leaf];
     const int plan = meta_plan(mt);
     key = plan == 0 ? 0 : plan * 8 + ((mt.x >> 16) & 0xff);
-    keys[i] = (uint8_t)key;
+    int sub = 0;
+    if (subkey && plan != 0)
+      sub = ((min(meta_k(mt), 4) - 1) << 2) | (perm[(int64_t)leaf * kPermW + kPermGend] & 3);
+    keys[i] = (uint16_t)((key << 4) | sub);
     ids[i] = leaf;
   }
   // block histogram in shared memory (32-bit: <= 256 leaves x 8 x 47 per bin), warp-aggregated
@@ -1416,6 +1488,14 @@ template <int PLAN>
 int launch_tree_nfix(int fi, const Launch& L) {
   switch (fi) {
     case 0: return launch_tree<nfix_of(0), PLAN>(L);
+#ifdef SPERM_DEV_SUBSET  // quick ptxas checks of a few variants (never a product build)
+    default: return SPERM_ERR_ARG;
+  }
+}
+template <int PLAN>
+int launch_tree_nfix_unused(int fi, const Launch& L) {
+  switch (fi) {
+#endif
     case 1: return launch_tree<nfix_of(1), PLAN>(L);
     case 2: return launch_tree<nfix_of(2), PLAN>(L);
     case 3: return launch_tree<nfix_of(3), PLAN>(L);
@@ -1439,11 +1519,20 @@ int launch_key(int key, int NPg, const Launch& L) {
   }
   const int plan = key / 8, fi = key % 8;
   switch (plan) {
-    case 1: return launch_tree_nfix<1>(fi, L);
     case 2: return launch_tree_nfix<2>(fi, L);
+    case 5: return launch_tree_nfix<5>(fi, L);
+#ifdef SPERM_DEV_SUBSET
+    default: return SPERM_ERR_ARG;
+  }
+}
+template <int DUMMY>
+int launch_key_unused(int key, int NPg, const Launch& L) {
+  const int plan = key / 8, fi = key % 8;
+  switch (plan) {
+#endif
+    case 1: return launch_tree_nfix<1>(fi, L);
     case 3: return launch_tree_nfix<3>(fi, L);
     case 4: return launch_tree_nfix<4>(fi, L);
-    case 5: return launch_tree_nfix<5>(fi, L);
     case 6: return launch_tree_nfix<6>(fi, L);
     case 7: return launch_tree_nfix<7>(fi, L);
     case 8: return launch_tree_nfix<8>(fi, L);
@@ -1479,6 +1568,14 @@ bool pdl_enabled() {
 bool lift_enabled() {
   const char* e = getenv("SPERM_LIFT");
   return !(e && e[0] == '0');
+}
+
+bool subkey_enabled() {  // A-B knob SPERM_RNW_SUBKEY=1 (measured: order-15 leaves 17.04 -> 16.95 ms
+  static const bool on = [] {  // per 4M, within noise of the extra sort pass; off by default)
+    const char* e = getenv("SPERM_RNW_SUBKEY");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 // f[q][y] = (-1)^(n-1) 2^(1-n) (2^32)^y mod p_q (exact uint64 arithmetic on the host)
@@ -1736,7 +1833,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   int2* meta = nullptr;
   unsigned long long* leaf_acc = nullptr;
   int8_t* perm = nullptr;
-  uint8_t* keys = nullptr;
+  uint16_t* keys = nullptr;
   int32_t* ids = nullptr;
   int* small = nullptr;  // [2] err, [4..) hist, hist_k, then u64 queue[keys], hist_kx[keys]
   void* sort_tmp = nullptr;
@@ -1757,7 +1854,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
   SPERM_TRY(cudaMallocAsync((void**)&meta, sizeof(int2) * count, st));
   SPERM_TRY(cudaMallocAsync((void**)&leaf_acc, sizeof(unsigned long long) * count * SPERM_KMAX, st));
   SPERM_TRY(cudaMallocAsync((void**)&perm, (size_t)kPermW * count, st));
-  SPERM_TRY(cudaMallocAsync((void**)&keys, 2 * (size_t)count, st));
+  SPERM_TRY(cudaMallocAsync((void**)&keys, 2 * sizeof(uint16_t) * (size_t)count, st));
   SPERM_TRY(cudaMallocAsync((void**)&ids, sizeof(int32_t) * 2 * count, st));
   const size_t small_bytes = sizeof(int) * (4 + 2 * kNumKeys) + sizeof(unsigned long long) * 2 * kNumKeys;
   SPERM_TRY(cudaMallocAsync((void**)&small, small_bytes, st));
@@ -1835,20 +1932,20 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
                            pdl_enabled(), (int)count, d_order, (const int2*)meta, (int32_t*)(ids + count), hist,
                            hist + kNumKeys, hist_kx, err, queue, spec.hist, speculate ? 1 : 0, go));
     else
-      rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, keys, ids, hist,
-                                                                       hist + kNumKeys, hist_kx);
+      rnw_keys_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(count, d_order, meta, perm, subkey_enabled() ? 1 : 0,
+                                                                       keys, ids, hist, hist + kNumKeys, hist_kx);
     SPERM_TRY(cudaGetLastError());
   }
-  // leaves grouped by plan key, evaluation order kept inside each group (stable radix sort on
-  // the 7-bit keys), queued before the histogram read-back so that the host's only work after
+  // leaves grouped by plan key (and loop-instantiation sub-key), evaluation order kept inside each
+  // group (stable radix sort on the 11-bit keys), queued before the histogram read-back so that the host's only work after
   // the synchronization is launching the plan groups
   const int32_t* sorted = ids + count;
   if (!small_group) {
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 7, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + count, ids, ids + count, (int)count, 0, 11, st);
     SPERM_TRY(cudaMallocAsync(&sort_tmp, tmp_bytes, st));
     SPERM_TRY(cub::DeviceRadixSort::SortPairs(sort_tmp, tmp_bytes, keys, keys + count, ids, ids + count,
-                                              (int)count, 0, 7, st));
+                                              (int)count, 0, 11, st));
   }
   // one read-back of the whole small block (err, histograms, queues, kx) into a per-thread
   // pinned buffer (a pageable copy is staged and slower), marked by a per-thread event
