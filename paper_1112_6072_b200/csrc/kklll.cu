@@ -422,14 +422,29 @@ __global__ void __launch_bounds__(32) kklll_warp_kernel(const int32_t* __restric
                                 div_by(__dsub_rn(__dmul_rn(vi.y, pk.x), __dmul_rn(vi.x, pk.y)), d, y, d_ok));
       __syncwarp();
       const bool unz = below && (u.x != 0.0 || u.y != 0.0);
-      for (unsigned r = rows; r; r &= r - 1) {
-        const int i = __ffs(r) - 1;
-        const double2 l = lv[i];
+      // four rows per pass (independent load -> multiply -> subtract -> store chains in flight)
+      for (unsigned r = rows; r;) {
+        int ri[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ri[q] = __ffs(r) - 1;  // -1 once the rows run out (warp-uniform)
+          r &= r - 1;
+        }
         if (unz) {
-          double2 w = b[i * kWarpNS + lane];
-          w.x = __dsub_rn(w.x, __dsub_rn(__dmul_rn(l.x, u.x), __dmul_rn(l.y, u.y)));
-          w.y = __dsub_rn(w.y, __dadd_rn(__dmul_rn(l.x, u.y), __dmul_rn(l.y, u.x)));
-          b[i * kWarpNS + lane] = w;
+          double2 l[4], w[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ri[q] >= 0) {
+              l[q] = lv[ri[q]];
+              w[q] = b[ri[q] * kWarpNS + lane];
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (ri[q] >= 0) {
+              w[q].x = __dsub_rn(w[q].x, __dsub_rn(__dmul_rn(l[q].x, u.x), __dmul_rn(l[q].y, u.y)));
+              w[q].y = __dsub_rn(w[q].y, __dadd_rn(__dmul_rn(l[q].x, u.y), __dmul_rn(l[q].y, u.x)));
+              b[ri[q] * kWarpNS + lane] = w[q];
+            }
         }
       }
       __syncwarp();
@@ -716,7 +731,9 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     const char* e = getenv("SPERM_KKLLL_SMEM_MIN");  // measured crossover: n = 23 register kernel
     return e ? atoi(e) : 28;                          // 76 vs 267 ms, 27: 170 vs 163, 32: 115 vs 80
   }();
-  static const int warp_min = [] {  // A-B knob: smallest order for the warp-per-trial kernel (n <= 32)
+  // smallest order for the warp-per-trial kernel (n <= 32); read per call so tests can route every
+  // order through it (measured, C60 jobs of order 32: 16.9 ms vs 32.1 ms for the 64-thread CTA kernel)
+  const int warp_min = [] {
     const char* e = getenv("SPERM_KKLLL_WARP_MIN");
     return e ? atoi(e) : 28;
   }();

@@ -329,7 +329,7 @@ def test_kklll_bit_exact_trials():
 
 @pytest.mark.parametrize("n", [25, 26, 27, 28, 29, 30, 31, 32, 33, 36, 39, 47, 64, 65, 77, 96, 100, 112])
 def test_kklll_bit_exact_large_orders(n):
-    """Register kernel (n < 28, SPERM_KKLLL_SMEM_MIN) and shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
+    """Register kernel (n < 28, SPERM_KKLLL_SMEM_MIN), warp-per-trial kernel (28 <= n <= 32) and shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
     threads), 128 (n < 48) and 256 threads (SPERM_KKLLL_T64_MAX / _T128_MAX move the bounds):
     every trial bit-identical to the oracle, including singular (zero) trials (24 trials:
     ~1e4-1e5 multiplier quotients per order through the reciprocal-based division)."""
@@ -343,6 +343,37 @@ def test_kklll_bit_exact_large_orders(n):
         ref = [kklll_trial(mats[j], 3, j, t) for t in range(24)]
         assert np.array_equal(xs[j], np.array(ref)), (n, j)
     assert (xs[1] == 0).all()
+
+
+def test_kklll_warp_kernel_every_order(monkeypatch):
+    """The warp-per-trial kernel (default for 28 <= n <= 32) forced for every order 1..32
+    (SPERM_KKLLL_WARP_MIN=1): every trial bit-identical to the oracle — sparse job-like patterns,
+    a denser pattern (many rows per elimination step: several passes of the 4-row update), a zero
+    column (singular in every trial) and C60 job matrices of order 32 with their job ids."""
+    monkeypatch.setenv("SPERM_KKLLL_WARP_MIN", "1")
+    for n in list(range(1, 33)):
+        rng = np.random.default_rng(100 + n)
+        mats = (rng.random((3, n, n)) < min(1.0, 3.5 / n)).astype(np.int64)
+        mats[2] = (rng.random((n, n)) < 0.6).astype(np.int64)
+        mats[:, np.arange(n), np.arange(n)] = 1
+        if n > 1:
+            mats[1, :, n // 2] = 0
+        T = 6 if n > 8 else 12
+        est, xs = P.sperm_estimate(dev(mats), trials=T, seed=21, keep_trials=True)
+        xs = xs.cpu().numpy()
+        for j in range(3):
+            ref = [kklll_trial(mats[j], 21, j, t) for t in range(T)]
+            assert np.array_equal(xs[j], np.array(ref)), (n, j)
+        if n > 1:
+            assert (xs[1] == 0).all()
+    jobs = pre_expand(truncated_icosahedron(), jobs_at_least=992)
+    mats = np.array([to_dense(m, k) for _, m, k in jobs[:3]], dtype=np.int64)
+    assert mats.shape[1] == 32
+    ids = [7, 1000, 3]
+    est, xs = P.sperm_estimate(dev(mats), trials=5, seed=9, keep_trials=True, ids=dev(ids))
+    xs = xs.cpu().numpy()
+    for j in range(3):
+        assert np.array_equal(xs[j], np.array([kklll_trial(mats[j], 9, ids[j], t) for t in range(5)])), j
 
 
 def test_kklll_frontal_bit_exact_on_job_matrices():
