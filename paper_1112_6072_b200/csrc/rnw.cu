@@ -1488,14 +1488,6 @@ template <int PLAN>
 int launch_tree_nfix(int fi, const Launch& L) {
   switch (fi) {
     case 0: return launch_tree<nfix_of(0), PLAN>(L);
-#ifdef SPERM_DEV_SUBSET  // quick ptxas checks of a few variants (never a product build)
-    default: return SPERM_ERR_ARG;
-  }
-}
-template <int PLAN>
-int launch_tree_nfix_unused(int fi, const Launch& L) {
-  switch (fi) {
-#endif
     case 1: return launch_tree<nfix_of(1), PLAN>(L);
     case 2: return launch_tree<nfix_of(2), PLAN>(L);
     case 3: return launch_tree<nfix_of(3), PLAN>(L);
@@ -1504,6 +1496,76 @@ int launch_tree_nfix_unused(int fi, const Launch& L) {
     default: return launch_tree<nfix_of(6), PLAN>(L);
   }
 }
+
+}  // namespace
+
+// Build parts.  The 84 tree-kernel variants (each with its block loops per prime count and E mode)
+// dominate the compile time of this file, so the build compiles it several times in parallel with
+// -DSPERM_RNW_PART=p: part 0 holds the C ABI, the host code and every other kernel, parts 1..3 only
+// instantiate the tree variants of the plans they own and export one launcher each
+// (rnw_tree_part<p>); without the macro (tools/build_variant.py, single object) everything is
+// instantiated here.  The launch record crosses the parts as an opaque pointer: every part compiles
+// the same `Launch` definition.
+#ifndef SPERM_RNW_PART
+#define SPERM_RNW_PART -1
+#endif
+constexpr int kRnwPart = SPERM_RNW_PART;
+__host__ __device__ constexpr int plan_part(int plan) {  // owner of a plan's variants
+  return plan == 1 || plan == 2 || plan == 9 ? 1 : plan == 3 || plan == 4 || plan == 10 ? 2
+       : plan >= 5 && plan <= 8 ? 3 : 0;
+}
+int rnw_tree_part1(int plan, int fi, const void* launch);
+int rnw_tree_part2(int plan, int fi, const void* launch);
+int rnw_tree_part3(int plan, int fi, const void* launch);
+
+namespace {
+
+template <int PLAN>
+int tree_dispatch(int fi, const Launch& L) {
+  constexpr int owner = plan_part(PLAN);
+  if constexpr (kRnwPart < 0 || kRnwPart == owner) return launch_tree_nfix<PLAN>(fi, L);
+  else if constexpr (owner == 1) return rnw_tree_part1(PLAN, fi, &L);
+  else if constexpr (owner == 2) return rnw_tree_part2(PLAN, fi, &L);
+  else if constexpr (owner == 3) return rnw_tree_part3(PLAN, fi, &L);
+  else return set_error(SPERM_ERR_ARG, "sperm_permanent: plan owned by build part 0");
+}
+
+int launch_tree_plan(int plan, int fi, const Launch& L) {
+  switch (plan) {
+    case 1: return tree_dispatch<1>(fi, L);
+    case 2: return tree_dispatch<2>(fi, L);
+    case 3: return tree_dispatch<3>(fi, L);
+    case 4: return tree_dispatch<4>(fi, L);
+    case 5: return tree_dispatch<5>(fi, L);
+    case 6: return tree_dispatch<6>(fi, L);
+    case 7: return tree_dispatch<7>(fi, L);
+    case 8: return tree_dispatch<8>(fi, L);
+    case 9: return tree_dispatch<9>(fi, L);
+    case 10: return tree_dispatch<10>(fi, L);
+    case 11: return tree_dispatch<11>(fi, L);
+    case 12: return tree_dispatch<12>(fi, L);
+    default: return set_error(SPERM_ERR_ARG, "sperm_permanent: bad plan key");
+  }
+}
+
+}  // namespace
+
+#if SPERM_RNW_PART == 1
+int rnw_tree_part1(int plan, int fi, const void* launch) {
+  return launch_tree_plan(plan, fi, *static_cast<const Launch*>(launch));
+}
+#elif SPERM_RNW_PART == 2
+int rnw_tree_part2(int plan, int fi, const void* launch) {
+  return launch_tree_plan(plan, fi, *static_cast<const Launch*>(launch));
+}
+#elif SPERM_RNW_PART == 3
+int rnw_tree_part3(int plan, int fi, const void* launch) {
+  return launch_tree_plan(plan, fi, *static_cast<const Launch*>(launch));
+}
+#endif
+
+#if SPERM_RNW_PART <= 0  // the rest of the file: part 0 (or the single-object build) only
+namespace {
 
 int launch_key(int key, int NPg, const Launch& L) {
   if (key == 0) {
@@ -1517,31 +1579,7 @@ int launch_key(int key, int NPg, const Launch& L) {
       default: return set_error(SPERM_ERR_ARG, "sperm_permanent: unsupported order");
     }
   }
-  const int plan = key / 8, fi = key % 8;
-  switch (plan) {
-    case 2: return launch_tree_nfix<2>(fi, L);
-    case 5: return launch_tree_nfix<5>(fi, L);
-#ifdef SPERM_DEV_SUBSET
-    default: return SPERM_ERR_ARG;
-  }
-}
-template <int DUMMY>
-int launch_key_unused(int key, int NPg, const Launch& L) {
-  const int plan = key / 8, fi = key % 8;
-  switch (plan) {
-#endif
-    case 1: return launch_tree_nfix<1>(fi, L);
-    case 3: return launch_tree_nfix<3>(fi, L);
-    case 4: return launch_tree_nfix<4>(fi, L);
-    case 6: return launch_tree_nfix<6>(fi, L);
-    case 7: return launch_tree_nfix<7>(fi, L);
-    case 8: return launch_tree_nfix<8>(fi, L);
-    case 9: return launch_tree_nfix<9>(fi, L);
-    case 10: return launch_tree_nfix<10>(fi, L);
-    case 11: return launch_tree_nfix<11>(fi, L);
-    case 12: return launch_tree_nfix<12>(fi, L);
-    default: return set_error(SPERM_ERR_ARG, "sperm_permanent: bad plan key");
-  }
+  return launch_tree_plan(key / 8, key % 8, L);
 }
 
 // First tree plan the prep pass may choose (0 = generic kernel only).  Testing / A-B
@@ -2131,3 +2169,7 @@ extern "C" int sperm_permanent_host(const int32_t* h_mats, int n, int64_t count,
   if (rc == SPERM_OK && e != cudaSuccess) rc = cuda_check(e, "sperm_permanent_host: synchronize");
   return rc;
 }
+
+#else  // parts 1..3 end here
+}  // namespace sperm
+#endif  // SPERM_RNW_PART <= 0

@@ -1,4 +1,5 @@
-"""Build an A-B variant of libsperm.so with extra nvcc flags (measurements only).
+"""Build an A-B variant of libsperm.so with extra nvcc flags (measurements only); csrc/rnw.cu is
+compiled as one object here (no -DSPERM_RNW_PART: every tree variant in one unit, ~4 min).
 
     python tools/build_variant.py NAME -DSPERM_RNW_SPARSE_E=1 ...
     SPERM_LIB=paper_1112_6072_b200/variants/libsperm_NAME.so python bench.py ...
