@@ -118,7 +118,8 @@ constexpr int kMaxLow = 8;  // low columns picked per leaf
 // -> 17.0 ms per 4M (with the per-leaf setup loops rolled; see there), order-16 17.0 -> 14.4 ms, C60
 // order-32 leaves 76 -> 66 ms.  Groups of 8 spill in the 3-CTA variants (order-15: 17.5 ms), of 2
 // save less (18.0 ms).  SPERM_RNW_GROUP_FENCE: a compiler fence between the blocks of a group keeps
-// ptxas from hoisting the next blocks' loads (without it: spills, configs[1] 0.133 ms).
+// ptxas from hoisting the next blocks' loads (without it: spills, configs[1] 0.133 ms; = 2, a
+// fence between pairs of blocks only: no measurable difference).
 #ifndef SPERM_RNW_GROUP
 #define SPERM_RNW_GROUP 4
 #endif
@@ -922,7 +923,8 @@ __global__ void __launch_bounds__(kRnwThreads, tree_min_blocks(plan_b(PLAN), NFI
           for (int i = 1; i < (GRP > 1 ? GRP : 1); ++i) {
             const int hh = (i & 1) ? 0 : (i & 2) ? 1 : (i & 4) ? 2 : 3;  // ctz(i), i < 16
             const bool add = (hh + 1 < LG) ? !((i >> (hh + 1)) & 1) : !((go_ >> LG) & 1u);
-            if (SPERM_RNW_GROUP_FENCE) asm volatile("" ::: "memory");  // keep the blocks in order
+            // keep the blocks in order (FENCE = 2: only between pairs of blocks)
+            if (SPERM_RNW_GROUP_FENCE == 1 || (SPERM_RNW_GROUP_FENCE == 2 && !(i & 1))) asm volatile("" ::: "memory");
             flip(hh, add, 0xffffffffu);
             eval((i & 1) != 0, 0xffffffffu);
           }

@@ -1,5 +1,4 @@
-"""Build an A-B variant of libsperm.so with extra nvcc flags (measurements only); csrc/rnw.cu is
-compiled as one object here (no -DSPERM_RNW_PART: every tree variant in one unit, ~4 min).
+"""Build an A-B variant of libsperm.so with extra nvcc flags (measurements only).
 
     python tools/build_variant.py NAME -DSPERM_RNW_SPARSE_E=1 ...
     SPERM_LIB=paper_1112_6072_b200/variants/libsperm_NAME.so python bench.py ...
@@ -18,15 +17,16 @@ def main():
     name, flags = sys.argv[1], sys.argv[2:]
     out = os.path.join(B.HERE, "variants")
     os.makedirs(out, exist_ok=True)
-    srcs = sorted(f for f in os.listdir(B.CSRC) if f.endswith(".cu"))
+    units = B._units()  # csrc/rnw.cu in its build parts, like the main build
 
-    def comp(f):
-        o = os.path.join(out, f"{name}_{f[:-3]}.o")
-        subprocess.check_call([B.NVCC, *B.ARCH, *B.FLAGS, *flags, "-c", os.path.join(B.CSRC, f), "-o", o],
+    def comp(unit):
+        src, stem, extra = unit
+        o = os.path.join(out, f"{name}_{stem}.o")
+        subprocess.check_call([B.NVCC, *B.ARCH, *B.FLAGS, *extra, *flags, "-c", src, "-o", o],
                               stderr=subprocess.DEVNULL)
         return o
-    with ThreadPoolExecutor(len(srcs)) as ex:
-        objs = list(ex.map(comp, srcs))
+    with ThreadPoolExecutor(len(units)) as ex:
+        objs = list(ex.map(comp, units))
     lib = os.path.join(out, f"libsperm_{name}.so")
     subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-cudart", "shared", "-o", lib, *objs,
                            "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
