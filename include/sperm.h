@@ -102,7 +102,10 @@ int sperm_bound_primes(const int32_t* h_mat, int n, int* h_k);
  *             (stable grouping; improved Step 3: the pipeline
  *             expands a rank's jobs in non-increasing-estimate order, so the
  *             natural leaf order already follows it).  Must be a permutation
- *             of 0..count-1.
+ *             of 0..count-1.  (Measurement knob SPERM_RNW_SUBKEY=1: batches of
+ *             more than 4096 leaves are ordered, inside a group, by prime class
+ *             and exact-E mode first and by this order within those; off by
+ *             default.)
  *  d_job      [count] int32 job id of each leaf (device) or NULL (every leaf
  *             belongs to job 0, so d_job_acc[0] accumulates the total).
  *  num_jobs   size of d_job_acc's first dimension (>= 1 when d_job_acc is set).
