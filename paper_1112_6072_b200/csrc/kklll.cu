@@ -470,6 +470,10 @@ __global__ void __launch_bounds__(32) kklll_warp_kernel(const int32_t* __restric
 // have more than kNzRow nonzeros) is flagged and re-run by the CTA kernel above.
 constexpr int kFrR = 24;    // front rows (lanes 0..23)
 constexpr int kFrC = 64;    // window columns (circular, power of two)
+#ifndef SPERM_KKLLL_FRONT_STRIDE  // row stride of the front in double2: 65 spreads the rows of one
+#define SPERM_KKLLL_FRONT_STRIDE 65  // column over the banks (at 64 every row of a column shares them)
+#endif
+constexpr int kFrS = SPERM_KKLLL_FRONT_STRIDE;
 constexpr int kNzRow = 12;  // original nonzeros per row in the row table
 constexpr int kRowTab = 2 + kNzRow;
 
@@ -501,10 +505,10 @@ __global__ void kklll_rowtab_kernel(const int32_t* __restrict__ mats, int n, int
 __global__ void __launch_bounds__(32) kklll_front_kernel(int n, int64_t count, const int32_t* __restrict__ ids,
                                                            int trials, uint64_t seed, const int8_t* __restrict__ tab,
                                                            double* __restrict__ xout, int* __restrict__ over) {
-  // F[kFrR][kFrC] | rowAt[128] posOf[128] | the current job's row table [n][kRowTab] (int8)
+  // F[kFrR][kFrS] | rowAt[128] posOf[128] | the current job's row table [n][kRowTab] (int8)
   extern __shared__ double2 fsm[];
   double2* F = fsm;
-  int8_t* rowAt = reinterpret_cast<int8_t*>(fsm + kFrR * kFrC);
+  int8_t* rowAt = reinterpret_cast<int8_t*>(fsm + kFrR * kFrS);
   int8_t* posOf = rowAt + 128;
   int8_t* rts = posOf + 128;
   const int lane = threadIdx.x;
@@ -534,7 +538,7 @@ __global__ void __launch_bounds__(32) kklll_front_kernel(int n, int64_t count, c
     // the lane's front row: original index (-1: free slot) and current position
     int myrow = -1, mypos = 0;
     unsigned freem = (1u << kFrR) - 1u;  // free slots (warp-uniform)
-    double2* my = F + min(lane, kFrR - 1) * kFrC;  // lanes >= kFrR never own a row (reads only)
+    double2* my = F + min(lane, kFrR - 1) * kFrS;  // lanes >= kFrR never own a row (reads only)
     int E = -1;         // window right edge
     bool fail = false;  // front or window overflow
     // the lane's row over window columns lo..hi: zeros, then its original nonzeros (Step 1 of KKLLL:
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(32) kklll_front_kernel(int n, int64_t count, c
       x = __dmul_rn(x, d);
       if (k + 1 == n) break;
       const int prow = __shfl_sync(0xffffffffu, myrow, ps);
-      const double2* pr = F + ps * kFrC;
+      const double2* pr = F + ps * kFrS;
       // the pivot row's last nonzero: an original nonzero right of the window extends it
       {
         const int8_t* r = rts + prow * kRowTab;
@@ -819,7 +823,7 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
       count_launch();
       kklll_rowtab_kernel<<<(unsigned)((count * 32 + 127) / 128), 128, 0, st>>>(d_mats, n, count, tab, over);
       SPERM_LAUNCH_CHECK("kklll_rowtab_kernel");
-      const size_t fsmem = sizeof(double2) * kFrR * kFrC + 256 + (size_t)kKNmax * kRowTab;
+      const size_t fsmem = sizeof(double2) * kFrR * kFrS + 256 + (size_t)kKNmax * kRowTab;
       static std::atomic<unsigned> attr_done{0};
       int dev = 0;
       cudaGetDevice(&dev);
