@@ -217,7 +217,9 @@ __global__ void rnw_prep_kernel(const int32_t* __restrict__ mats, int n, int NPg
   // stage the leaf in shared memory with coalesced loads; the per-lane row/column scans
   // below then read shared memory (one segment per leaf, 256 / W segments per CTA)
   extern __shared__ int32_t prep_sm[];
-  const int ns = n + 1;  // padded row stride: the row scans a[i*ns + j] hit distinct banks
+  // odd row stride: the lane-per-row scans a[i*ns + j] hit distinct banks (n + 1 is even for odd n:
+  // at n = 15 the 16 lanes of a segment shared two banks; C100 order-15 prep 5.36 -> see DESIGN)
+  const int ns = n | 1;
   int32_t* sa = prep_sm + wib * (n * ns);
   {
     // every load of a batch is issued before its stores (U = the smallest of 4, 8, 12, 16 words
@@ -1945,7 +1947,7 @@ extern "C" int sperm_permanent(const int32_t* d_mats, int n, int64_t count, cons
     // fifth of the SMs, its warps sharing their SMs' issue slots (ncu: 10 of 11.7 us)
     int prep_threads = 256;
     while (prep_threads > 32 && (threads + prep_threads - 1) / prep_threads < 2 * (int64_t)sm_count()) prep_threads >>= 1;
-    const size_t prep_smem = (size_t)(prep_threads / W) * n * (n + 1) * sizeof(int32_t);  // padded rows per segment
+    const size_t prep_smem = (size_t)(prep_threads / W) * n * (n | 1) * sizeof(int32_t);  // odd row stride per segment
     const int per_lane = (n * n + W - 1) / W;
     auto prep = n > 32 ? rnw_prep_kernel<unsigned long long, 16, 32>
               : W == 16 ? (per_lane <= 8 ? rnw_prep_kernel<uint32_t, 8, 16> : rnw_prep_kernel<uint32_t, 16, 16>)
