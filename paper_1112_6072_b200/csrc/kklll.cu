@@ -1,8 +1,9 @@
 // kklll.cu — Algorithm KKLLL: approximate permanents used as the
 // job weights of the improved Step 3.
 //
-// Per (job, trial): n < 28 one warp with B in registers (kklll_reg_kernel), else one CTA with
-// B in shared memory (kklll_smem_kernel).
+// Per (job, trial): n <= 32 one warp with B in shared memory (kklll_warp_kernel), n >= 48 one warp
+// over the front of the sparse job matrix (kklll_front_kernel), else one CTA with B in shared
+// memory (kklll_smem_kernel, also the frontal kernel's fallback).
 //   Step 1: B_ij = 0 where a_ij = 0, else the cube root of unity w_r, r = root_index(
 //           trial_key(seed, id, trial), i, j)  (counter-based SplitMix64; K1)
 //   Step 2: X = |det B|^2 by LU with partial pivoting (first maximal |b_ik|^2), every real
@@ -57,105 +58,6 @@ __device__ __forceinline__ double div_by(double a, double d, double y, bool d_ok
   return __fma_rn(r, y, q0);
 }
 
-
-// Register variant for n <= NC <= 32: lane i holds row i of B (re/im in registers, every
-// index static because the elimination loop is fully unrolled).  Rows are never moved: each
-// lane tracks its row's current position, so "swap rows k and p" is a position exchange and
-// the pivot tie-break "first maximal |b_ik|^2" compares positions — the same arithmetic, in
-// the same order, as the shared-memory kernel and the reference.  The pivot row is
-// broadcast through shared memory (one 16-byte broadcast load per column).
-template <int NC>
-__global__ void __launch_bounds__(128) kklll_reg_kernel(const int32_t* __restrict__ mats, int n, int64_t count,
-                                                        const int32_t* __restrict__ ids, int trials, uint64_t seed,
-                                                        double* __restrict__ xout) {
-  __shared__ double2 prow_all[8][NC];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  double2* prow = prow_all[wib];
-  const int wpb = blockDim.x >> 5;
-  const double S32 = 0.8660254037844386;
-  const int64_t items = count * (int64_t)trials;
-  for (int64_t item = (int64_t)blockIdx.x * wpb + wib; item < items; item += (int64_t)gridDim.x * wpb) {
-    const int64_t job = item / trials;
-    const int trial = (int)(item % trials);
-    const int32_t* a = mats + job * (int64_t)n * n;
-    const uint64_t key = trial_key(seed, (uint64_t)(ids ? ids[job] : job), (uint64_t)trial);
-    // Step 1: the lane's row of B.  Only the row's nonzeros draw a root (one round per
-    // nonzero, warp-uniform trip count), then land in their static register slot.
-    uint32_t nzmask = 0;
-    if (lane < n) {
-#pragma unroll
-      for (int j = 0; j < NC; ++j)
-        if (j < n && a[lane * n + j] != 0) nzmask |= 1u << j;
-    }
-    double re[NC], im[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) re[j] = im[j] = 0.0;
-    while (__any_sync(0xffffffffu, nzmask != 0)) {
-      const int jn = nzmask ? __ffs(nzmask) - 1 : -1;
-      nzmask &= nzmask - 1;
-      double r = 0.0, s = 0.0;
-      if (jn >= 0) {
-        const int ri = root_index(key, (uint64_t)lane, (uint64_t)jn);
-        r = ri == 0 ? 1.0 : -0.5;
-        s = ri == 0 ? 0.0 : (ri == 1 ? S32 : -S32);
-      }
-#pragma unroll
-      for (int j = 0; j < NC; ++j)
-        if (j == jn) { re[j] = r; im[j] = s; }
-    }
-    int pos = lane;
-    bool active = lane < n;
-    double x = 1.0;
-    bool done = false;
-#pragma unroll NC
-    for (int k = 0; k < NC; ++k) {
-      if (done || k >= n) continue;
-      // pivot: maximal |b_ik|^2 over active rows, first (lowest position) on ties.  A
-      // non-negative double orders like its bit pattern, so warp max = two 32-bit REDUX.
-      const double mag = active ? __dadd_rn(__dmul_rn(re[k], re[k]), __dmul_rn(im[k], im[k])) : 0.0;
-      const unsigned mh = active ? (unsigned)__double2hiint(mag) : 0u;
-      const unsigned ml = active ? (unsigned)__double2loint(mag) : 0u;
-      const unsigned bh = __reduce_max_sync(0xffffffffu, mh);
-      const bool c1 = active && mh == bh;
-      const unsigned bl_ = __reduce_max_sync(0xffffffffu, c1 ? ml : 0u);
-      const bool c2 = c1 && ml == bl_;
-      const int bp = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)pos : 0xffffffffu);
-      const int bl = __ffs(__ballot_sync(0xffffffffu, c2 && pos == bp)) - 1;
-      const double d = __hiloint2double((int)bh, (int)bl_);
-      if (d == 0.0) { x = 0.0; done = true; continue; }
-      if (lane == bl) pos = k;
-      else if (active && pos == k) pos = bp;
-      x = __dmul_rn(x, d);
-      if (k + 1 == n) { done = true; continue; }
-      if (lane == bl) {
-#pragma unroll
-        for (int j = 0; j < NC; ++j)
-          if (j >= k) prow[j] = make_double2(re[j], im[j]);
-      }
-      __syncwarp();
-      active = active && pos > k;
-      if (active) {
-        const double2 pk = prow[k];
-        const double xr = re[k], xi = im[k];
-        const double y = __drcp_rn(d);
-        const bool d_ok = div_range_ok(d);
-        const double lr = div_by(__dadd_rn(__dmul_rn(xr, pk.x), __dmul_rn(xi, pk.y)), d, y, d_ok);
-        const double li = div_by(__dsub_rn(__dmul_rn(xi, pk.x), __dmul_rn(xr, pk.y)), d, y, d_ok);
-#pragma unroll
-        for (int j = 1; j < NC; ++j) {  // j > k (static trip count keeps re/im in registers)
-          if (j <= k) continue;
-          const double2 u = prow[j];
-          if (u.x == 0.0 && u.y == 0.0) continue;  // sparse pivot row: see kklll_smem_kernel
-          re[j] = __dsub_rn(re[j], __dsub_rn(__dmul_rn(lr, u.x), __dmul_rn(li, u.y)));
-          im[j] = __dsub_rn(im[j], __dadd_rn(__dmul_rn(lr, u.y), __dmul_rn(li, u.x)));
-        }
-      }
-      __syncwarp();
-    }
-    if (lane == 0) xout[item] = x;
-  }
-}
 
 // Shared-memory-resident variant for 32 < n <= 112: one 256-thread CTA per trial, B row-major
 // in shared memory (16-byte complex entries), several trials (CTAs) per SM so one trial's
@@ -731,15 +633,14 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
   double* xs = d_trials_out;
   if (!xs) SPERM_CUDA(cudaMallocAsync((void**)&xs, sizeof(double) * count * trials, st));
   const int64_t items = count * (int64_t)trials;
-  static const int smem_min = [] {  // A-B knob: smallest order for the shared-memory kernel
-    const char* e = getenv("SPERM_KKLLL_SMEM_MIN");  // measured crossover: n = 23 register kernel
-    return e ? atoi(e) : 28;                          // 76 vs 267 ms, 27: 170 vs 163, 32: 115 vs 80
-  }();
-  // smallest order for the warp-per-trial kernel (n <= 32); read per call so tests can route every
-  // order through it (measured, C60 jobs of order 32: 16.9 ms vs 32.1 ms for the 64-thread CTA kernel)
+  // orders warp_min..32 take the warp-per-trial kernel, the rest the CTA / frontal kernels (A-B knob
+  // SPERM_KKLLL_WARP_MIN, read per call; measured: C60 jobs of order 32 16.9 ms vs 32.1 ms for the
+  // 64-thread CTA kernel; 2000 3-regular matrices x n^2 trials at n = 12 / 16 / 20 / 24 / 27: 0.89 /
+  // 2.2 / 4.8 / 8.9 / 14.7 ms vs 1.6 / 3.3 / 11.1 / 16.9 / 58.2 ms for the register-resident kernel
+  // of earlier versions, which it replaced)
   const int warp_min = [] {
     const char* e = getenv("SPERM_KKLLL_WARP_MIN");
-    return e ? atoi(e) : 28;
+    return e ? atoi(e) : 1;
   }();
   if (n <= 32 && n >= warp_min) {
     const size_t wsmem = sizeof(double2) * ((size_t)n * kWarpNS + 32);
@@ -759,17 +660,6 @@ extern "C" int sperm_estimate(const int32_t* d_mats, int n, int64_t count, const
     count_launch();
     kklll_warp_kernel<<<(unsigned)grid, 32, wsmem, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
     SPERM_LAUNCH_CHECK("kklll_warp_kernel");
-  } else if (n <= 32 && n < smem_min) {
-    const int NC = n <= 8 ? 8 : n <= 16 ? 16 : n <= 24 ? 24 : 32;
-    auto kern = NC == 8 ? kklll_reg_kernel<8> : NC == 16 ? kklll_reg_kernel<16> : NC == 24 ? kklll_reg_kernel<24>
-                                                                                          : kklll_reg_kernel<32>;
-    int per_sm = 0;
-    SPERM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0));
-    int64_t grid = (int64_t)sm_count() * std::max(per_sm, 1);
-    grid = std::max<int64_t>(1, std::min(grid, (items + 3) / 4));
-    TimingScope ts("kklll", st);
-    count_launch();
-    kern<<<(unsigned)grid, 128, 0, st>>>(d_mats, n, count, d_ids, trials, seed, xs);
   } else {
     // shared-memory-resident LU, one CTA per trial (smem_kernel on jobs [j0, j0 + cnt) of the
     // given matrices / ids, trials written to out)

@@ -329,7 +329,7 @@ def test_kklll_bit_exact_trials():
 
 @pytest.mark.parametrize("n", [25, 26, 27, 28, 29, 30, 31, 32, 33, 36, 39, 47, 64, 65, 77, 96, 100, 112])
 def test_kklll_bit_exact_large_orders(n):
-    """Register kernel (n < 28, SPERM_KKLLL_SMEM_MIN), warp-per-trial kernel (28 <= n <= 32) and shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
+    """Warp-per-trial kernel (n <= 32) and shared-memory kernel with 64 (n < 40; n >= 34 has more trailing columns than update
     threads), 128 (n < 48) and 256 threads (SPERM_KKLLL_T64_MAX / _T128_MAX move the bounds):
     every trial bit-identical to the oracle, including singular (zero) trials (24 trials:
     ~1e4-1e5 multiplier quotients per order through the reciprocal-based division)."""
@@ -346,8 +346,8 @@ def test_kklll_bit_exact_large_orders(n):
 
 
 def test_kklll_warp_kernel_every_order(monkeypatch):
-    """The warp-per-trial kernel (default for 28 <= n <= 32) forced for every order 1..32
-    (SPERM_KKLLL_WARP_MIN=1): every trial bit-identical to the oracle — sparse job-like patterns,
+    """The warp-per-trial kernel on every order 1..32 (its default range; SPERM_KKLLL_WARP_MIN=1
+    pins it): every trial bit-identical to the oracle — sparse job-like patterns,
     a denser pattern (many rows per elimination step: several passes of the 4-row update), a zero
     column (singular in every trial) and C60 job matrices of order 32 with their job ids."""
     monkeypatch.setenv("SPERM_KKLLL_WARP_MIN", "1")
@@ -374,6 +374,20 @@ def test_kklll_warp_kernel_every_order(monkeypatch):
     xs = xs.cpu().numpy()
     for j in range(3):
         assert np.array_equal(xs[j], np.array([kklll_trial(mats[j], 9, ids[j], t) for t in range(5)])), j
+
+
+def test_kklll_cta_kernel_small_orders(monkeypatch):
+    """SPERM_KKLLL_WARP_MIN=33 (the A-B knob) sends orders <= 32 to the CTA shared-memory kernel
+    instead of the warp kernel: the same bit-identical trials."""
+    monkeypatch.setenv("SPERM_KKLLL_WARP_MIN", "33")
+    for n in (2, 5, 16, 24, 30, 32):
+        rng = np.random.default_rng(300 + n)
+        mats = (rng.random((2, n, n)) < min(1.0, 3.5 / n)).astype(np.int64)
+        mats[:, np.arange(n), np.arange(n)] = 1
+        est, xs = P.sperm_estimate(dev(mats), trials=6, seed=4, keep_trials=True)
+        xs = xs.cpu().numpy()
+        for j in range(2):
+            assert np.array_equal(xs[j], np.array([kklll_trial(mats[j], 4, j, t) for t in range(6)])), (n, j)
 
 
 def test_kklll_frontal_bit_exact_on_job_matrices():
