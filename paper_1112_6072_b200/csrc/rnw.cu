@@ -1618,12 +1618,9 @@ bool lift_enabled() {
   return !(e && e[0] == '0');
 }
 
-bool subkey_enabled() {  // A-B knob SPERM_RNW_SUBKEY=1 (measured: order-15 leaves 17.04 -> 16.95 ms
-  static const bool on = [] {  // per 4M, within noise of the extra sort pass; off by default)
-    const char* e = getenv("SPERM_RNW_SUBKEY");
-    return e && e[0] == '1';
-  }();
-  return on;
+bool subkey_enabled() {  // A-B knob SPERM_RNW_SUBKEY=1, read per call (measured: order-15 leaves 17.04 ->
+  const char* e = getenv("SPERM_RNW_SUBKEY");  // 16.95 ms per 4M, within noise of the extra sort
+  return e && e[0] == '1';                     // pass; off by default; tested)
 }
 
 // f[q][y] = (-1)^(n-1) 2^(1-n) (2^32)^y mod p_q (exact uint64 arithmetic on the host)

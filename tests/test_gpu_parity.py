@@ -698,6 +698,23 @@ def test_crt_device_matches_host():
     assert got == want and got[0] == 0 and any(v < 0 for v in got)
 
 
+def test_rnw_subkey_sort_large_batch(monkeypatch):
+    """SPERM_RNW_SUBKEY=1 (measurement knob): a batch above the small-batch limit is ordered inside
+    each plan group by prime class and exact-E mode; residues and prime counts are those of the
+    default order, and sampled values equal the oracle's."""
+    mats = np.concatenate([random_3perm_batch(2600, 12, seed=41), random_3perm_batch(2600, 12, seed=42)])
+    mats[2600:] *= np.random.default_rng(3).integers(1, 60, size=(2600, 12, 12))
+    d = dev(mats)
+    res0, k0 = P.sperm_permanent(d, min_primes=1)
+    monkeypatch.setenv("SPERM_RNW_SUBKEY", "1")
+    res1, k1 = P.sperm_permanent(d, min_primes=1)
+    assert np.array_equal(k0.cpu().numpy(), k1.cpu().numpy()) and np.array_equal(res0.cpu().numpy(), res1.cpu().numpy())
+    assert len(set(k1.cpu().tolist())) > 1  # several prime classes in the batch
+    got = P.residues_to_ints(res1, k1)
+    for j in (0, 17, 2599, 2600, 4000, 5199):
+        assert got[j] == per_ryser_nw_gray(mats[j]), j
+
+
 def test_rnw_prime_count_bregman_and_cap():
     """0/1 leaves size their prime count by Bregman-Minc (configs[1] 0/1 half: 1 prime);
     max_primes caps it, leaving every residue correct modulo the primes kept."""
